@@ -1,0 +1,345 @@
+#!/usr/bin/env python
+"""Benchmark of the VSP hot path on B200: bootstrapped gates/s.
+
+Workload (BASELINE.json configs[0]): one batch of G=4096 independent random NAND/XOR
+gates bootstrapped at the paper's TFHE parameters with n=630 (tfhe-80 copy with
+n=630, N=1024, l=2, Bg=2^10).  One "step" = one pass of the hot path over the batch
+(linear combination -> blind rotation -> sample extract -> identity key switch).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--gates G]
+
+Multi-GPU (launched by torchrun): every rank bootstraps its own independent batch
+(weak scaling; gates of one netlist level shard with no data-path exchange), value =
+all gates / max-over-ranks device time.
+
+Prints ONE JSON line (rank 0).  `value` is device-timed with CUDA events with inputs
+resident in HBM and L2 flushed between steps; `e2e` is the same metric through the
+C-ABI host entry point (vsp_hom_gate_batch) with pinned host buffers and the
+H2D/D2H copies inside the timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "bootstrapped_gates_per_sec"
+UNIT = "gates/s"
+# Algorithmic work per external product and per level-1 bootstrap:
+# F_EP = (2l+2)*5*M*log2(M) + 2l*2*8*M with M = 512, l = 2.
+F_EP = (2 * 2 + 2) * 5 * 512 * 9 + 2 * 2 * 2 * 8 * 512
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--gates", type=int, default=4096)
+    ap.add_argument("--n", type=int, default=630, help="LWE dimension (630 = BASELINE config)")
+    ap.add_argument("--cpu-sample", type=int, default=0,
+                    help="gates per CPU-baseline sample (0 = auto)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 9:
+                self.rows.append(f)
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[5:9]) if v == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def make_workload(vsp, p, G, seed):
+    rng = np.random.default_rng(seed)
+    keys = vsp.keygen(p, seed, False)
+    kinds = [("NAND", "XOR")[int(x)] for x in rng.integers(0, 2, G)]
+    bits = rng.integers(0, 2, size=(G, 2)).astype(np.uint8)
+    ins = np.zeros((G, 3, p.n + 1), np.uint32)
+    ins[:, :2] = vsp.encrypt(p, keys["lv0"], bits.reshape(-1), seed + 1).reshape(G, 2, p.n + 1)
+    truth = np.where(np.array(kinds) == "NAND", 1 - (bits[:, 0] & bits[:, 1]),
+                     bits[:, 0] ^ bits[:, 1]).astype(np.uint8)
+    return keys, kinds, ins, truth
+
+
+def cpu_reference_rate(p_name, n, keys, kinds, ins, sample, threads):
+    """Time the reference's own homGate batch (oracle/_ref, parallelFor over host
+    threads) on a bounded sample of the workload; returns gates/s."""
+    from oracle.pyoracle import CpuTfhe, GATE_KINDS, available
+    kind = "ref" if available("ref") else "orc"
+    r = CpuTfhe(kind, p_name, n_override=n, seed=1)
+    r.import_keys(keys)
+    kid = np.array([GATE_KINDS.index(k) for k in kinds[:sample]], np.int32)
+    r.hom_gate_batch(kid[:threads], ins[:threads], threads=threads)  # warm caches/plans
+    t0 = time.perf_counter()
+    r.hom_gate_batch(kid, ins[:sample], threads=threads)
+    dt = time.perf_counter() - t0
+    return sample / dt, kind, dt
+
+
+def traffic_from_profiles():
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(path):
+        try:
+            return json.load(open(path)).get("br1024_bytes_per_launch")
+        except Exception:
+            return None
+    return None
+
+
+def run_ours(args, world, rank, local):
+    import torch
+    import paper_2010_09410_b200 as vsp
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    p = vsp.ParameterSet("tfhe-80", n_override=args.n)
+    G = args.gates
+    keys, kinds, ins, truth = make_workload(vsp, p, G, 1000 + rank)
+    eng = vsp.Engine(p, device=local)
+    eng.upload_keys(keys)
+
+    d_in = torch.from_numpy(ins.view(np.int32)).to(f"cuda:{local}")
+    d_out = torch.empty((G, p.n + 1), dtype=torch.int32, device=f"cuda:{local}")
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=f"cuda:{local}")
+    stream = torch.cuda.current_stream()
+
+    def step():
+        eng.hom_gate_batch_dev(kinds, d_in.data_ptr(), d_out.data_ptr(), G, stream.cuda_stream)
+
+    for _ in range(max(args.warmup, 1)):
+        step()
+    torch.cuda.synchronize()
+    out = d_out.cpu().numpy().view(np.uint32)
+    correct = bool(np.array_equal(vsp.decrypt(keys["lv0"], out), truth))
+
+    # ---- device-timed region: inputs resident, L2 flushed between steps ----
+    eng.profile_reset()
+    eng.profile_enable(True)
+    launches0 = eng.kernel_launches()
+    clocks = ClockSampler(local)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    evs = []
+    for _ in range(args.steps):
+        flush.zero_()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        step()
+        b.record(stream)
+        evs.append((a, b))
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clk = clocks.stop()
+    launches = eng.kernel_launches() - launches0
+    eng.profile_enable(False)
+    ms = sum(a.elapsed_time(b) for a, b in evs)
+    br_ms, br_n = eng.profile_read("br1024")
+    iks_ms, iks_n = eng.profile_read("iks")
+    prep_ms, prep_n = eng.profile_read("gate_prep")
+    t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = G * world * args.steps / (ms_max / 1e3)
+
+    # ---- end to end through the C ABI with pinned host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        h_in = torch.from_numpy(ins.view(np.int32)).pin_memory()
+        h_out = torch.empty((G, p.n + 1), dtype=torch.int32).pin_memory()
+        h_in_np, h_out_np = h_in.numpy().view(np.uint32), h_out.numpy().view(np.uint32)
+        eng.hom_gate_batch(kinds, h_in_np)  # warm
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            res = eng.hom_gate_batch(kinds, h_in_np)
+        dt = time.perf_counter() - t0
+        te = torch.tensor([dt], dtype=torch.float64, device=f"cuda:{local}")
+        if dist:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": G * world * args.steps / float(te.item()), "unit": UNIT,
+               "h2d_bytes_per_step": int(ins.nbytes), "d2h_bytes_per_step": int(res.nbytes),
+               "api": "vsp_hom_gate_batch (C ABI, pinned host buffers)"}
+        del h_out_np, h_out
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    peak = vsp.fp64_peak_tflops(local)
+    avg_br = br_ms / max(br_n, 1)
+    flops = G * p.n * F_EP
+    achieved = flops / (avg_br * 1e-3) / 1e12
+    traffic = traffic_from_profiles()
+    roofline = {"bound": "fp64", "kernel": "br1024_kernel (blind rotation)",
+                "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": "TFLOP/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "peak_source": "measured live: vsp_fp64_peak_probe (DFMA loop) on this GPU",
+                "flops_per_launch": flops,
+                "flops_rule": "G * n * F_EP, F_EP = (2l+2)*5*M*log2 M + 2l*2*8*M = 171008"}
+    share = {"br1024_ms_per_step": round(br_ms / args.steps, 3),
+             "iks_ms_per_step": round(iks_ms / args.steps, 3),
+             "gate_prep_ms_per_step": round(prep_ms / args.steps, 3)}
+
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        threads = os.cpu_count() or 1
+        sample = args.cpu_sample or max(2 * threads, 64)
+        rate, kind, dt = cpu_reference_rate("tfhe-80", args.n, keys, kinds, ins, sample, threads)
+        cpu = {"value": round(rate, 2), "unit": UNIT, "cores": threads,
+               "kind": "reference" if kind == "ref" else "port",
+               "sample": f"{sample} of the {G} gates (same keys/ciphertexts), homGate via the "
+                         f"reference's parallelFor on {threads} threads, {dt:.1f} s wall"}
+
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32+f64",
+        "data": "synthetic (seeded client keygen + encryption of uniform random bits)",
+        "config": {"workload": f"{G} random NAND/XOR gates per GPU, tfhe-80 with n={p.n} "
+                               "(BASELINE.json configs[0])",
+                   "gates_per_gpu": G, "n": p.n, "N": p.N1, "l": p.l1, "Bg_bits": p.Bg1Bits,
+                   "ks": f"2^{p.ksBaseBits} x {p.ksLen}", "l2": "flushed (512 MiB write) "
+                   "between timed steps", "parallelism": f"dp{world} (independent batches)"},
+        "outputs_decrypt_correct": correct,
+        "gpu_launches": int(launches),
+        "e2e": e2e,
+        "roofline": roofline,
+        "breakdown": share,
+        "cpu_baseline": cpu,
+        "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def run_reference(args, world, rank, local):
+    """The reference's own CPU implementation of the path (oracle/_ref built from the
+    reference sources) on the host cores, same metric/config, bounded samples."""
+    if rank != 0:
+        return
+    from oracle.pyoracle import CpuTfhe, GATE_KINDS, available
+    if not available("ref"):
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "oracle/_ref/libhvpref.so not built (needs /root/reference at build)"}))
+        return
+    import paper_2010_09410_b200 as vsp
+    threads = os.cpu_count() or 1
+    sample = args.cpu_sample or max(2 * threads, 64)
+    r = CpuTfhe("ref", "tfhe-80", n_override=args.n, seed=1000)
+    r.keygen(False)  # the reference's own BootstrappingKey::generate
+    rng = np.random.default_rng(1000)
+    kinds = np.array([GATE_KINDS.index(("NAND", "XOR")[int(x)]) for x in
+                      rng.integers(0, 2, sample)], np.int32)
+    ins = np.zeros((sample, 3, r.n + 1), np.uint32)
+    for g in range(sample):
+        ins[g, 0] = r.encrypt(int(rng.integers(0, 2)))
+        ins[g, 1] = r.encrypt(int(rng.integers(0, 2)))
+    for _ in range(args.warmup):
+        r.hom_gate_batch(kinds[:threads], ins[:threads], threads=threads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        r.hom_gate_batch(kinds, ins, threads=threads)
+        times.append(time.perf_counter() - t0)
+    value = sample * args.steps / sum(times)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 2), "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * sum(times) / args.steps, 2), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32+f64",
+        "data": "synthetic (reference keygen + encryption of uniform random bits)",
+        "config": {"workload": f"{args.gates} random NAND/XOR gates, tfhe-80 with n={args.n} "
+                               "(BASELINE.json configs[0]); each step times a bounded sample",
+                   "gates_per_step_sample": sample, "n": args.n},
+        "cpu_baseline": {"value": round(value, 2), "unit": UNIT, "cores": threads,
+                         "kind": "reference",
+                         "sample": f"{sample} gates per step, homGate via parallelFor"},
+        "e2e": {"value": round(value, 2), "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, world, rank, local)
+    else:
+        run_ours(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

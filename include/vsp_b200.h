@@ -1,0 +1,134 @@
+/*
+ * vsp_b200.h — C ABI of the B200-native VSP hot-path engine (libvsp_b200.so).
+ *
+ * Drop-in boundary for the reference's gate-evaluation / CMUX-memory / netlist-runner
+ * path (hvp, /root/reference/proj).  The reference exposes C++ only;
+ * every entry point below names the reference interface it replaces (file:line).
+ * Plain pointers and sizes only.  All functions return 0 on success and a nonzero
+ * status otherwise; vsp_last_error() gives the message.  Status codes mirror the
+ * reference's exception types so the C++/Python facades rethrow the same kind:
+ *   VSP_EINVAL  std::invalid_argument   (arity, geometry, parameters)
+ *   VSP_ERANGE  std::out_of_range       (sample-extract index)
+ *   VSP_ERUNTIME std::runtime_error     (missing key material, CUDA failure, ...)
+ *
+ * Flat layouts (little-endian u32 torus words, identical to the reference vectors):
+ *   TLWE  level 0 : (n+1)  u32   a[0..n) then b          (ciphertext.hpp:14-28)
+ *   TLWE  level 1 : (N1+1) u32
+ *   TRLWE         : 2*N1 u32     a[0..N1) then b[0..N1)  (ciphertext.hpp:34-53)
+ *   TRGSW         : 2*l1 TRLWE rows                      (ciphertext.hpp:60-64)
+ *   bk1           : n x TRGSW                            (BootstrappingKey::bk1Raw, ops.hpp:98)
+ *   bk2           : n x 2*l2 x 2 x N2 u64                (BootstrappingKey::bk2Raw, ops.hpp:102)
+ *   ksk           : N1 x ksLen x (2^ksBaseBits-1) x (n+1) u32     (KeySwitchKey, ops.hpp:18-29)
+ *   pks           : (N2+1) x pksLen x (2^pksBaseBits-1) x 2*N1 u32 (PrivKeySwitchKey, ops.hpp:32-42)
+ *   RAM           : w*2^v TRLWE cells, cells[j*2^v + A]  (EncryptedRam, mem.hpp:32-46)
+ *   ROM           : 2^highBits TRLWE LUTs                (EncryptedRom, mem.hpp:48-61)
+ * Gate kinds use hvp::tfhe::GateKind order (ops.hpp:183-194):
+ *   0 AND, 1 ANDNOT, 2 MUX, 3 NAND, 4 NOR, 5 NOT, 6 OR, 7 ORNOT, 8 XNOR, 9 XOR.
+ */
+#ifndef VSP_B200_H
+#define VSP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VSP_OK 0
+#define VSP_EINVAL 1
+#define VSP_ERANGE 2
+#define VSP_ERUNTIME 3
+
+typedef struct vsp_ctx vsp_ctx;
+
+/* hvp::tfhe::ParameterSet (params.hpp:23-66), integer fields. */
+typedef struct vsp_params {
+    uint32_t n, N1, l1, Bg1Bits, N2, l2, Bg2Bits, ksBaseBits, ksLen, pksBaseBits, pksLen;
+    int32_t fft; /* MulBackend: 1 = Fft, 0 = Exact */
+} vsp_params;
+
+/* ParameterSet::byName (params.cpp:88-95) + ParameterSet::validate (params.cpp:17-29).
+ * n_override > 0 replaces n (BASELINE's n=630 copy of tfhe-80). */
+int vsp_params_by_name(const char* name, uint32_t n_override, vsp_params* out);
+
+const char* vsp_last_error(void);
+
+/* Engine context on one CUDA device.  Replaces the implicit global state of the
+ * reference (thread-local FFT plans fft.cpp:79-85, scratch ops.cpp:20-33). */
+vsp_ctx* vsp_create(const vsp_params* params, int device);
+void vsp_destroy(vsp_ctx* ctx);
+
+/* BootstrappingKey::fromParts + prepareAll (ops.cpp:387-415): upload raw key
+ * material once and transform it on the device.  bk2/pks may be NULL when
+ * has_cb == 0 (key without circuit-bootstrapping material, ops.cpp:417-423). */
+int vsp_upload_keys(vsp_ctx* ctx, const uint32_t* bk1, const uint32_t* ksk,
+                    const uint64_t* bk2, const uint32_t* pks_negs, const uint32_t* pks_id,
+                    int has_cb);
+
+/* homGate (ops.cpp:839-896) over a batch of independent gates, host buffers.
+ * kinds[G]; in[G x 3 x (n+1)] (unused operand slots ignored; MUX = {sel, a, b});
+ * out[G x (n+1)].  Equivalent to G calls of homGate. */
+int vsp_hom_gate_batch(vsp_ctx* ctx, const int32_t* kinds, const uint32_t* in,
+                       uint32_t* out, size_t G);
+
+/* Same with device-resident ciphertexts on `stream` (cudaStream_t, 0 = the
+ * context stream); kinds stay in host memory.  Asynchronous. */
+int vsp_hom_gate_batch_dev(vsp_ctx* ctx, const int32_t* kinds, const uint32_t* d_in,
+                           uint32_t* d_out, size_t G, void* stream);
+
+/* bootstrapToTrlwe (ops.cpp:750-757) for G level-0 TLWEs -> G TRLWEs (host). */
+int vsp_bootstrap_to_trlwe_batch(vsp_ctx* ctx, const uint32_t* in, uint32_t* out, size_t G);
+
+/* gateBootstrap (ops.cpp:759-762) batch (host). */
+int vsp_gate_bootstrap_batch(vsp_ctx* ctx, const uint32_t* in, uint32_t* out, size_t G);
+
+/* identityKeySwitch (ops.cpp:651-679): G level-1 TLWEs -> G level-0 TLWEs (host). */
+int vsp_identity_key_switch_batch(vsp_ctx* ctx, const uint32_t* in, uint32_t* out, size_t G);
+
+/* OpCounters (counters.hpp:11-28): cmux, blindRotate, identityKeySwitch,
+ * privateKeySwitch, circuitBootstrap — counted per batched operation exactly as
+ * the reference increments them per call. */
+int vsp_counters(vsp_ctx* ctx, uint64_t out[5]);
+int vsp_counters_reset(vsp_ctx* ctx);
+
+/* Number of engine kernel launches issued so far (evidence for bench.py). */
+uint64_t vsp_kernel_launches(vsp_ctx* ctx);
+
+int vsp_synchronize(vsp_ctx* ctx);
+
+/* Optional per-kernel CUDA-event timing on the launching stream (bench.py's live
+ * roofline): enable, then read the accumulated time/count of a kernel by name
+ * ("br1024", "br_exact", "iks", "gate_prep", ...). */
+int vsp_profile_enable(vsp_ctx* ctx, int on);
+int vsp_profile_read(vsp_ctx* ctx, const char* name, double* total_ms, uint64_t* count);
+int vsp_profile_reset(vsp_ctx* ctx);
+
+/* Measured dense FP64 FMA throughput of `device` in TFLOP/s (the denominator of the
+ * blind-rotation roofline; MEASURED_PEAKS.json carries no FP64 figure). */
+int vsp_fp64_peak_probe(int device, double* tflops);
+
+/* ---- client side (Alice): key generation / encryption / decryption -------------
+ * Not on the evaluation hot path; provided so the engine can be driven without the
+ * reference.  Same CSPRNG stream and draw order as the reference client code. */
+
+const char* vsp_client_last_error(void);
+
+/* genSecretKey + BootstrappingKey::generate (ops.cpp:264-385) from
+ * Csprng::fromSeed(seed) (rng.cpp:81-91).  bk2/pks_* only written when with_cb. */
+int vsp_client_keygen(const vsp_params* params, uint64_t seed, int with_cb, uint32_t* lv0,
+                      uint32_t* lv1, uint32_t* lv2, uint32_t* bk1, uint32_t* ksk,
+                      uint64_t* bk2, uint32_t* pks_negs, uint32_t* pks_id);
+
+/* tlweEncrypt (ops.cpp:428-440) of count bits, one CSPRNG stream from seed. */
+int vsp_client_tlwe_encrypt(const vsp_params* params, const uint32_t* lv0, uint64_t seed,
+                            const uint8_t* bits, size_t count, uint32_t* out);
+
+/* tlwePhase / tlweDecrypt (ops.cpp:442-456); bits and/or phases may be NULL. */
+int vsp_client_tlwe_decrypt(const uint32_t* key, uint32_t dim, const uint32_t* ct,
+                            size_t count, uint8_t* bits, uint32_t* phases);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

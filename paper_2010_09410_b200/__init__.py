@@ -1,0 +1,308 @@
+"""B200-native engine for the VSP (arXiv 2010.09410) TFHE hot path.
+
+Python host mirror of the reference's gate-evaluation API (hvp::tfhe, ops.hpp:149-221)
+over the C ABI in include/vsp_b200.h (libvsp_b200.so, built in-tree by
+``python -m paper_2010_09410_b200.build``).  The CUDA library is mandatory: there is
+no CPU fallback; importing the engine without the built .so raises.
+
+Error behaviour mirrors the reference's exception types:
+std::invalid_argument -> ValueError, std::out_of_range -> IndexError,
+std::runtime_error -> RuntimeError.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libvsp_b200.so")
+
+# hvp::tfhe::GateKind order (ops.hpp:183-194)
+GATE_KINDS = ["AND", "ANDNOT", "MUX", "NAND", "NOR", "NOT", "OR", "ORNOT", "XNOR", "XOR"]
+GATE_ARITY = {k: (1 if k == "NOT" else 3 if k == "MUX" else 2) for k in GATE_KINDS}
+MU32 = 1 << 29
+
+_lib = None
+
+
+class VspParams(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_uint32) for f in
+                ("n", "N1", "l1", "Bg1Bits", "N2", "l2", "Bg2Bits", "ksBaseBits", "ksLen",
+                 "pksBaseBits", "pksLen")] + [("fft", ctypes.c_int32)]
+
+
+def lib() -> ctypes.CDLL:
+    """Load libvsp_b200.so (fails loudly if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built; run `python -m paper_2010_09410_b200.build`")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, sz, u32, u64 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_uint32, ctypes.c_uint64
+        L.vsp_last_error.restype = ctypes.c_char_p
+        L.vsp_client_last_error.restype = ctypes.c_char_p
+        L.vsp_params_by_name.argtypes = [ctypes.c_char_p, u32, ctypes.POINTER(VspParams)]
+        L.vsp_create.restype = vp
+        L.vsp_create.argtypes = [ctypes.POINTER(VspParams), ctypes.c_int]
+        L.vsp_destroy.argtypes = [vp]
+        L.vsp_upload_keys.argtypes = [vp, vp, vp, vp, vp, vp, ctypes.c_int]
+        L.vsp_hom_gate_batch.argtypes = [vp, vp, vp, vp, sz]
+        L.vsp_hom_gate_batch_dev.argtypes = [vp, vp, vp, vp, sz, vp]
+        L.vsp_bootstrap_to_trlwe_batch.argtypes = [vp, vp, vp, sz]
+        L.vsp_gate_bootstrap_batch.argtypes = [vp, vp, vp, sz]
+        L.vsp_identity_key_switch_batch.argtypes = [vp, vp, vp, sz]
+        L.vsp_counters.argtypes = [vp, vp]
+        L.vsp_counters_reset.argtypes = [vp]
+        L.vsp_kernel_launches.argtypes = [vp]
+        L.vsp_kernel_launches.restype = u64
+        L.vsp_synchronize.argtypes = [vp]
+        L.vsp_profile_enable.argtypes = [vp, ctypes.c_int]
+        L.vsp_profile_read.argtypes = [vp, ctypes.c_char_p, ctypes.POINTER(ctypes.c_double),
+                                       ctypes.POINTER(ctypes.c_uint64)]
+        L.vsp_profile_reset.argtypes = [vp]
+        L.vsp_fp64_peak_probe.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
+        L.vsp_client_keygen.argtypes = [ctypes.POINTER(VspParams), u64, ctypes.c_int] + [vp] * 8
+        L.vsp_client_tlwe_encrypt.argtypes = [ctypes.POINTER(VspParams), vp, u64, vp, sz, vp]
+        L.vsp_client_tlwe_decrypt.argtypes = [vp, u32, vp, sz, vp, vp]
+        _lib = L
+    return _lib
+
+
+def _raise(rc: int, msg: bytes | None):
+    text = (msg or b"").decode()
+    if rc == 1:
+        raise ValueError(text)
+    if rc == 2:
+        raise IndexError(text)
+    raise RuntimeError(text)
+
+
+def _check(rc: int):
+    if rc != 0:
+        _raise(rc, lib().vsp_last_error())
+
+
+def _ccheck(rc: int):
+    if rc != 0:
+        _raise(rc, lib().vsp_client_last_error())
+
+
+def _ptr(a: np.ndarray | None) -> ctypes.c_void_p:
+    if a is None:
+        return ctypes.c_void_p(0)
+    assert a.flags["C_CONTIGUOUS"], "arrays passed to the engine must be C-contiguous"
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+class ParameterSet:
+    """hvp::tfhe::ParameterSet (params.hpp:23-66); ``byName`` (params.cpp:88-95)."""
+
+    def __init__(self, name: str = "tfhe-80", n_override: int = 0):
+        self.c = VspParams()
+        _check(lib().vsp_params_by_name(name.encode(), n_override, ctypes.byref(self.c)))
+        self.name = name
+        for f, _ in VspParams._fields_:
+            setattr(self, f, int(getattr(self.c, f)))
+
+    @property
+    def deterministic(self) -> bool:
+        return not self.fft
+
+    def ksk_words(self) -> int:
+        return self.N1 * self.ksLen * ((1 << self.ksBaseBits) - 1) * (self.n + 1)
+
+    def pks_words(self) -> int:
+        return (self.N2 + 1) * self.pksLen * ((1 << self.pksBaseBits) - 1) * 2 * self.N1
+
+
+# ---------------------------------------------------------------------------
+# client side (Alice)
+
+def keygen(params: ParameterSet, seed: int, with_cb: bool = False) -> dict:
+    """genSecretKey + BootstrappingKey::generate (ops.cpp:264-385), raw arrays."""
+    p = params
+    k = dict(
+        lv0=np.zeros(p.n, np.uint32), lv1=np.zeros(p.N1, np.uint32),
+        lv2=np.zeros(p.N2, np.uint32),
+        bk1=np.zeros((p.n, 2 * p.l1, 2, p.N1), np.uint32),
+        ksk=np.zeros(p.ksk_words(), np.uint32),
+        bk2=np.zeros((p.n, 2 * p.l2, 2, p.N2), np.uint64) if with_cb else None,
+        pks_negs=np.zeros(p.pks_words(), np.uint32) if with_cb else None,
+        pks_id=np.zeros(p.pks_words(), np.uint32) if with_cb else None,
+    )
+    _ccheck(lib().vsp_client_keygen(ctypes.byref(p.c), seed, int(with_cb), _ptr(k["lv0"]),
+                                     _ptr(k["lv1"]), _ptr(k["lv2"]), _ptr(k["bk1"]),
+                                     _ptr(k["ksk"]), _ptr(k["bk2"]), _ptr(k["pks_negs"]),
+                                     _ptr(k["pks_id"])))
+    return k
+
+
+def encrypt(params: ParameterSet, lv0: np.ndarray, bits, seed: int) -> np.ndarray:
+    """tlweEncrypt (ops.cpp:428-440) of each bit; returns (len, n+1) u32."""
+    b = np.ascontiguousarray(np.asarray(bits, np.uint8).reshape(-1))
+    out = np.zeros((b.size, params.n + 1), np.uint32)
+    _ccheck(lib().vsp_client_tlwe_encrypt(ctypes.byref(params.c), _ptr(lv0), seed, _ptr(b),
+                                          b.size, _ptr(out)))
+    return out
+
+
+def decrypt(key: np.ndarray, ct: np.ndarray) -> np.ndarray:
+    """tlweDecrypt (ops.cpp:452-456); ct (..., dim+1) with dim = len(key)."""
+    ct = np.ascontiguousarray(ct, np.uint32)
+    flat = ct.reshape(-1, ct.shape[-1])
+    bits = np.zeros(flat.shape[0], np.uint8)
+    _ccheck(lib().vsp_client_tlwe_decrypt(_ptr(np.ascontiguousarray(key, np.uint32)),
+                                          len(key), _ptr(flat), flat.shape[0], _ptr(bits), None))
+    return bits.reshape(ct.shape[:-1])
+
+
+def phase(key: np.ndarray, ct: np.ndarray) -> np.ndarray:
+    ct = np.ascontiguousarray(ct, np.uint32)
+    flat = ct.reshape(-1, ct.shape[-1])
+    ph = np.zeros(flat.shape[0], np.uint32)
+    _ccheck(lib().vsp_client_tlwe_decrypt(_ptr(np.ascontiguousarray(key, np.uint32)),
+                                          len(key), _ptr(flat), flat.shape[0], None, _ptr(ph)))
+    return ph.reshape(ct.shape[:-1])
+
+
+# ---------------------------------------------------------------------------
+# evaluation engine (Bob)
+
+class Engine:
+    """One device context holding an uploaded BootstrappingKey.
+
+    Method names follow the reference (ops.hpp:149-221) in snake case; every method
+    accepts a batch (leading axis) and is equivalent to calling the reference
+    function once per element.
+    """
+
+    def __init__(self, params: ParameterSet | str = "tfhe-80", device: int = 0,
+                 n_override: int = 0):
+        self.params = params if isinstance(params, ParameterSet) else \
+            ParameterSet(params, n_override)
+        L = lib()
+        self.h = L.vsp_create(ctypes.byref(self.params.c), device)
+        if not self.h:
+            _raise(3, L.vsp_last_error())
+        self.h = ctypes.c_void_p(self.h)
+        self.device = device
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().vsp_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # BootstrappingKey::fromParts (ops.cpp:387-402)
+    def upload_keys(self, k: dict):
+        has_cb = k.get("bk2") is not None
+        c = lambda a: None if a is None else np.ascontiguousarray(a)
+        self._keys = {key: c(v) for key, v in k.items()}
+        kk = self._keys
+        _check(lib().vsp_upload_keys(self.h, _ptr(kk["bk1"]), _ptr(kk["ksk"]),
+                                     _ptr(kk.get("bk2")), _ptr(kk.get("pks_negs")),
+                                     _ptr(kk.get("pks_id")), int(has_cb)))
+        self._keys = None
+
+    @staticmethod
+    def _kind_ids(kinds) -> np.ndarray:
+        out = []
+        for k in kinds:
+            if isinstance(k, str):
+                if k not in GATE_KINDS:
+                    raise ValueError(f"homGate: unknown kind {k}")
+                out.append(GATE_KINDS.index(k))
+            else:
+                out.append(int(k))
+        return np.ascontiguousarray(np.asarray(out, np.int32))
+
+    def hom_gate(self, kind, inputs) -> np.ndarray:
+        """homGate (ops.cpp:839-896) for one gate; inputs: list of TLWEs."""
+        name = kind if isinstance(kind, str) else GATE_KINDS[int(kind)]
+        if len(inputs) != GATE_ARITY.get(name, -1):
+            raise ValueError(f"homGate: bad arity for {name}")
+        x = np.zeros((1, 3, self.params.n + 1), np.uint32)
+        for i, t in enumerate(inputs):
+            x[0, i] = t
+        return self.hom_gate_batch([name], x)[0]
+
+    def hom_gate_batch(self, kinds, ins: np.ndarray) -> np.ndarray:
+        """Batched homGate: kinds[G], ins (G, 3, n+1) -> (G, n+1)."""
+        kid = self._kind_ids(kinds)
+        ins = np.ascontiguousarray(ins, np.uint32)
+        G = kid.size
+        if ins.shape != (G, 3, self.params.n + 1):
+            raise ValueError(f"expected inputs of shape {(G, 3, self.params.n + 1)}")
+        out = np.zeros((G, self.params.n + 1), np.uint32)
+        _check(lib().vsp_hom_gate_batch(self.h, _ptr(kid), _ptr(ins), _ptr(out), G))
+        return out
+
+    def hom_gate_batch_dev(self, kinds, d_in_ptr: int, d_out_ptr: int, G: int,
+                           stream_ptr: int = 0):
+        """Device-resident variant (pointers from torch tensors); asynchronous."""
+        kid = self._kind_ids(kinds)
+        _check(lib().vsp_hom_gate_batch_dev(self.h, _ptr(kid), ctypes.c_void_p(d_in_ptr),
+                                            ctypes.c_void_p(d_out_ptr), G,
+                                            ctypes.c_void_p(stream_ptr)))
+
+    def bootstrap_to_trlwe(self, cts: np.ndarray) -> np.ndarray:
+        """bootstrapToTrlwe (ops.cpp:750-757); (G, n+1) -> (G, 2*N1)."""
+        cts = np.ascontiguousarray(np.atleast_2d(cts), np.uint32)
+        out = np.zeros((cts.shape[0], 2 * self.params.N1), np.uint32)
+        _check(lib().vsp_bootstrap_to_trlwe_batch(self.h, _ptr(cts), _ptr(out), cts.shape[0]))
+        return out
+
+    def gate_bootstrap(self, cts: np.ndarray) -> np.ndarray:
+        """gateBootstrap (ops.cpp:759-762); (G, n+1) -> (G, n+1)."""
+        cts = np.ascontiguousarray(np.atleast_2d(cts), np.uint32)
+        out = np.zeros_like(cts)
+        _check(lib().vsp_gate_bootstrap_batch(self.h, _ptr(cts), _ptr(out), cts.shape[0]))
+        return out
+
+    def identity_key_switch(self, cts: np.ndarray) -> np.ndarray:
+        """identityKeySwitch (ops.cpp:651-679); (G, N1+1) -> (G, n+1)."""
+        cts = np.ascontiguousarray(np.atleast_2d(cts), np.uint32)
+        out = np.zeros((cts.shape[0], self.params.n + 1), np.uint32)
+        _check(lib().vsp_identity_key_switch_batch(self.h, _ptr(cts), _ptr(out), cts.shape[0]))
+        return out
+
+    def counters(self) -> dict:
+        """OpCounters (counters.hpp:11-28)."""
+        o = np.zeros(5, np.uint64)
+        _check(lib().vsp_counters(self.h, _ptr(o)))
+        return dict(zip(["cmux", "blindRotate", "identityKeySwitch", "privateKeySwitch",
+                         "circuitBootstrap"], (int(x) for x in o)))
+
+    def counters_reset(self):
+        _check(lib().vsp_counters_reset(self.h))
+
+    def kernel_launches(self) -> int:
+        return int(lib().vsp_kernel_launches(self.h))
+
+    def synchronize(self):
+        _check(lib().vsp_synchronize(self.h))
+
+    def profile_enable(self, on: bool = True):
+        _check(lib().vsp_profile_enable(self.h, int(on)))
+
+    def profile_read(self, name: str) -> tuple[float, int]:
+        ms, cnt = ctypes.c_double(), ctypes.c_uint64()
+        _check(lib().vsp_profile_read(self.h, name.encode(), ctypes.byref(ms), ctypes.byref(cnt)))
+        return ms.value, int(cnt.value)
+
+    def profile_reset(self):
+        _check(lib().vsp_profile_reset(self.h))
+
+
+def fp64_peak_tflops(device: int = 0) -> float:
+    """Measured DFMA throughput of the device (TFLOP/s)."""
+    t = ctypes.c_double()
+    _check(lib().vsp_fp64_peak_probe(device, ctypes.byref(t)))
+    return t.value

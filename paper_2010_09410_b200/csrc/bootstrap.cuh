@@ -1,0 +1,368 @@
+// Gate-bootstrapping kernels (level 1, N1 = 1024, FFT path) plus the batched
+// identity key switch and the gate linear-combination / finalize kernels.
+//
+// Reference path replaced (ops.cpp): homGate (839-896) -> linComb (774-806) ->
+// gateBootstrap (759-762) -> bootstrapToTrlwe (750-757) -> blindRotate (713-742)
+// -> externalProduct (553-599) -> sampleExtract (628-643) -> identityKeySwitch (651-679).
+#pragma once
+
+#include "fft512.cuh"
+
+namespace vsp {
+
+// Gate kinds in hvp::tfhe::GateKind order (ops.hpp:183-194).
+enum GateKindDev : int {
+    kAnd = 0, kAndNot, kMux, kNand, kNor, kNot, kOr, kOrNot, kXnor, kXor
+};
+
+// ---------------------------------------------------------------------------
+// Bootstrapping-key preparation: raw TRGSW rows (u32, signed interpretation as in
+// FftPlan::forward, fft.hpp:64-75) -> transformed rows in the kernel's slot layout
+// [row][poly][j][lane] (double2), pre-scaled by 1/512 so the inverse needs no scale.
+// One warp per polynomial.  (prepareTrgsw, ops.cpp:520-546.)
+__global__ void __launch_bounds__(128) prepare_poly1024_kernel(
+    const uint32_t* __restrict__ raw, const double2* __restrict__ tw2g,
+    double2* __restrict__ out, int npolys)
+{
+    __shared__ double2 tw2[kTw2Entries * 32];
+    __shared__ double2 xb[4][kFftXbufStride];
+    for (int i = threadIdx.x; i < kTw2Entries * 32; i += blockDim.x)
+        tw2[i] = tw2g[i];
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int q = blockIdx.x * 4 + warp;
+    if (q >= npolys)
+        return;
+    const uint32_t* src = raw + (size_t)q * 1024;
+    double2 z[16];
+#pragma unroll
+    for (int j = 0; j < 16; j++) {
+        z[j].x = (double)(int32_t)src[lane + 32 * j];
+        z[j].y = (double)(int32_t)src[lane + 32 * j + 512];
+    }
+    fft512_fwd(z, xb[warp], tw2, lane);
+    double2* dst = out + (size_t)(q >> 1) * 1024 + (q & 1) * 512;
+    const double s = 1.0 / 512.0;
+#pragma unroll
+    for (int j = 0; j < 16; j++)
+        dst[j * 32 + lane] = make_double2(z[j].x * s, z[j].y * s);
+}
+
+// ---------------------------------------------------------------------------
+// Batched blind rotation, one warp per task (bootstrapToTrlwe: test vector
+// a = 0, b = mu everywhere).  All warps of a CTA walk the same bootstrapping key
+// bk[i] row by row; each 16 KiB row (both output polynomials) is staged once per
+// CTA through a ring of S shared-memory slots by the bulk-copy (TMA) engine and
+// consumed by every warp.  The last warp to release a slot refills it.
+//
+// Output: the full TRLWE accumulator (a[1024], b[1024]) per task.
+template <int WARPS, int S>
+struct Br1024Smem {
+    double2 ring[S][1024];
+    double2 tw2[kTw2Entries * 32];
+    double2 xbuf[WARPS][kFftXbufStride];
+    uint32_t acc[WARPS][2048];
+    uint64_t full[S];
+    uint32_t cnt[S];
+};
+
+template <int WARPS, int S>
+__global__ void __launch_bounds__(WARPS * 32, 1)
+    br1024_kernel(const uint32_t* __restrict__ tasks, const double2* __restrict__ bkfd,
+                  const double2* __restrict__ tw2g, uint32_t* __restrict__ out, int T, int n,
+                  int bgbits)
+{
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    auto& sm = *reinterpret_cast<Br1024Smem<WARPS, S>*>(smem_raw);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int task = blockIdx.x * WARPS + warp;
+    const bool active = task < T;
+    if (!active)
+        task = T - 1;  // inactive warps shadow a real task to keep the slot protocol
+    const uint32_t* lwe = tasks + (size_t)task * (n + 1);
+    const int nchunks = 4 * n;
+
+    for (int i = threadIdx.x; i < kTw2Entries * 32; i += blockDim.x)
+        sm.tw2[i] = tw2g[i];
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; s++) {
+            mbar_init(&sm.full[s], 1);
+            sm.cnt[s] = 0;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S && s < nchunks; s++) {
+            mbar_arrive_expect_tx(&sm.full[s], 16384);
+            bulk_g2s(sm.ring[s], bkfd + (size_t)s * 1024, 16384, &sm.full[s]);
+        }
+    }
+
+    // acc = X^{-round(2N b)} * (0, mu...mu)  (blindRotate init, ops.cpp:727-730)
+    uint32_t* acc = sm.acc[warp];
+    {
+        const uint32_t rot = (2048u - mod_switch_2n(lwe[n], 11)) & 2047u;
+        for (int q = lane; q < 1024; q += 32) {
+            acc[q] = 0;
+            uint32_t val;
+            if (rot < 1024)
+                val = ((uint32_t)q < rot) ? (0u - kMu32) : kMu32;
+            else
+                val = ((uint32_t)q < rot - 1024) ? kMu32 : (0u - kMu32);
+            acc[1024 + q] = val;
+        }
+    }
+    __syncwarp();
+
+    // decomposePoly constants (poly.hpp:79-97), l = 2: no final rounding bit.
+    const uint32_t half = 1u << (bgbits - 1);
+    const uint32_t mask = (1u << bgbits) - 1;
+    const uint32_t offset = (half << (32 - bgbits)) + (half << (32 - 2 * bgbits));
+    const int sh1 = 32 - bgbits, sh2 = 32 - 2 * bgbits;
+    double2* xbuf = sm.xbuf[warp];
+
+    double2 accA[16], accB[16];
+
+#pragma unroll 1
+    for (int i = 0; i < n; i++) {
+        const uint32_t bara = mod_switch_2n(lwe[i], 11);
+#pragma unroll
+        for (int j = 0; j < 16; j++) {
+            accA[j] = make_double2(0.0, 0.0);
+            accB[j] = make_double2(0.0, 0.0);
+        }
+#pragma unroll 1
+        for (int P = 0; P < 2; P++) {
+            const uint32_t* src = acc + P * 1024;
+#pragma unroll 1
+            for (int lvl = 0; lvl < 2; lvl++) {
+                // diff = (X^bara - 1) * acc (polyMulByXkMinusOne, poly.hpp:51-57), then the
+                // level-lvl signed digit of every coefficient (decomposePoly, poly.hpp:79-97)
+                const int sh = lvl == 0 ? sh1 : sh2;
+                double2 z[16];
+#pragma unroll
+                for (int j = 0; j < 16; j++) {
+                    const uint32_t p0 = lane + 32 * j, p1 = p0 + 512;
+                    const uint32_t i0 = (p0 - bara) & 2047u, i1 = (p1 - bara) & 2047u;
+                    const uint32_t r0 = i0 < 1024 ? src[i0] : 0u - src[i0 - 1024];
+                    const uint32_t r1 = i1 < 1024 ? src[i1] : 0u - src[i1 - 1024];
+                    const uint32_t v0 = r0 - src[p0] + offset;
+                    const uint32_t v1 = r1 - src[p1] + offset;
+                    z[j].x = (double)(int32_t)(((v0 >> sh) & mask) - half);
+                    z[j].y = (double)(int32_t)(((v1 >> sh) & mask) - half);
+                }
+                fft512_fwd(z, xbuf, sm.tw2, lane);
+                const int c = i * 4 + P * 2 + lvl;
+                const int s = c % S;
+                mbar_wait(&sm.full[s], (uint32_t)((c / S) & 1));
+                const double2* bk = sm.ring[s];
+#pragma unroll
+                for (int j = 0; j < 16; j++) {
+                    const double2 ba = bk[j * 32 + lane];
+                    const double2 bb = bk[512 + j * 32 + lane];
+                    accA[j].x = fma(z[j].x, ba.x, fma(-z[j].y, ba.y, accA[j].x));
+                    accA[j].y = fma(z[j].x, ba.y, fma(z[j].y, ba.x, accA[j].y));
+                    accB[j].x = fma(z[j].x, bb.x, fma(-z[j].y, bb.y, accB[j].x));
+                    accB[j].y = fma(z[j].x, bb.y, fma(z[j].y, bb.x, accB[j].y));
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    const uint32_t old = atomicAdd(&sm.cnt[s], 1u);
+                    if (old == WARPS - 1) {
+                        sm.cnt[s] = 0;
+                        const int cn = c + S;
+                        if (cn < nchunks) {
+                            fence_proxy_async();
+                            mbar_arrive_expect_tx(&sm.full[s], 16384);
+                            bulk_g2s(sm.ring[s], bkfd + (size_t)cn * 1024, 16384, &sm.full[s]);
+                        }
+                    }
+                }
+            }
+        }
+        // inverse transforms, round (llrint, fft.hpp:47-50) and accumulate
+        fft512_inv(accA, xbuf, sm.tw2, lane);
+#pragma unroll
+        for (int j = 0; j < 16; j++) {
+            const int p = lane + 32 * j;
+            acc[p] += (uint32_t)__double2ll_rn(accA[j].x);
+            acc[p + 512] += (uint32_t)__double2ll_rn(accA[j].y);
+        }
+        fft512_inv(accB, xbuf, sm.tw2, lane);
+#pragma unroll
+        for (int j = 0; j < 16; j++) {
+            const int p = lane + 32 * j;
+            acc[1024 + p] += (uint32_t)__double2ll_rn(accB[j].x);
+            acc[1024 + p + 512] += (uint32_t)__double2ll_rn(accB[j].y);
+        }
+        __syncwarp();
+    }
+    if (active) {
+        uint4* dst = reinterpret_cast<uint4*>(out + (size_t)task * 2048);
+        const uint4* s4 = reinterpret_cast<const uint4*>(acc);
+        for (int q = lane; q < 512; q += 32)
+            dst[q] = s4[q];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Gate linear combinations (linComb + per-kind coefficients, ops.cpp:774-893).
+// Emits the level-0 TLWE input of each blind-rotation task; NOT is finished here
+// (pure negation, ops.cpp:849-855).
+// gtask[g] = (t0, t1): task slots of gate g (t1 >= 0 only for MUX; t0 < 0 for NOT).
+__global__ void gate_prep_kernel(const int* __restrict__ kinds, const uint32_t* __restrict__ in,
+                                 const int2* __restrict__ gtask, uint32_t* __restrict__ tasks,
+                                 uint32_t* __restrict__ out, int G, int n)
+{
+    const int g = blockIdx.x;
+    if (g >= G)
+        return;
+    const int kind = kinds[g];
+    const int2 tt = gtask[g];
+    const uint32_t* x = in + (size_t)g * 3 * (n + 1);
+    const uint32_t* y = x + (n + 1);
+    const uint32_t* z = y + (n + 1);
+    const uint32_t mu = kMu32, nmu = 0u - kMu32;
+    int c0 = 1, c1 = 1;
+    uint32_t bias = nmu;
+    switch (kind) {
+    case kAnd: c0 = 1; c1 = 1; bias = nmu; break;
+    case kNand: c0 = -1; c1 = -1; bias = mu; break;
+    case kOr: c0 = 1; c1 = 1; bias = mu; break;
+    case kNor: c0 = -1; c1 = -1; bias = nmu; break;
+    case kXor: c0 = 2; c1 = 2; bias = 2 * mu; break;
+    case kXnor: c0 = -2; c1 = -2; bias = 2 * nmu; break;
+    case kAndNot: c0 = 1; c1 = -1; bias = nmu; break;
+    case kOrNot: c0 = 1; c1 = -1; bias = mu; break;
+    default: break;
+    }
+    for (int k = threadIdx.x; k <= n; k += blockDim.x) {
+        const uint32_t bk = (k == n) ? 1u : 0u;
+        if (kind == kNot) {
+            out[(size_t)g * (n + 1) + k] = 0u - x[k];
+        }
+        else if (kind == kMux) {  // in = {sel, a, b}
+            tasks[(size_t)tt.x * (n + 1) + k] = x[k] + y[k] + bk * nmu;
+            tasks[(size_t)tt.y * (n + 1) + k] = z[k] - x[k] + bk * nmu;
+        }
+        else {
+            tasks[(size_t)tt.x * (n + 1) + k] =
+                (uint32_t)c0 * x[k] + (uint32_t)c1 * y[k] + bk * bias;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Batched identity key switch (ops.cpp:651-679) fused with sampleExtract(.,0)
+// (ops.cpp:628-643) and the MUX level-1 sum (ops.cpp:886-892).
+// One CTA handles GT gates x all n+1 output coordinates; for every (i, j) it reads
+// the (2^b - 1) candidate KSK rows once (coalesced) and each gate selects its row
+// by digit, so the KSK is streamed once per GT gates instead of once per gate.
+// Source of level-1 input for listed gate g: TRLWE of task t0 (+ task t1 + mu).
+template <int BASEBITS, int GT, int KPT>
+__global__ void __launch_bounds__(256) iks_kernel(
+    const uint32_t* __restrict__ trlwe, const int2* __restrict__ gtask,
+    const int* __restrict__ glist, int Gl, const uint32_t* __restrict__ ksk,
+    uint32_t* __restrict__ out, int n, int N, int t)
+{
+    static_assert(GT * BASEBITS <= 64, "digit packing");
+    constexpr uint32_t kMask = (1u << BASEBITS) - 1;
+    constexpr int kPerBase = (1 << BASEBITS) - 1;
+    extern __shared__ __align__(16) uint64_t dig[];  // [N * t]
+    __shared__ uint32_t bsh[GT];
+    const int g0 = blockIdx.x * GT;
+    const int ng = min(GT, Gl - g0);
+    const uint32_t offset = (uint32_t)(BASEBITS * t >= 32 ? 0u : 1u << (32 - (1 + BASEBITS * t)));
+
+    // digits of the sample-extracted level-1 TLWE of every gate in the tile
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+        uint64_t word[16];
+#pragma unroll
+        for (int j = 0; j < 16; j++)
+            word[j] = 0;
+        for (int g = 0; g < ng; g++) {
+            const int gate = glist[g0 + g];
+            const int2 tt = gtask[gate];
+            const uint32_t* A = trlwe + (size_t)tt.x * 2 * N;
+            uint32_t a = (i == 0) ? A[0] : 0u - A[N - i];
+            if (tt.y >= 0) {
+                const uint32_t* B = trlwe + (size_t)tt.y * 2 * N;
+                a += (i == 0) ? B[0] : 0u - B[N - i];
+            }
+            const uint32_t v = a + offset;
+            for (int j = 0; j < t; j++) {
+                const uint64_t d = (v >> (32 - (j + 1) * BASEBITS)) & kMask;
+                word[j] |= d << (g * BASEBITS);
+            }
+        }
+        for (int j = 0; j < t; j++)
+            dig[i * t + j] = word[j];
+    }
+    if (threadIdx.x < ng) {
+        const int gate = glist[g0 + threadIdx.x];
+        const int2 tt = gtask[gate];
+        uint32_t b = trlwe[(size_t)tt.x * 2 * N + N];
+        if (tt.y >= 0)
+            b += trlwe[(size_t)tt.y * 2 * N + N] + kMu32;
+        bsh[threadIdx.x] = b;
+    }
+    __syncthreads();
+
+    uint32_t acc[GT][KPT];
+#pragma unroll
+    for (int g = 0; g < GT; g++)
+#pragma unroll
+        for (int kk = 0; kk < KPT; kk++) {
+            const int k = threadIdx.x + kk * 256;
+            acc[g][kk] = (k == n && g < ng) ? bsh[g] : 0u;
+        }
+
+    const size_t rowStride = (size_t)n + 1;
+#pragma unroll 1
+    for (int ij = 0; ij < N * t; ij++) {
+        const uint64_t dd = dig[ij];
+        if (dd == 0)
+            continue;
+        const uint32_t* base = ksk + (size_t)ij * kPerBase * rowStride;
+#pragma unroll
+        for (int kk = 0; kk < KPT; kk++) {
+            const int k = threadIdx.x + kk * 256;
+            if (k > n)
+                continue;
+            if constexpr (BASEBITS == 2) {
+                const uint32_t r1 = __ldg(base + k);
+                const uint32_t r2 = __ldg(base + rowStride + k);
+                const uint32_t r3 = __ldg(base + 2 * rowStride + k);
+#pragma unroll
+                for (int g = 0; g < GT; g++) {
+                    const uint32_t d = (uint32_t)(dd >> (2 * g)) & 3u;
+                    const uint32_t lo = (d & 1u) ? r1 : 0u;
+                    const uint32_t hi = (d & 1u) ? r3 : r2;
+                    acc[g][kk] -= (d & 2u) ? hi : lo;
+                }
+            }
+            else {
+#pragma unroll
+                for (int g = 0; g < GT; g++) {
+                    const uint32_t d = (uint32_t)(dd >> (BASEBITS * g)) & kMask;
+                    if (d)
+                        acc[g][kk] -= __ldg(base + (size_t)(d - 1) * rowStride + k);
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int g = 0; g < GT; g++) {
+        if (g >= ng)
+            break;
+        const int gate = glist[g0 + g];
+#pragma unroll
+        for (int kk = 0; kk < KPT; kk++) {
+            const int k = threadIdx.x + kk * 256;
+            if (k <= n)
+                out[(size_t)gate * (n + 1) + k] = acc[g][kk];
+        }
+    }
+}
+
+}  // namespace vsp

@@ -1,0 +1,36 @@
+"""Client-side key generation/encryption of the product (libvsp_b200.so, host code)
+against the reference (golden key hashes)."""
+import hashlib
+
+import numpy as np
+
+import paper_2010_09410_b200 as vsp
+from tests.helpers import golden
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def test_client_keygen_matches_reference_testdet():
+    g = golden("testdet_seed515253.npz")
+    k = vsp.keygen(vsp.ParameterSet("test-det"), 515253, True)
+    names = ["lv0", "lv1", "lv2", "bk1", "ksk", "bk2", "pks_negs", "pks_id"]
+    assert [sha(k[x]) for x in names] == list(g["key_sha"])
+
+
+def test_client_keygen_matches_reference_tfhe80():
+    g = golden("tfhe80_seed20200729.npz")
+    k = vsp.keygen(vsp.ParameterSet("tfhe-80"), 20200729, False)
+    assert [sha(k[x]) for x in ["lv0", "lv1", "lv2", "bk1", "ksk"]] == list(g["key_sha"])
+
+
+def test_client_encrypt_decrypt_roundtrip():
+    p = vsp.ParameterSet("tfhe-80")
+    k = vsp.keygen(p, 3, False)
+    bits = np.random.default_rng(1).integers(0, 2, 1000).astype(np.uint8)
+    ct = vsp.encrypt(p, k["lv0"], bits, 99)
+    assert np.array_equal(vsp.decrypt(k["lv0"], ct), bits)
+    ph = vsp.phase(k["lv0"], ct).astype(np.int64)
+    ph = np.where(ph >= 2**31, ph - 2**32, ph)
+    assert np.all(np.abs(np.abs(ph) - vsp.MU32) < 2**29 // 8)

@@ -1,0 +1,159 @@
+"""GPU parity of the batched gate-bootstrapping path (blind rotation, sample extract,
+identity key switch) against the CPU oracle and the reference's golden vectors.
+
+Bar: bit-exact ciphertexts (integer torus words) on identical keys and inputs.
+"""
+import numpy as np
+import pytest
+
+import paper_2010_09410_b200 as vsp
+from oracle.pyoracle import GATE_KINDS
+from tests.helpers import TRUTH, golden, oracle, oracle_keys, random_gate_batch
+
+pytestmark = pytest.mark.gpu
+
+
+def engine(params, seed, with_cb=False, n_override=0):
+    e = vsp.Engine(params, n_override=n_override)
+    e.upload_keys(oracle_keys(params, seed, with_cb, n_override))
+    return e
+
+
+@pytest.fixture(scope="module")
+def det():
+    return engine("test-det", 515253, True), oracle("test-det", 515253, True)
+
+
+@pytest.fixture(scope="module")
+def prod():
+    return engine("tfhe-80", 20200729), oracle("tfhe-80", 20200729, False)
+
+
+def test_golden_testdet(det):
+    e, _ = det
+    g = golden("testdet_seed515253.npz")
+    out = e.hom_gate_batch(list(g["kinds"]), g["ins"])
+    assert np.array_equal(out, g["outs"])
+
+
+def test_golden_tfhe80(prod):
+    e, _ = prod
+    g = golden("tfhe80_seed20200729.npz")
+    out = e.hom_gate_batch(list(g["kinds"]), g["ins"])
+    assert np.array_equal(out, g["outs"])
+    assert np.array_equal(e.bootstrap_to_trlwe(g["br_in"]), g["br_out"])
+
+
+def test_golden_n630():
+    e = engine("tfhe-80", 630, n_override=630)
+    g = golden("tfhe80n630_seed630.npz")
+    assert np.array_equal(e.hom_gate_batch(list(g["kinds"]), g["ins"]), g["outs"])
+
+
+@pytest.mark.parametrize("kind", GATE_KINDS)
+def test_truth_tables_testdet_exhaustive(det, kind):
+    e, o = det
+    ar = vsp.GATE_ARITY[kind]
+    combos = [(a, b, c) for a in (0, 1) for b in (0, 1) for c in (0, 1)]
+    ins = np.zeros((len(combos), 3, o.n + 1), np.uint32)
+    for i, bits in enumerate(combos):
+        for j in range(3):
+            ins[i, j] = o.encrypt(bits[j])
+    out = e.hom_gate_batch([kind] * len(combos), ins)
+    for i, bits in enumerate(combos):
+        ref = o.hom_gate(kind, list(ins[i][:ar]))
+        assert np.array_equal(out[i], ref)
+        assert o.decrypt(out[i]) == TRUTH[kind](*bits)
+
+
+def test_random_mixed_batch_tfhe80_bit_exact(prod):
+    e, o = prod
+    rng = np.random.default_rng(11)
+    kinds, bits, ins = random_gate_batch(o, rng, 37)   # ragged: not a multiple of 8 warps
+    out = e.hom_gate_batch(kinds, ins)
+    ref = o.hom_gate_batch(np.array([GATE_KINDS.index(k) for k in kinds]), ins, threads=8)
+    assert np.array_equal(out, ref)
+    for g, k in enumerate(kinds):
+        assert o.decrypt(out[g]) == TRUTH[k](*bits[g])
+
+
+def test_nand_xor_4096_decrypt_and_sample_bit_exact(prod):
+    """BASELINE config-1 shape at full size: every output decrypts to the truth table;
+    a strided sample is bit-exact against the oracle."""
+    e, o = prod
+    rng = np.random.default_rng(3)
+    G = 4096
+    kinds = [("NAND", "XOR")[int(x)] for x in rng.integers(0, 2, G)]
+    bits = rng.integers(0, 2, size=(G, 2)).astype(np.uint8)
+    k = oracle_keys("tfhe-80", 20200729, False)
+    p = vsp.ParameterSet("tfhe-80")
+    ins = np.zeros((G, 3, p.n + 1), np.uint32)
+    ins[:, :2] = vsp.encrypt(p, k["lv0"], bits.reshape(-1), 1234).reshape(G, 2, p.n + 1)
+    out = e.hom_gate_batch(kinds, ins)
+    dec = vsp.decrypt(k["lv0"], out)
+    want = np.array([TRUTH[kk](int(a), int(b), 0) for kk, (a, b) in zip(kinds, bits)])
+    assert np.array_equal(dec, want)
+    idx = np.arange(0, G, 293)
+    ref = o.hom_gate_batch(np.array([GATE_KINDS.index(kinds[i]) for i in idx]), ins[idx],
+                           threads=8)
+    assert np.array_equal(out[idx], ref)
+
+
+def test_identity_key_switch_and_gate_bootstrap(prod):
+    e, o = prod
+    rng = np.random.default_rng(7)
+    x = np.stack([o.encrypt(int(b)) for b in rng.integers(0, 2, 5)])
+    gb = e.gate_bootstrap(x)
+    for i in range(len(x)):
+        assert np.array_equal(gb[i], o.gate_bootstrap(x[i]))
+    tr = e.bootstrap_to_trlwe(x)
+    lvl1 = np.stack([o.sample_extract(t, 0) for t in tr])
+    ks = e.identity_key_switch(lvl1)
+    for i in range(len(x)):
+        assert np.array_equal(ks[i], o.identity_key_switch(lvl1[i]))
+
+
+def test_noise_inflated_to_0p9_mu_still_decodes(prod):
+    """test_tfhe.cpp:462-472 on the GPU path."""
+    e, o = prod
+    rng = np.random.default_rng(8)
+    xs, ms = [], []
+    for i in range(64):
+        m = int(rng.integers(0, 2))
+        c = o.encrypt(m)
+        c[-1] = np.uint32((int(c[-1]) + (int(0.9 * vsp.MU32) * (1 if i & 1 else -1))) % 2**32)
+        xs.append(c)
+        ms.append(m)
+    out = e.gate_bootstrap(np.stack(xs))
+    assert [o.decrypt(c) for c in out] == ms
+
+
+def test_edge_cases_and_errors(det):
+    e, o = det
+    empty = e.hom_gate_batch([], np.zeros((0, 3, o.n + 1), np.uint32))
+    assert empty.shape == (0, o.n + 1)
+    one = e.hom_gate("NOT", [o.encrypt(1)])
+    assert o.decrypt(one) == 0
+    twice = e.hom_gate("NOT", [one])
+    assert o.decrypt(twice) == 1
+    with pytest.raises(ValueError):
+        e.hom_gate("AND", [o.encrypt(1)])
+    with pytest.raises(ValueError):
+        e.hom_gate_batch([11], np.zeros((1, 3, o.n + 1), np.uint32))
+
+
+def test_counters_match_reference_semantics(det):
+    e, o = det
+    e.counters_reset()
+    o.counters_reset()
+    x = [o.encrypt(1), o.encrypt(0), o.encrypt(1)]
+    ins = np.zeros((3, 3, o.n + 1), np.uint32)
+    for i in range(3):
+        ins[i] = np.stack(x)
+    e.hom_gate_batch(["MUX", "NAND", "NOT"], ins)
+    o.hom_gate("MUX", x)
+    o.hom_gate("NAND", x[:2])
+    o.hom_gate("NOT", x[:1])
+    c = e.counters()
+    oc = o.counters()
+    assert (c["cmux"], c["blindRotate"], c["identityKeySwitch"]) == (oc[0], oc[1], oc[2])
