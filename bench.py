@@ -254,7 +254,7 @@ def run_ours(args, world, rank, local):
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         threads = os.cpu_count() or 1
-        sample = args.cpu_sample or max(2 * threads, 64)
+        sample = args.cpu_sample or min(G, max(64 * threads, 512))
         rate, kind, dt = cpu_reference_rate("tfhe-80", args.n, keys, kinds, ins, sample, threads)
         cpu = {"value": round(rate, 2), "unit": UNIT, "cores": threads,
                "kind": "reference" if kind == "ref" else "port",
@@ -296,7 +296,7 @@ def run_reference(args, world, rank, local):
         return
     import paper_2010_09410_b200 as vsp
     threads = os.cpu_count() or 1
-    sample = args.cpu_sample or max(2 * threads, 64)
+    sample = args.cpu_sample or max(16 * threads, 128)
     r = CpuTfhe("ref", "tfhe-80", n_override=args.n, seed=1000)
     r.keygen(False)  # the reference's own BootstrappingKey::generate
     rng = np.random.default_rng(1000)

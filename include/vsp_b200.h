@@ -61,7 +61,8 @@ void vsp_destroy(vsp_ctx* ctx);
 
 /* BootstrappingKey::fromParts + prepareAll (ops.cpp:387-415): upload raw key
  * material once and transform it on the device.  bk2/pks may be NULL when
- * has_cb == 0 (key without circuit-bootstrapping material, ops.cpp:417-423). */
+ * has_cb == 0 (key without circuit-bootstrapping material, ops.cpp:417-423); has_cb == 2
+ * uploads bk2 without the private key-switching tables (level-2 blind rotation only). */
 int vsp_upload_keys(vsp_ctx* ctx, const uint32_t* bk1, const uint32_t* ksk,
                     const uint64_t* bk2, const uint32_t* pks_negs, const uint32_t* pks_id,
                     int has_cb);
@@ -72,8 +73,8 @@ int vsp_upload_keys(vsp_ctx* ctx, const uint32_t* bk1, const uint32_t* ksk,
 int vsp_hom_gate_batch(vsp_ctx* ctx, const int32_t* kinds, const uint32_t* in,
                        uint32_t* out, size_t G);
 
-/* Same with device-resident ciphertexts on `stream` (cudaStream_t, 0 = the
- * context stream); kinds stay in host memory.  Asynchronous. */
+/* Same with device-resident ciphertexts, enqueued on `stream` (a cudaStream_t; 0 is
+ * the legacy default stream); kinds stay in host memory.  Asynchronous. */
 int vsp_hom_gate_batch_dev(vsp_ctx* ctx, const int32_t* kinds, const uint32_t* d_in,
                            uint32_t* d_out, size_t G, void* stream);
 
@@ -85,6 +86,38 @@ int vsp_gate_bootstrap_batch(vsp_ctx* ctx, const uint32_t* in, uint32_t* out, si
 
 /* identityKeySwitch (ops.cpp:651-679): G level-1 TLWEs -> G level-0 TLWEs (host). */
 int vsp_identity_key_switch_batch(vsp_ctx* ctx, const uint32_t* in, uint32_t* out, size_t G);
+
+/* ---- circuit bootstrapping and CMUX memory (host buffers) ---------------------- */
+
+/* circuitBootstrap (ops.cpp:914-935): C level-0 TLWEs -> C TRGSWs (level 1).
+ * Requires a key uploaded with has_cb = 1 (otherwise VSP_ERUNTIME, ops.cpp:417-423). */
+int vsp_circuit_bootstrap_batch(vsp_ctx* ctx, const uint32_t* in, uint32_t* out, size_t C);
+
+/* cmux (ops.cpp:606-626, convenience form that prepares the selector per call):
+ * out[g] = c0[g] + ExtProd(c1[g] - c0[g], sel[g]); sel: G raw TRGSWs. */
+int vsp_cmux_batch(vsp_ctx* ctx, const uint32_t* sel, const uint32_t* c1, const uint32_t* c0,
+                   uint32_t* out, size_t G);
+
+/* homMuxNoSeIks (ops.cpp:898-909): G x (sel, a, b) level-0 TLWEs -> G TRLWEs. */
+int vsp_hom_mux_no_se_iks_batch(vsp_ctx* ctx, const uint32_t* sel, const uint32_t* a,
+                                const uint32_t* b, uint32_t* out, size_t G);
+
+/* mem::ramCycle (mem.cpp:122-135): read-before-write single-port cycle.
+ * ram: w*2^v TRLWE cells, updated in place; addr: v TLWEs (LSB first); wflag: 1 TLWE;
+ * wdata: w TLWEs; readout: w TLWEs (the pre-write word). */
+int vsp_ram_cycle(vsp_ctx* ctx, uint32_t v, uint32_t w, uint32_t* ram, const uint32_t* addr,
+                  const uint32_t* wflag, const uint32_t* wdata, uint32_t* readout);
+
+/* addressToTrgsw + prepareAddress + mem::romRead (engine.cpp:133-143, mem.cpp:137-177):
+ * luts: nluts TRLWEs of an EncryptedRom of depth_bytes; addr: vrom TLWEs; out: 32 TLWEs. */
+int vsp_rom_read(vsp_ctx* ctx, uint32_t depth_bytes, const uint32_t* luts, uint32_t nluts,
+                 const uint32_t* addr, uint32_t vrom, uint32_t* out);
+
+/* blindRotate<uint64_t> (ops.cpp:713-742) with test vector (0, h[t]/2 ...): T level-0
+ * TLWEs -> T level-2 TRLWE accumulators (2 x N2 u64).  Exposed for parity tests of the
+ * circuit-bootstrapping inner loop. */
+int vsp_blind_rotate_lvl2_batch(vsp_ctx* ctx, const uint32_t* in, const uint64_t* h,
+                                uint64_t* out, size_t T);
 
 /* OpCounters (counters.hpp:11-28): cmux, blindRotate, identityKeySwitch,
  * privateKeySwitch, circuitBootstrap — counted per batched operation exactly as

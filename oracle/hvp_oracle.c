@@ -833,10 +833,12 @@ int orc_import_keys(orc_ctx* c, const uint32_t* lv0, const uint32_t* lv1,
         const size_t per2 = (size_t)2 * p->l2 * 2 * p->N2;
         c->bk2 = malloc(8 * p->n * per2);
         memcpy(c->bk2, bk2, 8 * p->n * per2);
-        c->pksNegS = malloc(4 * pks_words_p(p));
-        c->pksId = malloc(4 * pks_words_p(p));
-        memcpy(c->pksNegS, pks_negs, 4 * pks_words_p(p));
-        memcpy(c->pksId, pks_id, 4 * pks_words_p(p));
+        if (pks_negs && pks_id) {
+            c->pksNegS = malloc(4 * pks_words_p(p));
+            c->pksId = malloc(4 * pks_words_p(p));
+            memcpy(c->pksNegS, pks_negs, 4 * pks_words_p(p));
+            memcpy(c->pksId, pks_id, 4 * pks_words_p(p));
+        }
     }
     c->has_bk = 1;
     prepare_all(c);

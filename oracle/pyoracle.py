@@ -139,11 +139,12 @@ class CpuTfhe:
     def import_keys(self, k: dict):
         has_cb = k.get("bk2") is not None
         nul = ctypes.c_void_p(0)
+        has_pks = k.get("pks_id") is not None
         if self.kind == "orc":
             self._check(self.L.orc_import_keys(
                 self.h, _ptr(k["lv0"]), _ptr(k["lv1"]), _ptr(k["lv2"]), _ptr(k["bk1"]),
                 _ptr(k["bk2"]) if has_cb else nul, _ptr(k["ksk"]),
-                _ptr(k["pks_negs"]) if has_cb else nul, _ptr(k["pks_id"]) if has_cb else nul,
+                _ptr(k["pks_negs"]) if has_pks else nul, _ptr(k["pks_id"]) if has_pks else nul,
                 int(has_cb)))
         else:
             self.L.ref_import_sk(self.h, _ptr(k["lv0"]), _ptr(k["lv1"]), _ptr(k["lv2"]))
@@ -248,6 +249,15 @@ class CpuTfhe:
         out = np.zeros((2 * self.l1, 2, self.N1), np.uint32)
         self._check(self._f("circuit_bootstrap")(self.h, _ptr(np.ascontiguousarray(ct)),
                                                  _ptr(out)))
+        return out
+
+    def blind_rotate_lvl2(self, ct: np.ndarray, h: int) -> np.ndarray:
+        assert self.kind == "orc"
+        tv = np.zeros(2 * self.N2, np.uint64)
+        tv[self.N2:] = np.uint64(h // 2)
+        out = np.zeros(2 * self.N2, np.uint64)
+        self._check(self.L.orc_blind_rotate_lvl2(self.h, _ptr(np.ascontiguousarray(ct)),
+                                                 _ptr(tv), _ptr(out)))
         return out
 
     def private_key_switch(self, t2: np.ndarray, which: int):

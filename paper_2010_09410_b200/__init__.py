@@ -53,6 +53,12 @@ def lib() -> ctypes.CDLL:
         L.vsp_bootstrap_to_trlwe_batch.argtypes = [vp, vp, vp, sz]
         L.vsp_gate_bootstrap_batch.argtypes = [vp, vp, vp, sz]
         L.vsp_identity_key_switch_batch.argtypes = [vp, vp, vp, sz]
+        L.vsp_circuit_bootstrap_batch.argtypes = [vp, vp, vp, sz]
+        L.vsp_cmux_batch.argtypes = [vp, vp, vp, vp, vp, sz]
+        L.vsp_hom_mux_no_se_iks_batch.argtypes = [vp, vp, vp, vp, vp, sz]
+        L.vsp_ram_cycle.argtypes = [vp, u32, u32, vp, vp, vp, vp, vp]
+        L.vsp_rom_read.argtypes = [vp, u32, vp, u32, vp, u32, vp]
+        L.vsp_blind_rotate_lvl2_batch.argtypes = [vp, vp, vp, vp, sz]
         L.vsp_counters.argtypes = [vp, vp]
         L.vsp_counters_reset.argtypes = [vp]
         L.vsp_kernel_launches.argtypes = [vp]
@@ -120,17 +126,19 @@ class ParameterSet:
 # ---------------------------------------------------------------------------
 # client side (Alice)
 
-def keygen(params: ParameterSet, seed: int, with_cb: bool = False) -> dict:
-    """genSecretKey + BootstrappingKey::generate (ops.cpp:264-385), raw arrays."""
+def keygen(params: ParameterSet, seed: int, with_cb: bool | int = False) -> dict:
+    """genSecretKey + BootstrappingKey::generate (ops.cpp:264-385), raw arrays.
+    with_cb=2 draws bk2 but not the private key-switching tables (unit tests)."""
     p = params
+    full_cb = int(with_cb) == 1
     k = dict(
         lv0=np.zeros(p.n, np.uint32), lv1=np.zeros(p.N1, np.uint32),
         lv2=np.zeros(p.N2, np.uint32),
         bk1=np.zeros((p.n, 2 * p.l1, 2, p.N1), np.uint32),
         ksk=np.zeros(p.ksk_words(), np.uint32),
         bk2=np.zeros((p.n, 2 * p.l2, 2, p.N2), np.uint64) if with_cb else None,
-        pks_negs=np.zeros(p.pks_words(), np.uint32) if with_cb else None,
-        pks_id=np.zeros(p.pks_words(), np.uint32) if with_cb else None,
+        pks_negs=np.zeros(p.pks_words(), np.uint32) if full_cb else None,
+        pks_id=np.zeros(p.pks_words(), np.uint32) if full_cb else None,
     )
     _ccheck(lib().vsp_client_keygen(ctypes.byref(p.c), seed, int(with_cb), _ptr(k["lv0"]),
                                      _ptr(k["lv1"]), _ptr(k["lv2"]), _ptr(k["bk1"]),
@@ -202,7 +210,7 @@ class Engine:
 
     # BootstrappingKey::fromParts (ops.cpp:387-402)
     def upload_keys(self, k: dict):
-        has_cb = k.get("bk2") is not None
+        has_cb = 0 if k.get("bk2") is None else (1 if k.get("pks_id") is not None else 2)
         c = lambda a: None if a is None else np.ascontiguousarray(a)
         self._keys = {key: c(v) for key, v in k.items()}
         kk = self._keys
@@ -271,6 +279,67 @@ class Engine:
         cts = np.ascontiguousarray(np.atleast_2d(cts), np.uint32)
         out = np.zeros((cts.shape[0], self.params.n + 1), np.uint32)
         _check(lib().vsp_identity_key_switch_batch(self.h, _ptr(cts), _ptr(out), cts.shape[0]))
+        return out
+
+    # ---- circuit bootstrapping / CMUX memory -------------------------------
+    def circuit_bootstrap(self, cts: np.ndarray) -> np.ndarray:
+        """circuitBootstrap (ops.cpp:914-935); (C, n+1) -> (C, 2*l1, 2, N1)."""
+        p = self.params
+        cts = np.ascontiguousarray(np.atleast_2d(cts), np.uint32)
+        out = np.zeros((cts.shape[0], 2 * p.l1, 2, p.N1), np.uint32)
+        _check(lib().vsp_circuit_bootstrap_batch(self.h, _ptr(cts), _ptr(out), cts.shape[0]))
+        return out
+
+    def cmux(self, sel: np.ndarray, c1: np.ndarray, c0: np.ndarray) -> np.ndarray:
+        """cmux (ops.cpp:606-626) batch: sel (G, 2l, 2, N1), c1/c0 (G, 2*N1)."""
+        p = self.params
+        sel = np.ascontiguousarray(sel.reshape(-1, 2 * p.l1, 2, p.N1), np.uint32)
+        c1 = np.ascontiguousarray(c1.reshape(-1, 2 * p.N1), np.uint32)
+        c0 = np.ascontiguousarray(c0.reshape(-1, 2 * p.N1), np.uint32)
+        out = np.zeros_like(c1)
+        _check(lib().vsp_cmux_batch(self.h, _ptr(sel), _ptr(c1), _ptr(c0), _ptr(out), c1.shape[0]))
+        return out
+
+    def hom_mux_no_se_iks(self, sel, a, b) -> np.ndarray:
+        """homMuxNoSeIks (ops.cpp:898-909) batch: (G, n+1) x3 -> (G, 2*N1)."""
+        p = self.params
+        f = lambda x: np.ascontiguousarray(np.atleast_2d(x), np.uint32)
+        sel, a, b = f(sel), f(a), f(b)
+        out = np.zeros((sel.shape[0], 2 * p.N1), np.uint32)
+        _check(lib().vsp_hom_mux_no_se_iks_batch(self.h, _ptr(sel), _ptr(a), _ptr(b), _ptr(out),
+                                                 sel.shape[0]))
+        return out
+
+    def ram_cycle(self, ram: np.ndarray, v: int, w: int, addr, wflag, wdata):
+        """mem::ramCycle (mem.cpp:122-135).  Returns (readOut (w, n+1), new ram)."""
+        p = self.params
+        if len(addr) != v:
+            raise ValueError("ramCycle: address width mismatch")
+        ram = np.ascontiguousarray(np.array(ram, np.uint32).reshape((w << v), 2 * p.N1))
+        a = np.ascontiguousarray(addr, np.uint32)
+        f = np.ascontiguousarray(wflag, np.uint32)
+        d = np.ascontiguousarray(wdata, np.uint32)
+        ro = np.zeros((w, p.n + 1), np.uint32)
+        _check(lib().vsp_ram_cycle(self.h, v, w, _ptr(ram), _ptr(a), _ptr(f), _ptr(d), _ptr(ro)))
+        return ro, ram
+
+    def rom_read(self, luts: np.ndarray, depth_bytes: int, addr) -> np.ndarray:
+        """addressToTrgsw + romRead (engine.cpp:133-143): 32 TLWEs."""
+        p = self.params
+        luts = np.ascontiguousarray(luts, np.uint32)
+        a = np.ascontiguousarray(addr, np.uint32)
+        out = np.zeros((32, p.n + 1), np.uint32)
+        _check(lib().vsp_rom_read(self.h, depth_bytes, _ptr(luts), luts.shape[0], _ptr(a),
+                                  a.shape[0], _ptr(out)))
+        return out
+
+    def blind_rotate_lvl2(self, cts: np.ndarray, h) -> np.ndarray:
+        p = self.params
+        cts = np.ascontiguousarray(np.atleast_2d(cts), np.uint32)
+        hv = np.ascontiguousarray(np.broadcast_to(np.asarray(h, np.uint64), (cts.shape[0],)))
+        out = np.zeros((cts.shape[0], 2 * p.N2), np.uint64)
+        _check(lib().vsp_blind_rotate_lvl2_batch(self.h, _ptr(cts), _ptr(hv), _ptr(out),
+                                                 cts.shape[0]))
         return out
 
     def counters(self) -> dict:

@@ -255,56 +255,84 @@ __global__ void gate_prep_kernel(const int* __restrict__ kinds, const uint32_t* 
 // ---------------------------------------------------------------------------
 // Batched identity key switch (ops.cpp:651-679) fused with sampleExtract(.,0)
 // (ops.cpp:628-643) and the MUX level-1 sum (ops.cpp:886-892).
-// One CTA handles GT gates x all n+1 output coordinates; for every (i, j) it reads
-// the (2^b - 1) candidate KSK rows once (coalesced) and each gate selects its row
-// by digit, so the KSK is streamed once per GT gates instead of once per gate.
-// Source of level-1 input for listed gate g: TRLWE of task t0 (+ task t1 + mu).
+//
+// out[g][k] = b'_g [k == n] - sum_{i,j} ksk[i][j][d_g(i,j) - 1][k]   (mod 2^32)
+//
+// Grid (ceil(Gl/GT), KSPLIT): CTA (x, y) handles GT gates x all n+1 coordinates over
+// the slice y of the input index i.  For every (i, j) the CTA reads the (2^b - 1)
+// candidate KSK rows once (coalesced) and each gate selects its row by digit, so the
+// KSK is streamed once per GT gates; slices are combined with wrap-around u32
+// atomics into `out`, which iks_init_kernel pre-sets to (0,...,0, b').  Integer
+// addition is associative, so the result is independent of the order.
+// Coefficient i of sampleExtract(TRLWE, k) (ops.cpp:628-643): a'[i] = A[k-i] (i <= k),
+// -A[N+k-i] (i > k).
+__device__ __forceinline__ uint32_t se_coef(const uint32_t* A, int N, int k, int i)
+{
+    return i <= k ? A[k - i] : 0u - A[N + k - i];
+}
+
+__device__ __forceinline__ void iks_level1_coef(const uint32_t* __restrict__ trlwe, int2 tt, int N,
+                                                int k, int i, uint32_t& a)
+{
+    a = se_coef(trlwe + (size_t)tt.x * 2 * N, N, k, i);
+    if (tt.y >= 0)
+        a += se_coef(trlwe + (size_t)tt.y * 2 * N, N, k, i);
+}
+
+__global__ void iks_init_kernel(const uint32_t* __restrict__ trlwe, const int2* __restrict__ gtask,
+                                const int* __restrict__ glist, const int* __restrict__ seidx,
+                                int Gl, uint32_t* __restrict__ out, int n, int N)
+{
+    const int gi = blockIdx.x;
+    if (gi >= Gl)
+        return;
+    const int gate = glist[gi];
+    const int2 tt = gtask[gate];
+    const int se = seidx ? seidx[gate] : 0;
+    for (int k = threadIdx.x; k <= n; k += blockDim.x) {
+        uint32_t v = 0;
+        if (k == n) {
+            v = trlwe[(size_t)tt.x * 2 * N + N + se];
+            if (tt.y >= 0)
+                v += trlwe[(size_t)tt.y * 2 * N + N + se] + kMu32;
+        }
+        out[(size_t)gate * (n + 1) + k] = v;
+    }
+}
+
 template <int BASEBITS, int GT, int KPT>
 __global__ void __launch_bounds__(256) iks_kernel(
     const uint32_t* __restrict__ trlwe, const int2* __restrict__ gtask,
-    const int* __restrict__ glist, int Gl, const uint32_t* __restrict__ ksk,
-    uint32_t* __restrict__ out, int n, int N, int t)
+    const int* __restrict__ glist, const int* __restrict__ seidx, int Gl,
+    const uint32_t* __restrict__ ksk, uint32_t* __restrict__ out, int n, int N, int t)
 {
     static_assert(GT * BASEBITS <= 64, "digit packing");
     constexpr uint32_t kMask = (1u << BASEBITS) - 1;
     constexpr int kPerBase = (1 << BASEBITS) - 1;
-    extern __shared__ __align__(16) uint64_t dig[];  // [N * t]
-    __shared__ uint32_t bsh[GT];
+    extern __shared__ __align__(16) uint64_t dig[];  // [islice * t]
     const int g0 = blockIdx.x * GT;
     const int ng = min(GT, Gl - g0);
+    const int islice = N / gridDim.y;
+    const int i0 = blockIdx.y * islice;
     const uint32_t offset = (uint32_t)(BASEBITS * t >= 32 ? 0u : 1u << (32 - (1 + BASEBITS * t)));
 
-    // digits of the sample-extracted level-1 TLWE of every gate in the tile
-    for (int i = threadIdx.x; i < N; i += blockDim.x) {
-        uint64_t word[16];
+    for (int ii = threadIdx.x; ii < islice; ii += blockDim.x) {
+        uint64_t word[8];
 #pragma unroll
-        for (int j = 0; j < 16; j++)
+        for (int j = 0; j < 8; j++)
             word[j] = 0;
         for (int g = 0; g < ng; g++) {
+            uint32_t a;
             const int gate = glist[g0 + g];
-            const int2 tt = gtask[gate];
-            const uint32_t* A = trlwe + (size_t)tt.x * 2 * N;
-            uint32_t a = (i == 0) ? A[0] : 0u - A[N - i];
-            if (tt.y >= 0) {
-                const uint32_t* B = trlwe + (size_t)tt.y * 2 * N;
-                a += (i == 0) ? B[0] : 0u - B[N - i];
-            }
+            iks_level1_coef(trlwe, gtask[gate], N, seidx ? seidx[gate] : 0, i0 + ii, a);
             const uint32_t v = a + offset;
-            for (int j = 0; j < t; j++) {
-                const uint64_t d = (v >> (32 - (j + 1) * BASEBITS)) & kMask;
-                word[j] |= d << (g * BASEBITS);
-            }
+#pragma unroll
+            for (int j = 0; j < 8; j++)
+                if (j < t)
+                    word[j] |= (uint64_t)((v >> (32 - (j + 1) * BASEBITS)) & kMask) << (g * BASEBITS);
         }
         for (int j = 0; j < t; j++)
-            dig[i * t + j] = word[j];
-    }
-    if (threadIdx.x < ng) {
-        const int gate = glist[g0 + threadIdx.x];
-        const int2 tt = gtask[gate];
-        uint32_t b = trlwe[(size_t)tt.x * 2 * N + N];
-        if (tt.y >= 0)
-            b += trlwe[(size_t)tt.y * 2 * N + N] + kMu32;
-        bsh[threadIdx.x] = b;
+            dig[ii * t + j] = word[j];
     }
     __syncthreads();
 
@@ -312,18 +340,17 @@ __global__ void __launch_bounds__(256) iks_kernel(
 #pragma unroll
     for (int g = 0; g < GT; g++)
 #pragma unroll
-        for (int kk = 0; kk < KPT; kk++) {
-            const int k = threadIdx.x + kk * 256;
-            acc[g][kk] = (k == n && g < ng) ? bsh[g] : 0u;
-        }
+        for (int kk = 0; kk < KPT; kk++)
+            acc[g][kk] = 0u;
 
     const size_t rowStride = (size_t)n + 1;
+    const uint32_t* kbase = ksk + (size_t)i0 * t * kPerBase * rowStride;
 #pragma unroll 1
-    for (int ij = 0; ij < N * t; ij++) {
+    for (int ij = 0; ij < islice * t; ij++) {
         const uint64_t dd = dig[ij];
         if (dd == 0)
             continue;
-        const uint32_t* base = ksk + (size_t)ij * kPerBase * rowStride;
+        const uint32_t* base = kbase + (size_t)ij * kPerBase * rowStride;
 #pragma unroll
         for (int kk = 0; kk < KPT; kk++) {
             const int k = threadIdx.x + kk * 256;
@@ -338,7 +365,7 @@ __global__ void __launch_bounds__(256) iks_kernel(
                     const uint32_t d = (uint32_t)(dd >> (2 * g)) & 3u;
                     const uint32_t lo = (d & 1u) ? r1 : 0u;
                     const uint32_t hi = (d & 1u) ? r3 : r2;
-                    acc[g][kk] -= (d & 2u) ? hi : lo;
+                    acc[g][kk] += (d & 2u) ? hi : lo;
                 }
             }
             else {
@@ -346,7 +373,7 @@ __global__ void __launch_bounds__(256) iks_kernel(
                 for (int g = 0; g < GT; g++) {
                     const uint32_t d = (uint32_t)(dd >> (BASEBITS * g)) & kMask;
                     if (d)
-                        acc[g][kk] -= __ldg(base + (size_t)(d - 1) * rowStride + k);
+                        acc[g][kk] += __ldg(base + (size_t)(d - 1) * rowStride + k);
                 }
             }
         }
@@ -359,8 +386,8 @@ __global__ void __launch_bounds__(256) iks_kernel(
 #pragma unroll
         for (int kk = 0; kk < KPT; kk++) {
             const int k = threadIdx.x + kk * 256;
-            if (k <= n)
-                out[(size_t)gate * (n + 1) + k] = acc[g][kk];
+            if (k <= n && acc[g][kk] != 0u)
+                atomicAdd(out + (size_t)gate * (n + 1) + k, 0u - acc[g][kk]);
         }
     }
 }

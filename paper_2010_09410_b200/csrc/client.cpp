@@ -233,7 +233,8 @@ const char* vsp_client_last_error(void) { return g_cerr.c_str(); }
 
 // genSecretKey + BootstrappingKey::generate (ops.cpp:264-385) from Csprng::fromSeed(seed).
 // Output buffers: lv0[n], lv1[N1], lv2[N2], bk1[n*2l1*2*N1], ksk[...]; bk2/pks only
-// when with_cb (may be NULL otherwise).
+// when with_cb (may be NULL otherwise).  with_cb == 2 draws bk2 but stops before the
+// private key-switching tables (identical bk2; used by level-2 unit tests).
 int vsp_client_keygen(const vsp_params* pp, uint64_t seed, int with_cb, uint32_t* lv0,
                       uint32_t* lv1, uint32_t* lv2, uint32_t* bk1, uint32_t* ksk, uint64_t* bk2,
                       uint32_t* pks_negs, uint32_t* pks_id)
@@ -285,7 +286,7 @@ int vsp_client_keygen(const vsp_params* pp, uint64_t seed, int with_cb, uint32_t
         }
         // private key switching keys (ops.cpp:315-351)
         std::vector<ZeroEnc<uint32_t>> jp;
-        if (with_cb) {
+        if (with_cb == 1) {
             const uint32_t perBase = (1u << p.pksBaseBits) - 1;
             for (int which = 0; which < 2; which++) {
                 uint32_t* d = which == 0 ? pks_negs : pks_id;
@@ -319,7 +320,7 @@ int vsp_client_keygen(const vsp_params* pp, uint64_t seed, int with_cb, uint32_t
                 }
         }
         // PKS messages: func * key2[i] * (u+1) / base^(j+1) on b (ops.cpp:332-341)
-        if (with_cb) {
+        if (with_cb == 1) {
             const uint32_t perBase = (1u << p.pksBaseBits) - 1;
             for (int which = 0; which < 2; which++) {
                 uint32_t* d = which == 0 ? pks_negs : pks_id;

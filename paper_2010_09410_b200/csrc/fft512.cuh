@@ -22,8 +22,13 @@
 
 namespace vsp {
 
-// zeta_{d,b} for stages 0..3: index (1<<d)-1+b.  Filled by the host (capi).
-__constant__ double2 c_tw1[15];
+// zeta_{d,b} for stages 0..3 (index (1<<d)-1+b) of the 512-point transform rooted at
+// Y^512 = c_ROOT, for the three roots in use (filled by the host):
+//   ROOT 0: c = i            (level 1: X^1024 + 1 folded to Y^512 = i)
+//   ROOT 1: c = e^{i pi/4}   (level 2, branch 0 of Y^1024 = i)
+//   ROOT 2: c = e^{i 5pi/4}  (level 2, branch 1)
+// The per-lane table tw2 (stages 4-8) is likewise per root.
+__constant__ double2 c_tw1[3][15];
 
 constexpr int kFftXbufStride = 544;  // 512 + 32 swizzle pad (double2 units)
 constexpr int kTw2Entries = 23;      // 1+2+4+8 (stages 4-7) + 8 (stage 8)
@@ -57,6 +62,7 @@ __device__ __forceinline__ double2 shfl_xor_d2(double2 v, int m)
 
 // Forward transform in place.  xbuf: per-warp smem, kFftXbufStride double2.
 // tw2: smem table [kTw2Entries][32] double2.
+template <int ROOT = 0>
 __device__ __forceinline__ void fft512_fwd(double2 (&v)[16], double2* xbuf,
                                            const double2* tw2, int lane)
 {
@@ -66,7 +72,7 @@ __device__ __forceinline__ void fft512_fwd(double2 (&v)[16], double2* xbuf,
 #pragma unroll
         for (int j = 0; j < 16; j++)
             if ((j & h) == 0)
-                bf_fwd(v[j], v[j + h], c_tw1[(1 << d) - 1 + (j >> (4 - d))]);
+                bf_fwd(v[j], v[j + h], c_tw1[ROOT][(1 << d) - 1 + (j >> (4 - d))]);
     }
     __syncwarp();
 #pragma unroll
@@ -99,6 +105,7 @@ __device__ __forceinline__ void fft512_fwd(double2 (&v)[16], double2* xbuf,
 }
 
 // Exact inverse of fft512_fwd up to the factor 512 (folded into the key).
+template <int ROOT = 0>
 __device__ __forceinline__ void fft512_inv(double2 (&v)[16], double2* xbuf,
                                            const double2* tw2, int lane)
 {
@@ -135,7 +142,7 @@ __device__ __forceinline__ void fft512_inv(double2 (&v)[16], double2* xbuf,
 #pragma unroll
         for (int j = 0; j < 16; j++)
             if ((j & h) == 0)
-                bf_inv(v[j], v[j + h], c_tw1[(1 << d) - 1 + (j >> (4 - d))]);
+                bf_inv(v[j], v[j + h], c_tw1[ROOT][(1 << d) - 1 + (j >> (4 - d))]);
     }
 }
 

@@ -1,0 +1,326 @@
+// Circuit bootstrapping (level 2, N2 = 2048, 64-bit torus) for tfhe-80.
+//
+// Reference: circuitBootstrap (ops.cpp:914-935) = for i < l1:
+//   blindRotate<uint64_t>(ct, bk2, testvec b == h/2) (ops.cpp:713-742) -> sampleExtract(.,0)
+//   -> b += h/2 -> privateKeySwitch (ops.cpp:681-708) with pksNegS and pksId.
+//
+// The reference multiplies level-2 polynomials in double precision after casting the
+// 64-bit torus words to double (fft.hpp:64-75), which is only accurate to ~2^30
+// (test_tfhe.cpp:142-175).  Here every BK2 word is split exactly into two signed
+// 32-bit halves, x = hi * 2^32 + lo, and both halves go through the FFT; each partial
+// product is an exact integer below 2^53, so the external product is EXACT mod 2^64
+// (the reference's MulBackend::Exact result), at the cost of a second MAC/inverse.
+//
+// The 1024-point transform (Y^1024 = i) is one split stage into Y^512 = +-sqrt(i)
+// followed by two 512-point warp transforms (fft512 ROOT 1 / ROOT 2).
+#pragma once
+
+#include "fft512.cuh"
+
+namespace vsp {
+
+// s = sqrt(i) = e^{i pi/4}
+__device__ __forceinline__ double2 split_fwd(double2 u, double2 v, int branch)
+{
+    const double c = 0.70710678118654752440;
+    const double sx = c * (v.x - v.y), sy = c * (v.x + v.y);  // s * v
+    return branch == 0 ? make_double2(u.x + sx, u.y + sy) : make_double2(u.x - sx, u.y - sy);
+}
+
+// ---------------------------------------------------------------------------
+// BK2 preparation: raw u64 rows [i][r][poly][2048] -> [i][r][q][branch][j][lane]
+// double2 with q = poly*2 + half (half 0 = signed low word, 1 = high word), scaled by
+// 1/1024.  One warp per (i, r, q, branch).
+__global__ void __launch_bounds__(64) prepare_bk2_kernel(const uint64_t* __restrict__ raw,
+                                                          const double2* __restrict__ tw2g,
+                                                          double2* __restrict__ out, int jobs)
+{
+    __shared__ double2 tw2[2][kTw2Entries * 32];
+    __shared__ double2 xb[2][kFftXbufStride];
+    for (int i = threadIdx.x; i < 2 * kTw2Entries * 32; i += blockDim.x)
+        tw2[i / (kTw2Entries * 32)][i % (kTw2Entries * 32)] = tw2g[kTw2Entries * 32 + i];
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int job = blockIdx.x * 2 + warp;
+    if (job >= jobs)
+        return;
+    const int branch = job & 1, q = (job >> 1) & 3, ir = job >> 3;  // ir = i*8 + r
+    const int poly = q >> 1, half = q & 1;
+    const uint64_t* src = raw + ((size_t)ir * 2 + poly) * 2048;
+    auto word = [&](int k) -> double {
+        const uint64_t x = src[k];
+        const int32_t lo = (int32_t)(uint32_t)x;
+        if (half == 0)
+            return (double)lo;
+        const uint64_t h = (x - (uint64_t)(int64_t)lo) >> 32;
+        return (double)(int32_t)(uint32_t)h;
+    };
+    double2 z[16];
+#pragma unroll
+    for (int j = 0; j < 16; j++) {
+        const int p = lane + 32 * j;
+        const double2 u = make_double2(word(p), word(p + 1024));
+        const double2 v = make_double2(word(p + 512), word(p + 1536));
+        z[j] = split_fwd(u, v, branch);
+    }
+    if (branch == 0)
+        fft512_fwd<1>(z, xb[warp], tw2[0], lane);
+    else
+        fft512_fwd<2>(z, xb[warp], tw2[1], lane);
+    double2* dst = out + (size_t)job * 512;
+    const double sc = 1.0 / 1024.0;
+#pragma unroll
+    for (int j = 0; j < 16; j++)
+        dst[j * 32 + lane] = make_double2(z[j].x * sc, z[j].y * sc);
+}
+
+// ---------------------------------------------------------------------------
+// Level-2 blind rotation, one CTA (8 warps) per task.  Task t rotates the test vector
+// (0, h/2 ... h/2) with h = hv[t] by the level-0 TLWE tasks[t % ninputs]; the accumulator
+// (2 x 2048 u64) is written to out[t].
+constexpr int kRegion = kFftXbufStride;  // double2 per smem region (8704 B)
+
+struct Br2Smem {
+    uint64_t acc[2][2048];
+    double2 reg[16][kRegion];
+    double2 tw2[2][kTw2Entries * 32];
+};
+
+__global__ void __launch_bounds__(256, 1)
+    br2_kernel(const uint32_t* __restrict__ tasks, int ninputs, const uint64_t* __restrict__ hv,
+               const double2* __restrict__ bk2fd, const double2* __restrict__ tw2g,
+               uint64_t* __restrict__ out, int n, int bgbits)
+{
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    Br2Smem& sm = *reinterpret_cast<Br2Smem*>(smem_raw);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t* lwe = tasks + (size_t)(blockIdx.x % ninputs) * (n + 1);
+    for (int i = tid; i < 2 * kTw2Entries * 32; i += blockDim.x)
+        sm.tw2[i / (kTw2Entries * 32)][i % (kTw2Entries * 32)] = tw2g[kTw2Entries * 32 + i];
+    {
+        const uint64_t h2 = hv[blockIdx.x] / 2;
+        const uint32_t rot = (4096u - mod_switch_2n(lwe[n], 12)) & 4095u;
+        for (int q = tid; q < 2048; q += blockDim.x) {
+            sm.acc[0][q] = 0;
+            uint64_t val;
+            if (rot < 2048)
+                val = ((uint32_t)q < rot) ? (0ull - h2) : h2;
+            else
+                val = ((uint32_t)q < rot - 2048) ? h2 : (0ull - h2);
+            sm.acc[1][q] = val;
+        }
+    }
+    __syncthreads();
+    // decomposePoly<uint64_t> constants (poly.hpp:79-97), l2 = 4
+    const uint64_t half = 1ull << (bgbits - 1);
+    const uint64_t mask = (1ull << bgbits) - 1;
+    uint64_t offset = 0;
+    for (int i = 1; i <= 4; i++)
+        offset += half << (64 - i * bgbits);
+
+#pragma unroll 1
+    for (int i = 0; i < n; i++) {
+        const uint32_t bara = mod_switch_2n(lwe[i], 12);
+        // ---- phase A: row r = warp (poly r/4, digit level r%4), forward transforms
+        {
+            const int P = warp >> 2, L = warp & 3;
+            const uint64_t* src = sm.acc[P];
+            const int sh = 64 - (L + 1) * bgbits;
+            auto digit = [&](uint32_t q) -> double {
+                const uint32_t idx = (q - bara) & 4095u;
+                const uint64_t r = idx < 2048 ? src[idx] : 0ull - src[idx - 2048];
+                const uint64_t v = r - src[q] + offset;
+                return (double)(int32_t)(int64_t)(((v >> sh) & mask) - half);
+            };
+            double2 z0[16], z1[16];
+#pragma unroll
+            for (int j = 0; j < 16; j++) {
+                const uint32_t p = lane + 32 * j;
+                const double2 u = make_double2(digit(p), digit(p + 1024));
+                const double2 v = make_double2(digit(p + 512), digit(p + 1536));
+                z0[j] = split_fwd(u, v, 0);
+                z1[j] = split_fwd(u, v, 1);
+            }
+            double2* r0 = sm.reg[2 * warp];
+            double2* r1 = sm.reg[2 * warp + 1];
+            fft512_fwd<1>(z0, r0, sm.tw2[0], lane);
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < 16; j++)
+                r0[j * 32 + lane] = z0[j];
+            fft512_fwd<2>(z1, r1, sm.tw2[1], lane);
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < 16; j++)
+                r1[j * 32 + lane] = z1[j];
+        }
+        __syncthreads();
+        // ---- phase B: MAC over the 8 rows for 4 outputs (a_lo, a_hi, b_lo, b_hi)
+        {
+            const double2* K = bk2fd + (size_t)i * 8 * 4 * 1024;
+#pragma unroll 1
+            for (int m = 0; m < 4; m++) {
+                const int f = tid + 256 * m;
+                const int b = f >> 9, s = f & 511;
+                double2 o[4];
+#pragma unroll
+                for (int q = 0; q < 4; q++)
+                    o[q] = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int r = 0; r < 8; r++) {
+                    const double2 d = sm.reg[2 * r + b][s];
+#pragma unroll
+                    for (int q = 0; q < 4; q++) {
+                        const double2 k = __ldg(K + ((size_t)(r * 4 + q)) * 1024 + f);
+                        o[q].x = fma(d.x, k.x, fma(-d.y, k.y, o[q].x));
+                        o[q].y = fma(d.x, k.y, fma(d.y, k.x, o[q].y));
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < 4; q++)
+                    sm.reg[2 * q + b][s] = o[q];
+            }
+        }
+        __syncthreads();
+        // ---- phase C: inverse 512-point transforms, warp = (q, branch)
+        {
+            const int q = warp >> 1, b = warp & 1;
+            double2* rg = sm.reg[2 * q + b];
+            double2 v[16];
+#pragma unroll
+            for (int j = 0; j < 16; j++)
+                v[j] = rg[j * 32 + lane];
+            __syncwarp();
+            if (b == 0)
+                fft512_inv<1>(v, rg, sm.tw2[0], lane);
+            else
+                fft512_inv<2>(v, rg, sm.tw2[1], lane);
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < 16; j++)
+                rg[lane + 32 * j] = v[j];
+        }
+        __syncthreads();
+        // ---- phase D: inverse split stage, exact rounding, lo/hi recombination
+        {
+            const double c = 0.70710678118654752440;
+#pragma unroll 1
+            for (int w = 0; w < 2; w++) {
+                const int p = tid + 256 * w;
+#pragma unroll
+                for (int P = 0; P < 2; P++) {
+                    int64_t part[2][4];
+#pragma unroll
+                    for (int hh = 0; hh < 2; hh++) {
+                        const int q = 2 * P + hh;
+                        const double2 A = sm.reg[2 * q][p], B = sm.reg[2 * q + 1][p];
+                        const double2 u = make_double2(A.x + B.x, A.y + B.y);
+                        const double dx = A.x - B.x, dy = A.y - B.y;
+                        // (A - B) * conj(s), s = c (1 + i)
+                        const double2 v = make_double2(c * (dx + dy), c * (dy - dx));
+                        part[hh][0] = __double2ll_rn(u.x);  // coefficient p
+                        part[hh][1] = __double2ll_rn(v.x);  // p + 512
+                        part[hh][2] = __double2ll_rn(u.y);  // p + 1024
+                        part[hh][3] = __double2ll_rn(v.y);  // p + 1536
+                    }
+#pragma unroll
+                    for (int e = 0; e < 4; e++) {
+                        const uint64_t val =
+                            (uint64_t)part[0][e] + ((uint64_t)part[1][e] << 32);
+                        sm.acc[P][p + 512 * e] += val;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+    uint64_t* dst = out + (size_t)blockIdx.x * 4096;
+    for (int q = tid; q < 4096; q += blockDim.x)
+        dst[q] = (&sm.acc[0][0])[q];
+}
+
+// ---------------------------------------------------------------------------
+// Batched private key switch (ops.cpp:681-708), fused with sampleExtract(acc2, 0)
+// and b += h/2 (ops.cpp:928-930).  Input task g: level-2 accumulator acc2[g]
+// (a[2048], b[2048] u64); out_rows[g] receives -sum_{i,j} table[i][j][d-1] for
+// table 0 (pksNegS) into row rowA[g] and table 1 (pksId) into row rowB[g] of the
+// destination (each row 2*N1 u32, pre-zeroed).
+// Grid: (islices, N1*2 / 512, 2 tables); CTA: 256 threads x 2 coordinates x GT tasks.
+template <int GT>
+__global__ void __launch_bounds__(256) pks_kernel(const uint64_t* __restrict__ acc2,
+                                                  const uint64_t* __restrict__ hv, int T2,
+                                                  const uint32_t* __restrict__ pks_negs,
+                                                  const uint32_t* __restrict__ pks_id,
+                                                  uint32_t* __restrict__ dst,
+                                                  const int* __restrict__ rowA,
+                                                  const int* __restrict__ rowB, int N2, int N1,
+                                                  int basebits, int t)
+{
+    extern __shared__ uint32_t pk[];  // [islice][GT]: top (basebits*t) bits of v
+    const int islice = (N2 + 1 + gridDim.x - 1) / gridDim.x;
+    const int i0 = blockIdx.x * islice;
+    const int i1 = min(N2 + 1, i0 + islice);
+    const int table = blockIdx.z;
+    const uint32_t* tab = table == 0 ? pks_negs : pks_id;
+    const int nb = basebits * t;  // digits kept (30 for tfhe-80)
+    const uint64_t offset = nb >= 64 ? 0ull : 1ull << (64 - (1 + nb));
+    const int perBase = (1 << basebits) - 1;
+    const uint32_t dmask = (1u << basebits) - 1;
+    for (int g0 = 0; g0 < T2; g0 += GT) {
+        const int ng = min(GT, T2 - g0);
+        __syncthreads();
+        for (int x = threadIdx.x; x < (i1 - i0) * GT; x += blockDim.x) {
+            const int ii = x / GT, g = x % GT;
+            uint32_t w = 0;
+            if (g < ng) {
+                const int i = i0 + ii;
+                const uint64_t* A = acc2 + (size_t)(g0 + g) * 2 * N2;
+                uint64_t val;
+                if (i < N2)
+                    val = (i == 0) ? A[0] : 0ull - A[N2 - i];
+                else
+                    val = A[N2] + hv[g0 + g] / 2;
+                const uint64_t v = val + offset;
+                w = (uint32_t)(v >> (64 - nb));
+            }
+            pk[x] = w;
+        }
+        __syncthreads();
+        const int k = (blockIdx.y * 256 + threadIdx.x) * 2;
+        const bool kvalid = k < 2 * N1;
+        uint32_t acc[GT][2];
+#pragma unroll
+        for (int g = 0; g < GT; g++)
+            acc[g][0] = acc[g][1] = 0;
+        for (int i = i0; i < i1; i++) {
+            for (int j = 0; j < t; j++) {
+                const uint32_t* base = tab + ((size_t)i * t + j) * perBase * 2 * N1 + k;
+#pragma unroll
+                for (int g = 0; g < GT; g++) {
+                    const uint32_t d = (pk[(i - i0) * GT + g] >> (nb - (j + 1) * basebits)) & dmask;
+                    if (d && kvalid) {
+                        const uint2 r = __ldg(reinterpret_cast<const uint2*>(
+                            base + (size_t)(d - 1) * 2 * N1));
+                        acc[g][0] += r.x;
+                        acc[g][1] += r.y;
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int g = 0; g < GT; g++) {
+            if (g >= ng)
+                break;
+            if (!kvalid)
+                break;
+            const int row = table == 0 ? rowA[g0 + g] : rowB[g0 + g];
+            uint32_t* o = dst + (size_t)row * 2 * N1 + k;
+            if (acc[g][0])
+                atomicAdd(o, 0u - acc[g][0]);
+            if (acc[g][1])
+                atomicAdd(o + 1, 0u - acc[g][1]);
+        }
+    }
+}
+
+}  // namespace vsp

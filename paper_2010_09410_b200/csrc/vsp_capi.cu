@@ -17,7 +17,9 @@
 
 #include "../../include/vsp_b200.h"
 #include "bootstrap.cuh"
+#include "cmux.cuh"
 #include "exact.cuh"
+#include "level2.cuh"
 #include "vsp_common.cuh"
 
 using namespace vsp;
@@ -88,17 +90,40 @@ int ilog2(uint32_t x)
     return r;
 }
 
-// zeta_{d,b} = exp(i pi (2^-(d+2) + bitrev_d(b) / 2^d)): the root used by the
-// butterfly that splits block b at depth d of the negacyclic transform.
-double2 zeta(int d, uint32_t b)
+// Twiddle of the butterfly that splits block b at depth d of a negacyclic transform
+// rooted at Y^M = e^{i theta0}: zeta = exp(i (theta0 / 2^d + 2 pi bitrev_d(b) / 2^d) / 2).
+// theta0 = pi/2 (root i), pi/4 and 5pi/4 (the two halves of the level-2 transform).
+const long double kPi = 3.141592653589793238462643383279502884L;
+
+double2 zeta_root(long double theta0, int d, uint32_t b)
 {
     uint32_t r = 0;
     for (int i = 0; i < d; i++)
         r = (r << 1) | ((b >> i) & 1u);
-    const long double pi = 3.141592653589793238462643383279502884L;
-    const long double ang =
-        pi * (1.0L / (long double)(1u << (d + 2)) + (long double)r / (long double)(1u << d));
-    return make_double2((double)cosl(ang), (double)sinl(ang));
+    const long double th =
+        theta0 / (long double)(1u << d) + 2.0L * kPi * (long double)r / (long double)(1u << d);
+    return make_double2((double)cosl(th / 2), (double)sinl(th / 2));
+}
+
+long double root_theta(int root) { return root == 0 ? kPi / 2 : root == 1 ? kPi / 4 : 5 * kPi / 4; }
+
+// tw1 (15 constants) and the per-lane tw2 table [23][32] of one root.
+void twiddles(int root, double2* tw1, std::vector<double2>& tw2)
+{
+    const long double t0 = root_theta(root);
+    for (int d = 0; d < 4; d++)
+        for (int b = 0; b < (1 << d); b++)
+            tw1[(1 << d) - 1 + b] = zeta_root(t0, d, (uint32_t)b);
+    tw2.assign(kTw2Entries * 32, make_double2(0, 0));
+    for (int L = 0; L < 32; L++) {
+        const uint32_t hi = L >> 1, odd = L & 1;
+        int e = 0;
+        for (int d = 4; d < 8; d++)
+            for (uint32_t s = 0; s < (1u << (d - 4)); s++)
+                tw2[(e++) * 32 + L] = zeta_root(t0, d, (hi << (d - 4)) | s);
+        for (uint32_t k = 0; k < 8; k++)
+            tw2[(e++) * 32 + L] = zeta_root(t0, 8, hi * 16 + k + 8 * odd);
+    }
 }
 
 }  // namespace
@@ -113,11 +138,16 @@ struct vsp_ctx {
     uint32_t* d_bk1raw = nullptr;  // Exact path: raw TRGSW words
     uint32_t* d_ksk = nullptr;
     uint64_t* d_bk2raw = nullptr;
+    double2* d_bk2fd = nullptr;    // FFT path: n x 8 rows x 4 (poly,half) x 1024 double2
     uint32_t* d_pks[2] = {nullptr, nullptr};
-    double2* d_tw2 = nullptr;      // [23][32] per-lane twiddles of the 512-point transform
+    uint64_t* d_tv2[2] = {nullptr, nullptr};  // exact path level-2 test vectors (h/2), lev 0/1
+    double2* d_tw2 = nullptr;      // [3 roots][23][32] per-lane twiddles (512-point transforms)
     uint32_t* d_tv1 = nullptr;     // level-1 test vector (0, mu...mu) for the exact path
     // scratch
     DevBuf tasks, trlwe, in, out, kinds, gtask, glist;
+    // memory-path scratch
+    DevBuf acc2, hv, rows, cbraw, selraw, selfd, chains, layerA, layerB, ram, aux, aux2, seidx,
+        pairs;
     uint64_t counters[5] = {0, 0, 0, 0, 0};
     uint64_t launches = 0;
     std::mutex mu;
@@ -175,6 +205,7 @@ void validate(const Params& p)  // ParameterSet::validate (params.cpp:17-29)
 // Kernel configuration of the level-1 FFT blind rotation.
 constexpr int kBrWarps = 8;
 constexpr int kBrSlots = 4;
+constexpr int kChainWarps = 8;
 
 void launch_br(vsp_ctx* c, const uint32_t* d_tasks, uint32_t* d_trlwe, int T, cudaStream_t st)
 {
@@ -203,62 +234,81 @@ void launch_br(vsp_ctx* c, const uint32_t* d_tasks, uint32_t* d_trlwe, int T, cu
     c->counters[1] += (uint64_t)T;
 }
 
+int iks_split(int tiles, int N)
+{
+    // enough CTAs for ~4 waves of 148 SMs; power of two dividing N
+    int s = 1;
+    while (s < 64 && s * 2 <= N && tiles * s < 4 * 148)
+        s *= 2;
+    return s;
+}
+
 void launch_iks(vsp_ctx* c, const uint32_t* d_trlwe, const int2* d_gtask, const int* d_glist,
-                int Gl, uint32_t* d_out, cudaStream_t st)
+                int Gl, uint32_t* d_out, cudaStream_t st, const int* d_seidx = nullptr)
 {
     if (Gl == 0)
         return;
     const Params& p = c->p;
-    const size_t smem = (size_t)p.N1 * p.ksLen * sizeof(uint64_t);
     const int kpt = (int)((p.n + 1 + 255) / 256);
     timed(c, "iks", st, [&] {
-    if (p.ksBaseBits == 2) {
-        constexpr int GT = 32;
-        const int grid = (Gl + GT - 1) / GT;
-        if (kpt == 1)
-            iks_kernel<2, GT, 1><<<grid, 256, smem, st>>>(d_trlwe, d_gtask, d_glist, Gl, c->d_ksk,
-                                                          d_out, p.n, p.N1, p.ksLen);
-        else if (kpt == 2)
-            iks_kernel<2, GT, 2><<<grid, 256, smem, st>>>(d_trlwe, d_gtask, d_glist, Gl, c->d_ksk,
-                                                          d_out, p.n, p.N1, p.ksLen);
-        else if (kpt == 3)
-            iks_kernel<2, GT, 3><<<grid, 256, smem, st>>>(d_trlwe, d_gtask, d_glist, Gl, c->d_ksk,
-                                                          d_out, p.n, p.N1, p.ksLen);
-        else
-            throw std::invalid_argument("identity key switch: n too large");
-    }
-    else if (p.ksBaseBits == 4 && kpt == 1) {
-        constexpr int GT = 16;
-        const int grid = (Gl + GT - 1) / GT;
-        iks_kernel<4, GT, 1><<<grid, 256, smem, st>>>(d_trlwe, d_gtask, d_glist, Gl, c->d_ksk,
-                                                      d_out, p.n, p.N1, p.ksLen);
-    }
-    else {
-        throw std::invalid_argument("identity key switch: unsupported base");
-    }
+        iks_init_kernel<<<Gl, 128, 0, st>>>(d_trlwe, d_gtask, d_glist, d_seidx, Gl, d_out, p.n,
+                                            p.N1);
+        if (p.ksBaseBits == 2 && p.ksLen <= 8) {
+            constexpr int GT = 32;
+            const int tiles = (Gl + GT - 1) / GT;
+            const int split = iks_split(tiles, (int)p.N1);
+            const dim3 grid(tiles, split);
+            const size_t smem = (size_t)(p.N1 / split) * p.ksLen * sizeof(uint64_t);
+            if (kpt == 1)
+                iks_kernel<2, GT, 1><<<grid, 256, smem, st>>>(d_trlwe, d_gtask, d_glist, d_seidx, Gl,
+                                                              c->d_ksk, d_out, p.n, p.N1, p.ksLen);
+            else if (kpt == 2)
+                iks_kernel<2, GT, 2><<<grid, 256, smem, st>>>(d_trlwe, d_gtask, d_glist, d_seidx, Gl,
+                                                              c->d_ksk, d_out, p.n, p.N1, p.ksLen);
+            else if (kpt == 3)
+                iks_kernel<2, GT, 3><<<grid, 256, smem, st>>>(d_trlwe, d_gtask, d_glist, d_seidx, Gl,
+                                                              c->d_ksk, d_out, p.n, p.N1, p.ksLen);
+            else
+                throw std::invalid_argument("identity key switch: n too large");
+        }
+        else if (p.ksBaseBits == 4 && p.ksLen <= 8 && kpt == 1) {
+            constexpr int GT = 16;
+            const int tiles = (Gl + GT - 1) / GT;
+            const int split = iks_split(tiles, (int)p.N1);
+            const size_t smem = (size_t)(p.N1 / split) * p.ksLen * sizeof(uint64_t);
+            iks_kernel<4, GT, 1><<<dim3(tiles, split), 256, smem, st>>>(
+                d_trlwe, d_gtask, d_glist, d_seidx, Gl, c->d_ksk, d_out, p.n, p.N1, p.ksLen);
+        }
+        else {
+            throw std::invalid_argument("identity key switch: unsupported base");
+        }
     });
     VSP_CUDA_CHECK(cudaGetLastError());
-    c->launches++;
+    c->launches += 2;
     c->counters[2] += (uint64_t)Gl;
 }
 
-void configure_kernels(size_t br_smem, size_t iks_smem)
+// Per-device kernel attributes (large dynamic shared memory opt-in).  Called for
+// every new context; cudaFuncSetAttribute applies to the current device.
+void configure_kernels()
 {
-    static std::once_flag once;
-    std::call_once(once, [&] {
-        VSP_CUDA_CHECK(cudaFuncSetAttribute(br1024_kernel<kBrWarps, kBrSlots>,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)br_smem));
-        const int ik = (int)iks_smem;
-        VSP_CUDA_CHECK(cudaFuncSetAttribute(iks_kernel<2, 32, 1>,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, ik));
-        VSP_CUDA_CHECK(cudaFuncSetAttribute(iks_kernel<2, 32, 2>,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, ik));
-        VSP_CUDA_CHECK(cudaFuncSetAttribute(iks_kernel<2, 32, 3>,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, ik));
-        VSP_CUDA_CHECK(cudaFuncSetAttribute(iks_kernel<4, 16, 1>,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, ik));
-    });
+    const int br = (int)sizeof(Br1024Smem<kBrWarps, kBrSlots>);
+    VSP_CUDA_CHECK(cudaFuncSetAttribute(br1024_kernel<kBrWarps, kBrSlots>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, br));
+    VSP_CUDA_CHECK(cudaFuncSetAttribute(br2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)sizeof(Br2Smem)));
+    VSP_CUDA_CHECK(cudaFuncSetAttribute(cmux_chain1024_kernel<kChainWarps>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)sizeof(Chain1024Smem<kChainWarps>)));
+    const int ik = 1024 * 8 * 8;
+    VSP_CUDA_CHECK(cudaFuncSetAttribute(iks_kernel<2, 32, 1>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, ik));
+    VSP_CUDA_CHECK(cudaFuncSetAttribute(iks_kernel<2, 32, 2>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, ik));
+    VSP_CUDA_CHECK(cudaFuncSetAttribute(iks_kernel<2, 32, 3>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, ik));
+    VSP_CUDA_CHECK(cudaFuncSetAttribute(iks_kernel<4, 16, 1>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, ik));
 }
 
 void require_keys(const vsp_ctx* c)
@@ -328,6 +378,310 @@ void hom_gate_dev(vsp_ctx* c, const int32_t* kinds, const uint32_t* d_in, uint32
     launch_iks(c, d_trlwe, d_gtask, d_glist, (int)pl.glist.size(), d_out, st);
 }
 
+
+// ---------------------------------------------------------------------------
+// Circuit bootstrapping, selectors, CMUX chains, CMUX memory (mem.cpp)
+
+void require_cb(const vsp_ctx* c)
+{
+    require_keys(c);
+    if (!c->has_cb)
+        throw std::runtime_error("bootstrapping key lacks circuit bootstrapping material");
+}
+
+// circuitBootstrap (ops.cpp:914-935) of C level-0 TLWEs -> C raw TRGSWs
+// (2*l1 rows x 2 x N1 u32) in d_out.  Level-2 tasks are lev-major: g = lev*C + c.
+void cb_batch(vsp_ctx* c, const uint32_t* d_lwe, int C, uint32_t* d_out, cudaStream_t st)
+{
+    require_cb(c);
+    if (C == 0)
+        return;
+    const Params& p = c->p;
+    const int l = (int)p.l1, T2 = C * l;
+    const size_t N2 = p.N2, N1 = p.N1;
+    uint64_t* d_acc2 = c->acc2.as<uint64_t>((size_t)T2 * 2 * N2);
+    std::vector<uint64_t> hv(T2);
+    std::vector<int> rowA(T2), rowB(T2);
+    for (int lev = 0; lev < l; lev++)
+        for (int k = 0; k < C; k++) {
+            const int g = lev * C + k;
+            hv[g] = 1ull << (64 - (lev + 1) * p.Bg1Bits);
+            rowA[g] = k * 2 * l + lev;
+            rowB[g] = k * 2 * l + l + lev;
+        }
+    uint64_t* d_hv = c->hv.as<uint64_t>(T2);
+    int* d_rows = c->rows.as<int>(2 * (size_t)T2);
+    VSP_CUDA_CHECK(cudaMemcpyAsync(d_hv, hv.data(), T2 * 8, cudaMemcpyHostToDevice, st));
+    VSP_CUDA_CHECK(cudaMemcpyAsync(d_rows, rowA.data(), T2 * 4, cudaMemcpyHostToDevice, st));
+    VSP_CUDA_CHECK(cudaMemcpyAsync(d_rows + T2, rowB.data(), T2 * 4, cudaMemcpyHostToDevice, st));
+    if (p.fft) {
+        timed(c, "br2", st, [&] {
+            br2_kernel<<<T2, 256, sizeof(Br2Smem), st>>>(d_lwe, C, d_hv, c->d_bk2fd, c->d_tw2,
+                                                          d_acc2, (int)p.n, (int)p.Bg2Bits);
+        });
+        c->launches++;
+    }
+    else {
+        const int N = (int)p.N2;
+        const size_t smem = (size_t)6 * N * 8 + (size_t)2 * p.l2 * N * 4;
+        for (int lev = 0; lev < l; lev++) {
+            br_exact_kernel<uint64_t><<<C, N, smem, st>>>(d_lwe, (int)p.n, c->d_bk2raw, c->d_tv2[lev],
+                                                          d_acc2 + (size_t)lev * C * 2 * N2, N,
+                                                          ilog2(2 * N), (int)p.l2, (int)p.Bg2Bits);
+            c->launches++;
+        }
+    }
+    VSP_CUDA_CHECK(cudaGetLastError());
+    VSP_CUDA_CHECK(cudaMemsetAsync(d_out, 0, (size_t)C * 2 * l * 2 * N1 * 4, st));
+    const int islices = std::min<int>(64, (int)N2 + 1);
+    const dim3 grid(islices, (unsigned)((2 * N1 + 511) / 512), 2);
+    const size_t smem = (size_t)((N2 + 1 + islices - 1) / islices) * 32 * 4;
+    timed(c, "pks", st, [&] {
+        pks_kernel<32><<<grid, 256, smem, st>>>(d_acc2, d_hv, T2, c->d_pks[0], c->d_pks[1], d_out,
+                                                d_rows, d_rows + T2, (int)N2, (int)N1,
+                                                (int)p.pksBaseBits, (int)p.pksLen);
+    });
+    VSP_CUDA_CHECK(cudaGetLastError());
+    c->launches++;
+    c->counters[4] += (uint64_t)C;
+    c->counters[1] += (uint64_t)T2;
+    c->counters[3] += 2ull * T2;
+}
+
+size_t trgsw_words(const Params& p) { return (size_t)2 * p.l1 * 2 * p.N1; }
+
+// prepareAddress (mem.cpp:21-36): selector d = sel[d], selector v + d = trgswNot(sel[d]),
+// transformed for the active backend.
+void prepare_selectors(vsp_ctx* c, const uint32_t* d_raw, int v, cudaStream_t st)
+{
+    const Params& p = c->p;
+    const size_t tw = trgsw_words(p);
+    uint32_t* raw = c->selraw.as<uint32_t>(2 * v * tw);
+    VSP_CUDA_CHECK(cudaMemcpyAsync(raw, d_raw, v * tw * 4, cudaMemcpyDeviceToDevice, st));
+    trgsw_not_kernel<<<std::max(1, (int)((v * tw + 255) / 256)), 256, 0, st>>>(
+        d_raw, raw + v * tw, v, (int)p.N1, (int)p.l1, (int)p.Bg1Bits);
+    VSP_CUDA_CHECK(cudaGetLastError());
+    c->launches++;
+    if (p.fft) {
+        double2* fd = c->selfd.as<double2>((size_t)2 * v * 4 * 1024);
+        const int npolys = 2 * v * 8;
+        prepare_poly1024_kernel<<<(npolys + 3) / 4, 128, 0, st>>>(raw, c->d_tw2, fd, npolys);
+        VSP_CUDA_CHECK(cudaGetLastError());
+        c->launches++;
+    }
+}
+
+void run_chains(vsp_ctx* c, const std::vector<ChainTask>& tasks, cudaStream_t st)
+{
+    if (tasks.empty())
+        return;
+    const Params& p = c->p;
+    ChainTask* d = c->chains.as<ChainTask>(tasks.size());
+    VSP_CUDA_CHECK(cudaMemcpyAsync(d, tasks.data(), tasks.size() * sizeof(ChainTask),
+                                   cudaMemcpyHostToDevice, st));
+    const int T = (int)tasks.size();
+    if (p.fft) {
+        timed(c, "cmux_chain", st, [&] {
+            cmux_chain1024_kernel<kChainWarps>
+                <<<(T + kChainWarps - 1) / kChainWarps, kChainWarps * 32,
+                   sizeof(Chain1024Smem<kChainWarps>), st>>>(d, T, c->selfd.as<double2>(0),
+                                                             c->d_tw2, (int)p.Bg1Bits);
+        });
+    }
+    else {
+        const int N = (int)p.N1;
+        const size_t smem = (size_t)6 * N * 4 + (size_t)2 * p.l1 * N * 4;
+        cmux_chain_exact_kernel<<<T, N, smem, st>>>(d, c->selraw.as<uint32_t>(0), N, (int)p.l1,
+                                                    (int)p.Bg1Bits);
+    }
+    VSP_CUDA_CHECK(cudaGetLastError());
+    c->launches++;
+    for (const auto& t : tasks)
+        c->counters[0] += (uint64_t)t.nsteps;
+}
+
+ChainTask make_task(const uint32_t* c1, const uint32_t* c0, uint32_t* out, int mode)
+{
+    ChainTask t;
+    std::memset(&t, 0, sizeof t);
+    t.c1 = c1;
+    t.c0 = c0;
+    t.out = out;
+    t.mode = mode;
+    return t;
+}
+
+// IKS(SE(trlwe[i], se[i])) for `count` TRLWEs stored contiguously at d_trlwe.
+void iks_of_trlwes(vsp_ctx* c, const uint32_t* d_trlwe, int count, const int* se,
+                   uint32_t* d_out, cudaStream_t st)
+{
+    std::vector<int2> gt(count);
+    std::vector<int> gl(count);
+    for (int i = 0; i < count; i++) {
+        gt[i] = make_int2(i, -1);
+        gl[i] = i;
+    }
+    int2* d_gt = c->gtask.as<int2>(count);
+    int* d_gl = c->glist.as<int>(count);
+    VSP_CUDA_CHECK(cudaMemcpyAsync(d_gt, gt.data(), count * sizeof(int2), cudaMemcpyHostToDevice, st));
+    VSP_CUDA_CHECK(cudaMemcpyAsync(d_gl, gl.data(), count * sizeof(int), cudaMemcpyHostToDevice, st));
+    int* d_se = nullptr;
+    if (se) {
+        d_se = c->seidx.as<int>(count);
+        VSP_CUDA_CHECK(cudaMemcpyAsync(d_se, se, count * sizeof(int), cudaMemcpyHostToDevice, st));
+    }
+    launch_iks(c, d_trlwe, d_gt, d_gl, count, d_out, st, d_se);
+}
+
+// ramCycle (mem.cpp:122-135) on a device-resident RAM image (updated in place).
+void ram_cycle_dev(vsp_ctx* c, uint32_t* d_ram, int v, int w, const uint32_t* d_addr,
+                   const uint32_t* d_wflag, const uint32_t* d_wdata, uint32_t* d_readout,
+                   cudaStream_t st)
+{
+    require_cb(c);
+    const Params& p = c->p;
+    if (v < 1 || w < 1 || v > kChainMax)
+        throw std::invalid_argument("ramCycle: geometry out of range");
+    const size_t cw = 2 * (size_t)p.N1, words = (size_t)1 << v, n1 = p.n + 1;
+    // 1. addressToTrgsw + prepareAddress
+    uint32_t* raw = c->cbraw.as<uint32_t>(v * trgsw_words(p));
+    cb_batch(c, d_addr, v, raw, st);
+    prepare_selectors(c, raw, v, st);
+    // 2. ramReadUnit (mem.cpp:49-72): layer d halves every tree with sel[d]
+    uint32_t* A = c->layerA.as<uint32_t>((size_t)w * (words / 2) * cw);
+    uint32_t* B = c->layerB.as<uint32_t>((size_t)w * (words / 2) * cw);
+    const uint32_t* src = d_ram;
+    size_t size = words;
+    for (int d = 0; d < v; d++) {
+        const size_t half = size / 2;
+        uint32_t* dst = (d % 2 == 0) ? A : B;
+        std::vector<ChainTask> tasks;
+        for (int j = 0; j < w; j++)
+            for (size_t k = 0; k < half; k++) {
+                ChainTask t = make_task(src + (j * size + 2 * k + 1) * cw, src + (j * size + 2 * k) * cw,
+                                        dst + (j * half + k) * cw, 0);
+                t.nsteps = 1;
+                t.sel[0] = d;
+                tasks.push_back(t);
+            }
+        run_chains(c, tasks, st);
+        src = dst;
+        size = half;
+    }
+    const uint32_t* read = src;  // w TRLWEs
+    // 3. ramControlUnit (mem.cpp:74-90)
+    iks_of_trlwes(c, read, w, nullptr, d_readout, st);
+    uint32_t* mux_in = c->aux.as<uint32_t>(2 * (size_t)w * n1);
+    mux_prep_kernel<<<2 * w, 128, 0, st>>>(d_wflag, d_wdata, d_readout, mux_in, w, (int)p.n);
+    VSP_CUDA_CHECK(cudaGetLastError());
+    c->launches++;
+    uint32_t* mux_tr = c->aux2.as<uint32_t>(2 * (size_t)w * cw);
+    launch_br(c, mux_in, mux_tr, 2 * w, st);
+    std::vector<int2> pr(w);
+    for (int j = 0; j < w; j++)
+        pr[j] = make_int2(2 * j, 2 * j + 1);
+    int2* d_pr = c->pairs.as<int2>(w);
+    VSP_CUDA_CHECK(cudaMemcpyAsync(d_pr, pr.data(), w * sizeof(int2), cudaMemcpyHostToDevice, st));
+    uint32_t* controlled = (v % 2 == 1) ? B : A;  // the buffer not holding `read`
+    controlled = (controlled == read) ? ((controlled == A) ? B : A) : controlled;
+    trlwe_sum_mu_kernel<<<w, 256, 0, st>>>(mux_tr, d_pr, controlled, w, (int)p.N1);
+    VSP_CUDA_CHECK(cudaGetLastError());
+    c->launches++;
+    // 4. ramWriteUnit (mem.cpp:92-120): address-match chains, then noise refresh
+    const size_t cells = (size_t)w * words;
+    uint32_t* chain_out = c->ram.as<uint32_t>(cells * cw);
+    std::vector<ChainTask> tasks;
+    tasks.reserve(cells);
+    for (size_t idx = 0; idx < cells; idx++) {
+        const size_t j = idx / words, Ad = idx % words;
+        ChainTask t = make_task(controlled + j * cw, d_ram + idx * cw, chain_out + idx * cw, 0);
+        t.nsteps = v;
+        for (int d = 0; d < v; d++)
+            t.sel[d] = ((Ad >> d) & 1) ? d : v + d;
+        tasks.push_back(t);
+    }
+    run_chains(c, tasks, st);
+    uint32_t* lw = c->tasks.as<uint32_t>(cells * n1);
+    iks_of_trlwes(c, chain_out, (int)cells, nullptr, lw, st);
+    launch_br(c, lw, d_ram, (int)cells, st);
+}
+
+int ctz32(uint32_t x)
+{
+    int r = 0;
+    while (x && !(x & 1u)) {
+        x >>= 1;
+        r++;
+    }
+    return r;
+}
+
+// addressToTrgsw + prepareAddress + romRead (engine.cpp:133-143, mem.cpp:137-177).
+void rom_read_dev(vsp_ctx* c, const uint32_t* d_luts, int nluts, uint32_t depth_bytes,
+                  const uint32_t* d_addr, int vrom, uint32_t* d_out, cudaStream_t st)
+{
+    require_cb(c);
+    const Params& p = c->p;
+    const uint32_t blocks = depth_bytes / 4;
+    if (depth_bytes == 0 || depth_bytes % 4 || (blocks & (blocks - 1)))
+        throw std::invalid_argument("romRead: depth must be a power-of-two number of 32-bit blocks");
+    if (ctz32(blocks) != vrom)
+        throw std::invalid_argument("romRead: address width mismatch");
+    const int lowBits = std::min(vrom, ctz32(p.N1 / 32));
+    const int highBits = vrom - lowBits;
+    if (nluts != (1 << highBits))
+        throw std::invalid_argument("romRead: LUT count mismatch");
+    const size_t cw = 2 * (size_t)p.N1;
+    uint32_t* raw = c->cbraw.as<uint32_t>(std::max(vrom, 1) * trgsw_words(p));
+    cb_batch(c, d_addr, vrom, raw, st);
+    prepare_selectors(c, raw, vrom, st);
+    uint32_t* A = c->layerA.as<uint32_t>(std::max(nluts / 2, 1) * cw);
+    uint32_t* B = c->layerB.as<uint32_t>(std::max(nluts / 2, 1) * cw);
+    const uint32_t* src = d_luts;
+    int size = nluts;
+    for (int d = 0; d < highBits; d++) {
+        const int half = size / 2;
+        uint32_t* dst = (d % 2 == 0) ? A : B;
+        std::vector<ChainTask> tasks;
+        for (int k = 0; k < half; k++) {
+            ChainTask t = make_task(src + (2 * k + 1) * cw, src + 2 * k * cw, dst + k * cw, 0);
+            t.nsteps = 1;
+            t.sel[0] = lowBits + d;
+            tasks.push_back(t);
+        }
+        run_chains(c, tasks, st);
+        src = dst;
+        size = half;
+    }
+    uint32_t* acc = c->aux2.as<uint32_t>(cw);
+    if (lowBits > 0) {
+        ChainTask t = make_task(src, nullptr, acc, 1);
+        t.nsteps = lowBits;
+        for (int d = 0; d < lowBits; d++) {
+            t.sel[d] = d;
+            t.rot[d] = (int)(2 * p.N1 - (32u << d));
+        }
+        run_chains(c, std::vector<ChainTask>{t}, st);
+    }
+    else {
+        VSP_CUDA_CHECK(cudaMemcpyAsync(acc, src, cw * 4, cudaMemcpyDeviceToDevice, st));
+    }
+    int se[32];
+    for (int k = 0; k < 32; k++)
+        se[k] = k;
+    std::vector<int2> gt(32, make_int2(0, -1));
+    std::vector<int> gl(32);
+    for (int k = 0; k < 32; k++)
+        gl[k] = k;
+    int2* d_gt = c->gtask.as<int2>(32);
+    int* d_gl = c->glist.as<int>(32);
+    int* d_se = c->seidx.as<int>(32);
+    VSP_CUDA_CHECK(cudaMemcpyAsync(d_gt, gt.data(), 32 * sizeof(int2), cudaMemcpyHostToDevice, st));
+    VSP_CUDA_CHECK(cudaMemcpyAsync(d_gl, gl.data(), 32 * sizeof(int), cudaMemcpyHostToDevice, st));
+    VSP_CUDA_CHECK(cudaMemcpyAsync(d_se, se, 32 * sizeof(int), cudaMemcpyHostToDevice, st));
+    launch_iks(c, acc, d_gt, d_gl, 32, d_out, st, d_se);
+}
+
 }  // namespace
 
 // DFMA throughput probe: 16 independent FMA chains per thread.
@@ -386,31 +740,23 @@ vsp_ctx* vsp_create(const vsp_params* params, int device)
         c->set_device();
         VSP_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         // twiddles of the 512-point negacyclic transform
-        double2 tw1[15];
-        for (int d = 0; d < 4; d++)
-            for (int b = 0; b < (1 << d); b++)
-                tw1[(1 << d) - 1 + b] = zeta(d, (uint32_t)b);
-        VSP_CUDA_CHECK(cudaMemcpyToSymbol(c_tw1, tw1, sizeof(tw1)));
-        std::vector<double2> tw2(kTw2Entries * 32);
-        for (int L = 0; L < 32; L++) {
-            const uint32_t hi = L >> 1, odd = L & 1;
-            int e = 0;
-            for (int d = 4; d < 8; d++)
-                for (uint32_t s = 0; s < (1u << (d - 4)); s++)
-                    tw2[(e++) * 32 + L] = zeta(d, (hi << (d - 4)) | s);
-            for (uint32_t k = 0; k < 8; k++)
-                tw2[(e++) * 32 + L] = zeta(8, hi * 16 + k + 8 * odd);
+        double2 tw1[3][15];
+        std::vector<double2> tw2all;
+        for (int root = 0; root < 3; root++) {
+            std::vector<double2> tw2;
+            twiddles(root, tw1[root], tw2);
+            tw2all.insert(tw2all.end(), tw2.begin(), tw2.end());
         }
-        VSP_CUDA_CHECK(cudaMalloc(&c->d_tw2, tw2.size() * sizeof(double2)));
-        VSP_CUDA_CHECK(cudaMemcpy(c->d_tw2, tw2.data(), tw2.size() * sizeof(double2),
+        VSP_CUDA_CHECK(cudaMemcpyToSymbol(c_tw1, tw1, sizeof(tw1)));
+        VSP_CUDA_CHECK(cudaMalloc(&c->d_tw2, tw2all.size() * sizeof(double2)));
+        VSP_CUDA_CHECK(cudaMemcpy(c->d_tw2, tw2all.data(), tw2all.size() * sizeof(double2),
                                   cudaMemcpyHostToDevice));
         std::vector<uint32_t> tv(2 * c->p.N1, 0);
         for (uint32_t i = 0; i < c->p.N1; i++)
             tv[c->p.N1 + i] = kMu32;
         VSP_CUDA_CHECK(cudaMalloc(&c->d_tv1, tv.size() * 4));
         VSP_CUDA_CHECK(cudaMemcpy(c->d_tv1, tv.data(), tv.size() * 4, cudaMemcpyHostToDevice));
-        configure_kernels(sizeof(Br1024Smem<kBrWarps, kBrSlots>),
-                          (size_t)c->p.N1 * c->p.ksLen * sizeof(uint64_t));
+        configure_kernels();
         out = c.release();
     });
     return out;
@@ -426,8 +772,13 @@ void vsp_destroy(vsp_ctx* c)
                     (void*)c->d_pks[0], (void*)c->d_pks[1], (void*)c->d_tw2, (void*)c->d_tv1})
         if (q)
             cudaFree(q);
-    for (DevBuf* b : {&c->tasks, &c->trlwe, &c->in, &c->out, &c->kinds, &c->gtask, &c->glist})
+    for (DevBuf* b : {&c->tasks, &c->trlwe, &c->in, &c->out, &c->kinds, &c->gtask, &c->glist,
+                      &c->acc2, &c->hv, &c->rows, &c->cbraw, &c->selraw, &c->selfd, &c->chains,
+                      &c->layerA, &c->layerB, &c->ram, &c->aux, &c->aux2, &c->seidx, &c->pairs})
         b->release();
+    for (void* q : {(void*)c->d_bk2fd, (void*)c->d_tv2[0], (void*)c->d_tv2[1]})
+        if (q)
+            cudaFree(q);
     cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -441,8 +792,10 @@ int vsp_upload_keys(vsp_ctx* c, const uint32_t* bk1, const uint32_t* ksk, const 
         const Params& p = c->p;
         if (!bk1 || !ksk)
             throw std::invalid_argument("bk1 and ksk are required");
-        if (has_cb && (!bk2 || !pks_negs || !pks_id))
+        if (has_cb == 1 && (!bk2 || !pks_negs || !pks_id))
             throw std::invalid_argument("circuit-bootstrapping material incomplete");
+        if (has_cb == 2 && !bk2)
+            throw std::invalid_argument("bk2 missing");
         const size_t bk1_words = (size_t)p.n * 2 * p.l1 * 2 * p.N1;
         uint32_t* d_raw = nullptr;
         VSP_CUDA_CHECK(cudaMalloc(&d_raw, bk1_words * 4));
@@ -475,14 +828,43 @@ int vsp_upload_keys(vsp_ctx* c, const uint32_t* bk1, const uint32_t* ksk, const 
                 cudaFree(c->d_bk2raw);
             VSP_CUDA_CHECK(cudaMalloc(&c->d_bk2raw, bk2_words * 8));
             VSP_CUDA_CHECK(cudaMemcpy(c->d_bk2raw, bk2, bk2_words * 8, cudaMemcpyHostToDevice));
-            for (int w = 0; w < 2; w++) {
-                if (c->d_pks[w])
-                    cudaFree(c->d_pks[w]);
-                VSP_CUDA_CHECK(cudaMalloc(&c->d_pks[w], c->pks_words() * 4));
-                VSP_CUDA_CHECK(cudaMemcpy(c->d_pks[w], w == 0 ? pks_negs : pks_id,
-                                          c->pks_words() * 4, cudaMemcpyHostToDevice));
+            if (p.fft) {
+                if (p.N2 != 2048 || p.l2 != 4)
+                    throw std::invalid_argument("level-2 FFT path is specialised for N2=2048, l2=4");
+                if (c->d_bk2fd)
+                    cudaFree(c->d_bk2fd);
+                VSP_CUDA_CHECK(cudaMalloc(&c->d_bk2fd, (size_t)p.n * 8 * 4 * 1024 * sizeof(double2)));
+                const int jobs = (int)(p.n * 8 * 4 * 2);
+                prepare_bk2_kernel<<<(jobs + 1) / 2, 64, 0, c->stream>>>(c->d_bk2raw, c->d_tw2,
+                                                                        c->d_bk2fd, jobs);
+                VSP_CUDA_CHECK(cudaGetLastError());
+                c->launches++;
+                VSP_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+                cudaFree(c->d_bk2raw);  // the exact raw words are no longer needed
+                c->d_bk2raw = nullptr;
             }
-            c->has_cb = true;
+            else {
+                for (int lev = 0; lev < 2; lev++) {
+                    std::vector<uint64_t> tv(2 * p.N2, 0);
+                    const uint64_t h = 1ull << (64 - (lev + 1) * p.Bg1Bits);
+                    for (uint32_t k = 0; k < p.N2; k++)
+                        tv[p.N2 + k] = h / 2;
+                    if (!c->d_tv2[lev])
+                        VSP_CUDA_CHECK(cudaMalloc(&c->d_tv2[lev], tv.size() * 8));
+                    VSP_CUDA_CHECK(cudaMemcpy(c->d_tv2[lev], tv.data(), tv.size() * 8,
+                                              cudaMemcpyHostToDevice));
+                }
+            }
+            if (has_cb == 1) {
+                for (int w = 0; w < 2; w++) {
+                    if (c->d_pks[w])
+                        cudaFree(c->d_pks[w]);
+                    VSP_CUDA_CHECK(cudaMalloc(&c->d_pks[w], c->pks_words() * 4));
+                    VSP_CUDA_CHECK(cudaMemcpy(c->d_pks[w], w == 0 ? pks_negs : pks_id,
+                                              c->pks_words() * 4, cudaMemcpyHostToDevice));
+                }
+                c->has_cb = true;
+            }
         }
         c->has_keys = true;
     });
@@ -494,7 +876,7 @@ int vsp_hom_gate_batch_dev(vsp_ctx* c, const int32_t* kinds, const uint32_t* d_i
     return guard([&] {
         std::lock_guard<std::mutex> lk(c->mu);
         c->set_device();
-        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
         hom_gate_dev(c, kinds, d_in, d_out, G, st);
     });
 }
@@ -610,6 +992,203 @@ int vsp_identity_key_switch_batch(vsp_ctx* c, const uint32_t* in, uint32_t* out,
         launch_iks(c, d_tr, d_gt, d_gl, (int)G, d_out, c->stream);
         VSP_CUDA_CHECK(cudaMemcpyAsync(out, d_out, G * (c->p.n + 1) * 4, cudaMemcpyDeviceToHost,
                                        c->stream));
+        VSP_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+// ---- CMUX memory entry points (host buffers) ---------------------------------
+
+int vsp_circuit_bootstrap_batch(vsp_ctx* c, const uint32_t* in, uint32_t* out, size_t C)
+{
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(c->mu);
+        c->set_device();
+        require_cb(c);
+        if (C == 0)
+            return;
+        const size_t w = c->p.n + 1, tw = trgsw_words(c->p);
+        uint32_t* d_in = c->in.as<uint32_t>(C * w);
+        uint32_t* d_out = c->out.as<uint32_t>(C * tw);
+        VSP_CUDA_CHECK(cudaMemcpyAsync(d_in, in, C * w * 4, cudaMemcpyHostToDevice, c->stream));
+        cb_batch(c, d_in, (int)C, d_out, c->stream);
+        VSP_CUDA_CHECK(cudaMemcpyAsync(out, d_out, C * tw * 4, cudaMemcpyDeviceToHost, c->stream));
+        VSP_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int vsp_cmux_batch(vsp_ctx* c, const uint32_t* sel, const uint32_t* c1, const uint32_t* c0,
+                   uint32_t* out, size_t G)
+{
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(c->mu);
+        c->set_device();
+        if (G == 0)
+            return;
+        const Params& p = c->p;
+        const size_t tw = trgsw_words(p), cw = 2 * (size_t)p.N1;
+        uint32_t* raw = c->selraw.as<uint32_t>(G * tw);
+        uint32_t* d1 = c->layerA.as<uint32_t>(G * cw);
+        uint32_t* d0 = c->layerB.as<uint32_t>(G * cw);
+        uint32_t* d_out = c->out.as<uint32_t>(G * cw);
+        VSP_CUDA_CHECK(cudaMemcpyAsync(raw, sel, G * tw * 4, cudaMemcpyHostToDevice, c->stream));
+        VSP_CUDA_CHECK(cudaMemcpyAsync(d1, c1, G * cw * 4, cudaMemcpyHostToDevice, c->stream));
+        VSP_CUDA_CHECK(cudaMemcpyAsync(d0, c0, G * cw * 4, cudaMemcpyHostToDevice, c->stream));
+        if (p.fft) {
+            double2* fd = c->selfd.as<double2>(G * 4 * 1024);
+            const int npolys = (int)(G * 8);
+            prepare_poly1024_kernel<<<(npolys + 3) / 4, 128, 0, c->stream>>>(raw, c->d_tw2, fd,
+                                                                           npolys);
+            VSP_CUDA_CHECK(cudaGetLastError());
+            c->launches++;
+        }
+        std::vector<ChainTask> tasks;
+        for (size_t g = 0; g < G; g++) {
+            ChainTask t = make_task(d1 + g * cw, d0 + g * cw, d_out + g * cw, 0);
+            t.nsteps = 1;
+            t.sel[0] = (int)g;
+            tasks.push_back(t);
+        }
+        run_chains(c, tasks, c->stream);
+        VSP_CUDA_CHECK(cudaMemcpyAsync(out, d_out, G * cw * 4, cudaMemcpyDeviceToHost, c->stream));
+        VSP_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int vsp_hom_mux_no_se_iks_batch(vsp_ctx* c, const uint32_t* sel, const uint32_t* a,
+                                const uint32_t* b, uint32_t* out, size_t G)
+{
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(c->mu);
+        c->set_device();
+        require_keys(c);
+        if (G == 0)
+            return;
+        const Params& p = c->p;
+        const size_t n1 = p.n + 1, cw = 2 * (size_t)p.N1;
+        // homMuxNoSeIks = BR(sel + a - mu) + BR(-sel + b - mu) + mu X^0 (ops.cpp:898-909):
+        // reuse the RAM control-unit kernels with wflag := sel per item.
+        uint32_t* d = c->in.as<uint32_t>(3 * G * n1);
+        VSP_CUDA_CHECK(cudaMemcpyAsync(d, sel, G * n1 * 4, cudaMemcpyHostToDevice, c->stream));
+        VSP_CUDA_CHECK(cudaMemcpyAsync(d + G * n1, a, G * n1 * 4, cudaMemcpyHostToDevice, c->stream));
+        VSP_CUDA_CHECK(cudaMemcpyAsync(d + 2 * G * n1, b, G * n1 * 4, cudaMemcpyHostToDevice,
+                                       c->stream));
+        uint32_t* lin = c->aux.as<uint32_t>(2 * G * n1);
+        for (size_t g = 0; g < G; g++)
+            mux_prep_kernel<<<2, 128, 0, c->stream>>>(d + g * n1, d + G * n1 + g * n1,
+                                                      d + 2 * G * n1 + g * n1, lin + 2 * g * n1, 1,
+                                                      (int)p.n);
+        VSP_CUDA_CHECK(cudaGetLastError());
+        c->launches += G;
+        uint32_t* tr = c->aux2.as<uint32_t>(2 * G * cw);
+        launch_br(c, lin, tr, (int)(2 * G), c->stream);
+        std::vector<int2> pr(G);
+        for (size_t g = 0; g < G; g++)
+            pr[g] = make_int2((int)(2 * g), (int)(2 * g + 1));
+        int2* d_pr = c->pairs.as<int2>(G);
+        uint32_t* d_out = c->out.as<uint32_t>(G * cw);
+        VSP_CUDA_CHECK(cudaMemcpyAsync(d_pr, pr.data(), G * sizeof(int2), cudaMemcpyHostToDevice,
+                                       c->stream));
+        trlwe_sum_mu_kernel<<<(unsigned)G, 256, 0, c->stream>>>(tr, d_pr, d_out, (int)G, (int)p.N1);
+        VSP_CUDA_CHECK(cudaGetLastError());
+        c->launches++;
+        VSP_CUDA_CHECK(cudaMemcpyAsync(out, d_out, G * cw * 4, cudaMemcpyDeviceToHost, c->stream));
+        VSP_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int vsp_ram_cycle(vsp_ctx* c, uint32_t v, uint32_t w, uint32_t* ram, const uint32_t* addr,
+                  const uint32_t* wflag, const uint32_t* wdata, uint32_t* readout)
+{
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(c->mu);
+        c->set_device();
+        const Params& p = c->p;
+        const size_t n1 = p.n + 1, cw = 2 * (size_t)p.N1, cells = (size_t)w << v;
+        if (v == 0 || w == 0)
+            throw std::invalid_argument("ramCycle: address width mismatch");
+        DevBuf ramb;
+        uint32_t* d_ram = ramb.as<uint32_t>(cells * cw);
+        uint32_t* d_io = c->in.as<uint32_t>((v + 1 + 2 * (size_t)w) * n1);
+        uint32_t* d_addr = d_io;
+        uint32_t* d_wflag = d_io + v * n1;
+        uint32_t* d_wdata = d_wflag + n1;
+        uint32_t* d_ro = d_wdata + w * n1;
+        VSP_CUDA_CHECK(cudaMemcpyAsync(d_ram, ram, cells * cw * 4, cudaMemcpyHostToDevice, c->stream));
+        VSP_CUDA_CHECK(cudaMemcpyAsync(d_addr, addr, v * n1 * 4, cudaMemcpyHostToDevice, c->stream));
+        VSP_CUDA_CHECK(cudaMemcpyAsync(d_wflag, wflag, n1 * 4, cudaMemcpyHostToDevice, c->stream));
+        VSP_CUDA_CHECK(cudaMemcpyAsync(d_wdata, wdata, w * n1 * 4, cudaMemcpyHostToDevice, c->stream));
+        ram_cycle_dev(c, d_ram, (int)v, (int)w, d_addr, d_wflag, d_wdata, d_ro, c->stream);
+        VSP_CUDA_CHECK(cudaMemcpyAsync(readout, d_ro, w * n1 * 4, cudaMemcpyDeviceToHost, c->stream));
+        VSP_CUDA_CHECK(cudaMemcpyAsync(ram, d_ram, cells * cw * 4, cudaMemcpyDeviceToHost, c->stream));
+        VSP_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+        ramb.release();
+    });
+}
+
+int vsp_rom_read(vsp_ctx* c, uint32_t depth_bytes, const uint32_t* luts, uint32_t nluts,
+                 const uint32_t* addr, uint32_t vrom, uint32_t* out)
+{
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(c->mu);
+        c->set_device();
+        const Params& p = c->p;
+        const size_t n1 = p.n + 1, cw = 2 * (size_t)p.N1;
+        DevBuf lb;
+        uint32_t* d_luts = lb.as<uint32_t>(std::max<size_t>(nluts, 1) * cw);
+        uint32_t* d_io = c->in.as<uint32_t>((vrom + 32) * n1);
+        VSP_CUDA_CHECK(cudaMemcpyAsync(d_luts, luts, nluts * cw * 4, cudaMemcpyHostToDevice, c->stream));
+        VSP_CUDA_CHECK(cudaMemcpyAsync(d_io, addr, vrom * n1 * 4, cudaMemcpyHostToDevice, c->stream));
+        rom_read_dev(c, d_luts, (int)nluts, depth_bytes, d_io, (int)vrom, d_io + vrom * n1,
+                     c->stream);
+        VSP_CUDA_CHECK(cudaMemcpyAsync(out, d_io + vrom * n1, 32 * n1 * 4, cudaMemcpyDeviceToHost,
+                                       c->stream));
+        VSP_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+        lb.release();
+    });
+}
+
+int vsp_blind_rotate_lvl2_batch(vsp_ctx* c, const uint32_t* in, const uint64_t* h, uint64_t* out,
+                                size_t T)
+{
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(c->mu);
+        c->set_device();
+        require_keys(c);
+        if (!c->d_bk2fd && !c->d_bk2raw)
+            throw std::runtime_error("bootstrapping key lacks circuit bootstrapping material");
+        if (T == 0)
+            return;
+        const Params& p = c->p;
+        const size_t n1 = p.n + 1, N2 = p.N2;
+        uint32_t* d_in = c->in.as<uint32_t>(T * n1);
+        uint64_t* d_h = c->hv.as<uint64_t>(T);
+        uint64_t* d_acc = c->acc2.as<uint64_t>(T * 2 * N2);
+        VSP_CUDA_CHECK(cudaMemcpyAsync(d_in, in, T * n1 * 4, cudaMemcpyHostToDevice, c->stream));
+        VSP_CUDA_CHECK(cudaMemcpyAsync(d_h, h, T * 8, cudaMemcpyHostToDevice, c->stream));
+        if (p.fft) {
+            br2_kernel<<<(unsigned)T, 256, sizeof(Br2Smem), c->stream>>>(
+                d_in, (int)T, d_h, c->d_bk2fd, c->d_tw2, d_acc, (int)p.n, (int)p.Bg2Bits);
+        }
+        else {
+            const int N = (int)N2;
+            const size_t smem = (size_t)6 * N * 8 + (size_t)2 * p.l2 * N * 4;
+            std::vector<uint64_t> tv(2 * N2, 0);
+            uint64_t* d_tv = reinterpret_cast<uint64_t*>(c->aux.as<uint8_t>(T * 2 * N2 * 8));
+            for (size_t t = 0; t < T; t++) {
+                for (size_t k = 0; k < N2; k++)
+                    tv[N2 + k] = h[t] / 2;
+                VSP_CUDA_CHECK(cudaMemcpyAsync(d_tv + t * 2 * N2, tv.data(), 2 * N2 * 8,
+                                               cudaMemcpyHostToDevice, c->stream));
+                VSP_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+                br_exact_kernel<uint64_t><<<1, N, smem, c->stream>>>(
+                    d_in + t * n1, (int)p.n, c->d_bk2raw, d_tv + t * 2 * N2, d_acc + t * 2 * N2, N,
+                    ilog2(2 * N), (int)p.l2, (int)p.Bg2Bits);
+            }
+        }
+        VSP_CUDA_CHECK(cudaGetLastError());
+        c->launches++;
+        c->counters[1] += T;
+        VSP_CUDA_CHECK(cudaMemcpyAsync(out, d_acc, T * 2 * N2 * 8, cudaMemcpyDeviceToHost, c->stream));
         VSP_CUDA_CHECK(cudaStreamSynchronize(c->stream));
     });
 }
