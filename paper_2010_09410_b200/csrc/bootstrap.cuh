@@ -62,15 +62,24 @@ struct Br1024Smem {
     double2 tw2[kTw2Entries * 32];
     double2 xbuf[WARPS][kFftXbufStride];
     uint32_t acc[WARPS][2048];
+    uint32_t dig[WARPS][2][16 * 32];  // digits (2 levels), packed 2 x int16
     uint64_t full[S];
     uint32_t cnt[S];
 };
 
-template <int WARPS, int S>
+// (X^k p)[q] mod X^N + 1 (polyRotate, poly.hpp:32-48) = +-p[(q-k) mod 2N]; qk = q - k.
+__device__ __forceinline__ uint32_t rot_coef1024(const uint32_t* src, uint32_t qk)
+{
+    const uint32_t idx = qk & 2047u;
+    const uint32_t x = src[idx & 1023u];
+    const uint32_t neg = idx >> 10;  // 0 or 1
+    return (x ^ (0u - neg)) + neg;
+}
+
+template <int WARPS, int S, int BG>
 __global__ void __launch_bounds__(WARPS * 32, 1)
     br1024_kernel(const uint32_t* __restrict__ tasks, const double2* __restrict__ bkfd,
-                  const double2* __restrict__ tw2g, uint32_t* __restrict__ out, int T, int n,
-                  int bgbits)
+                  const double2* __restrict__ tw2g, uint32_t* __restrict__ out, int T, int n)
 {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     auto& sm = *reinterpret_cast<Br1024Smem<WARPS, S>*>(smem_raw);
@@ -115,10 +124,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     __syncwarp();
 
     // decomposePoly constants (poly.hpp:79-97), l = 2: no final rounding bit.
-    const uint32_t half = 1u << (bgbits - 1);
-    const uint32_t mask = (1u << bgbits) - 1;
-    const uint32_t offset = (half << (32 - bgbits)) + (half << (32 - 2 * bgbits));
-    const int sh1 = 32 - bgbits, sh2 = 32 - 2 * bgbits;
+    constexpr uint32_t kHalf = 1u << (BG - 1);
+    constexpr uint32_t kMask = (1u << BG) - 1;
+    constexpr uint32_t kOffset = (kHalf << (32 - BG)) + (kHalf << (32 - 2 * BG));
     double2* xbuf = sm.xbuf[warp];
 
     double2 accA[16], accB[16];
@@ -134,22 +142,33 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
 #pragma unroll 1
         for (int P = 0; P < 2; P++) {
             const uint32_t* src = acc + P * 1024;
+            // diff = (X^bara - 1) * acc (polyMulByXkMinusOne, poly.hpp:51-57) computed once;
+            // both digit levels (decomposePoly, poly.hpp:79-97) are parked in smem as
+            // packed int16 pairs (coefficients p, p+512) so no transform registers are live.
+            // lane + 32 j is recomputed from an opaque base every step so the compiler does
+            // not hoist 32 loop-invariant indices into (spilled) registers.
+            const uint32_t lo = (uint32_t)lane + (uint32_t)opaque_zero();
+            const uint32_t lk = lo - bara;
+            const uint32_t* srcl = src + lo;
+#pragma unroll
+            for (int j = 0; j < 16; j++) {
+                const uint32_t v0 = rot_coef1024(src, lk + 32 * j) - srcl[32 * j] + kOffset;
+                const uint32_t v1 = rot_coef1024(src, lk + 32 * j + 512) - srcl[32 * j + 512] + kOffset;
+                const uint32_t d0 = (v0 >> (32 - BG)) - kHalf;
+                const uint32_t d1 = (v1 >> (32 - BG)) - kHalf;
+                const uint32_t e0 = ((v0 >> (32 - 2 * BG)) & kMask) - kHalf;
+                const uint32_t e1 = ((v1 >> (32 - 2 * BG)) & kMask) - kHalf;
+                sm.dig[warp][0][j * 32 + lane] = (d0 & 0xffffu) | (d1 << 16);
+                sm.dig[warp][1][j * 32 + lane] = (e0 & 0xffffu) | (e1 << 16);
+            }
 #pragma unroll 1
             for (int lvl = 0; lvl < 2; lvl++) {
-                // diff = (X^bara - 1) * acc (polyMulByXkMinusOne, poly.hpp:51-57), then the
-                // level-lvl signed digit of every coefficient (decomposePoly, poly.hpp:79-97)
-                const int sh = lvl == 0 ? sh1 : sh2;
                 double2 z[16];
 #pragma unroll
                 for (int j = 0; j < 16; j++) {
-                    const uint32_t p0 = lane + 32 * j, p1 = p0 + 512;
-                    const uint32_t i0 = (p0 - bara) & 2047u, i1 = (p1 - bara) & 2047u;
-                    const uint32_t r0 = i0 < 1024 ? src[i0] : 0u - src[i0 - 1024];
-                    const uint32_t r1 = i1 < 1024 ? src[i1] : 0u - src[i1 - 1024];
-                    const uint32_t v0 = r0 - src[p0] + offset;
-                    const uint32_t v1 = r1 - src[p1] + offset;
-                    z[j].x = (double)(int32_t)(((v0 >> sh) & mask) - half);
-                    z[j].y = (double)(int32_t)(((v1 >> sh) & mask) - half);
+                    const uint32_t w = sm.dig[warp][lvl][j * 32 + lane];
+                    z[j].x = (double)(int16_t)(w & 0xffffu);
+                    z[j].y = (double)(int16_t)(w >> 16);
                 }
                 fft512_fwd(z, xbuf, sm.tw2, lane);
                 const int c = i * 4 + P * 2 + lvl;

@@ -29,7 +29,28 @@ namespace vsp {
 //   ROOT 2: c = e^{i 5pi/4}  (level 2, branch 1)
 // The per-lane table tw2 (stages 4-8) is likewise per root.
 __constant__ double2 c_tw1[3][15];
+// The same twiddles in "tangent" form for the forward butterflies: (kappa, tau) with
+// zeta = kappa (1 + i tau) (form A, |tan| <= 1) or zeta = kappa (tau + i) (form B,
+// |cot| < 1); the form of each (root, d, b) is known at compile time (tw_form_a).
+__constant__ double2 c_tw1t[3][15];
 
+__host__ __device__ constexpr int bitrev_const(int b, int d)
+{
+    int r = 0;
+    for (int i = 0; i < d; i++)
+        r = (r << 1) | ((b >> i) & 1);
+    return r;
+}
+
+// Angle of zeta_{d,b} for root ROOT in units of pi/64 (exact for d <= 3), and whether
+// |tan| <= 1 (angle mod pi within [0, pi/4] or [3pi/4, pi)).
+__host__ __device__ constexpr bool tw_form_a(int root, int d, int b)
+{
+    const int theta0 = root == 0 ? 32 : root == 1 ? 16 : 80;  // pi/2, pi/4, 5pi/4
+    const int ang = theta0 / (2 << d) + 64 * bitrev_const(b, d) / (1 << d);
+    const int m = ang % 64;  // mod pi (64 units)
+    return m <= 16 || m >= 48;
+}
 constexpr int kFftXbufStride = 544;  // 512 + 32 swizzle pad (double2 units)
 constexpr int kTw2Entries = 23;      // 1+2+4+8 (stages 4-7) + 8 (stage 8)
 
@@ -43,6 +64,26 @@ __device__ __forceinline__ void bf_fwd(double2& u, double2& v, const double2 w)
     u.y = u.y + ty;
 }
 
+// Forward butterfly with a tangent-form twiddle: 6 FMAs instead of 2 MUL + 2 FMA + 4 ADD.
+template <bool FORM_A>
+__device__ __forceinline__ void bf_fwd_tan(double2& u, double2& v, const double2 kt)
+{
+    const double k = kt.x, t = kt.y;
+    double tx, ty;
+    if (FORM_A) {  // zeta v = k (v.x - t v.y, v.y + t v.x)
+        tx = fma(-t, v.y, v.x);
+        ty = fma(t, v.x, v.y);
+    }
+    else {  // zeta v = k (t v.x - v.y, t v.y + v.x)
+        tx = fma(t, v.x, -v.y);
+        ty = fma(t, v.y, v.x);
+    }
+    v.x = fma(-k, tx, u.x);
+    v.y = fma(-k, ty, u.y);
+    u.x = fma(k, tx, u.x);
+    u.y = fma(k, ty, u.y);
+}
+
 // Inverse (Gentleman-Sande) butterfly without the 1/2: (a, b) -> (a + b, (a - b) conj(w)).
 __device__ __forceinline__ void bf_inv(double2& a, double2& b, const double2 w)
 {
@@ -51,6 +92,15 @@ __device__ __forceinline__ void bf_inv(double2& a, double2& b, const double2 w)
     a.y = a.y + b.y;
     b.x = dx * w.x + dy * w.y;
     b.y = dy * w.x - dx * w.y;
+}
+
+// An opaque zero: keeps the compiler from hoisting the per-stage twiddle loads out of
+// the blind-rotation loop (which would pin ~60 registers for the whole kernel).
+__device__ __forceinline__ int opaque_zero()
+{
+    int z;
+    asm volatile("mov.u32 %0, 0;" : "=r"(z));
+    return z;
 }
 
 __device__ __forceinline__ double2 shfl_xor_d2(double2 v, int m)
@@ -66,13 +116,20 @@ template <int ROOT = 0>
 __device__ __forceinline__ void fft512_fwd(double2 (&v)[16], double2* xbuf,
                                            const double2* tw2, int lane)
 {
+    const double2* tw1t = &c_tw1t[ROOT][0] + opaque_zero();
 #pragma unroll
     for (int d = 0; d < 4; d++) {
         const int h = 8 >> d;
 #pragma unroll
         for (int j = 0; j < 16; j++)
-            if ((j & h) == 0)
-                bf_fwd(v[j], v[j + h], c_tw1[ROOT][(1 << d) - 1 + (j >> (4 - d))]);
+            if ((j & h) == 0) {
+                const int b = j >> (4 - d);
+                const double2 kt = tw1t[(1 << d) - 1 + b];
+                if (tw_form_a(ROOT, d, b))
+                    bf_fwd_tan<true>(v[j], v[j + h], kt);
+                else
+                    bf_fwd_tan<false>(v[j], v[j + h], kt);
+            }
     }
     __syncwarp();
 #pragma unroll
@@ -136,13 +193,14 @@ __device__ __forceinline__ void fft512_inv(double2 (&v)[16], double2* xbuf,
 #pragma unroll
     for (int j = 0; j < 16; j++)
         v[j] = xbuf[lane + 34 * j];
+    const double2* tw1 = &c_tw1[ROOT][0] + opaque_zero();
 #pragma unroll
     for (int d = 3; d >= 0; d--) {
         const int h = 8 >> d;
 #pragma unroll
         for (int j = 0; j < 16; j++)
             if ((j & h) == 0)
-                bf_inv(v[j], v[j + h], c_tw1[ROOT][(1 << d) - 1 + (j >> (4 - d))]);
+                bf_inv(v[j], v[j + h], tw1[(1 << d) - 1 + (j >> (4 - d))]);
     }
 }
 

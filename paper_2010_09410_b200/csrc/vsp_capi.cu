@@ -107,13 +107,22 @@ double2 zeta_root(long double theta0, int d, uint32_t b)
 
 long double root_theta(int root) { return root == 0 ? kPi / 2 : root == 1 ? kPi / 4 : 5 * kPi / 4; }
 
-// tw1 (15 constants) and the per-lane tw2 table [23][32] of one root.
-void twiddles(int root, double2* tw1, std::vector<double2>& tw2)
+// tw1 (15 constants), their tangent forms, and the per-lane tw2 table [23][32] of one root.
+void twiddles(int root, double2* tw1, double2* tw1t, std::vector<double2>& tw2)
 {
     const long double t0 = root_theta(root);
     for (int d = 0; d < 4; d++)
-        for (int b = 0; b < (1 << d); b++)
+        for (int b = 0; b < (1 << d); b++) {
             tw1[(1 << d) - 1 + b] = zeta_root(t0, d, (uint32_t)b);
+            uint32_t r = 0;
+            for (int i = 0; i < d; i++)
+                r = (r << 1) | ((b >> i) & 1u);
+            const long double a = (t0 / (long double)(1u << d) +
+                                   2.0L * kPi * (long double)r / (long double)(1u << d)) / 2;
+            tw1t[(1 << d) - 1 + b] =
+                tw_form_a(root, d, b) ? make_double2((double)cosl(a), (double)tanl(a))
+                                      : make_double2((double)sinl(a), (double)(cosl(a) / sinl(a)));
+        }
     tw2.assign(kTw2Entries * 32, make_double2(0, 0));
     for (int L = 0; L < 32; L++) {
         const uint32_t hi = L >> 1, odd = L & 1;
@@ -131,6 +140,7 @@ void twiddles(int root, double2* tw1, std::vector<double2>& tw2)
 struct vsp_ctx {
     Params p{};
     int device = 0;
+    int sms = 148;
     cudaStream_t stream = nullptr;
     bool has_keys = false, has_cb = false;
     // key material
@@ -203,8 +213,25 @@ void validate(const Params& p)  // ParameterSet::validate (params.cpp:17-29)
 }
 
 // Kernel configuration of the level-1 FFT blind rotation.
-constexpr int kBrWarps = 8;
-constexpr int kBrSlots = 4;
+constexpr int kBrSlots = 2;
+constexpr int kBrBg = 10;  // the FFT path is specialised for Bg1 = 2^10 (tfhe-80)
+
+// Warps (= tasks) per CTA of the blind-rotation kernel: every task costs the same, so
+// choose W in {6, 7, 8} minimising waves x W for T tasks on the device's SMs.
+int br_warps_for(int T, int sms)
+{
+    int best = 8;
+    long best_cost = -1;
+    for (int w = 8; w >= 6; w--) {
+        const long waves = (T + (long)sms * w - 1) / ((long)sms * w);
+        const long cost = waves * w;
+        if (best_cost < 0 || cost < best_cost) {
+            best_cost = cost;
+            best = w;
+        }
+    }
+    return best;
+}
 constexpr int kChainWarps = 8;
 
 void launch_br(vsp_ctx* c, const uint32_t* d_tasks, uint32_t* d_trlwe, int T, cudaStream_t st)
@@ -213,11 +240,20 @@ void launch_br(vsp_ctx* c, const uint32_t* d_tasks, uint32_t* d_trlwe, int T, cu
         return;
     const Params& p = c->p;
     if (p.fft) {
-        const size_t smem = sizeof(Br1024Smem<kBrWarps, kBrSlots>);
-        const int grid = (T + kBrWarps - 1) / kBrWarps;
+        const int W = br_warps_for(T, c->sms);
         timed(c, "br1024", st, [&] {
-            br1024_kernel<kBrWarps, kBrSlots><<<grid, kBrWarps * 32, smem, st>>>(
-                d_tasks, c->d_bk1fd, c->d_tw2, d_trlwe, T, (int)p.n, (int)p.Bg1Bits);
+            if (W == 8)
+                br1024_kernel<8, kBrSlots, kBrBg><<<(T + 7) / 8, 256, sizeof(Br1024Smem<8, kBrSlots>),
+                                                    st>>>(d_tasks, c->d_bk1fd, c->d_tw2, d_trlwe,
+                                                          T, (int)p.n);
+            else if (W == 7)
+                br1024_kernel<7, kBrSlots, kBrBg><<<(T + 6) / 7, 224, sizeof(Br1024Smem<7, kBrSlots>),
+                                                    st>>>(d_tasks, c->d_bk1fd, c->d_tw2, d_trlwe,
+                                                          T, (int)p.n);
+            else
+                br1024_kernel<6, kBrSlots, kBrBg><<<(T + 5) / 6, 192, sizeof(Br1024Smem<6, kBrSlots>),
+                                                    st>>>(d_tasks, c->d_bk1fd, c->d_tw2, d_trlwe,
+                                                          T, (int)p.n);
         });
     }
     else {
@@ -292,9 +328,15 @@ void launch_iks(vsp_ctx* c, const uint32_t* d_trlwe, const int2* d_gtask, const 
 // every new context; cudaFuncSetAttribute applies to the current device.
 void configure_kernels()
 {
-    const int br = (int)sizeof(Br1024Smem<kBrWarps, kBrSlots>);
-    VSP_CUDA_CHECK(cudaFuncSetAttribute(br1024_kernel<kBrWarps, kBrSlots>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, br));
+    VSP_CUDA_CHECK(cudaFuncSetAttribute(br1024_kernel<8, kBrSlots, kBrBg>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)sizeof(Br1024Smem<8, kBrSlots>)));
+    VSP_CUDA_CHECK(cudaFuncSetAttribute(br1024_kernel<7, kBrSlots, kBrBg>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)sizeof(Br1024Smem<7, kBrSlots>)));
+    VSP_CUDA_CHECK(cudaFuncSetAttribute(br1024_kernel<6, kBrSlots, kBrBg>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)sizeof(Br1024Smem<6, kBrSlots>)));
     VSP_CUDA_CHECK(cudaFuncSetAttribute(br2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)sizeof(Br2Smem)));
     VSP_CUDA_CHECK(cudaFuncSetAttribute(cmux_chain1024_kernel<kChainWarps>,
@@ -734,20 +776,22 @@ vsp_ctx* vsp_create(const vsp_params* params, int device)
         auto c = std::make_unique<vsp_ctx>();
         std::memcpy(&c->p, params, sizeof(vsp_params));
         validate(c->p);
-        if (c->p.fft && (c->p.N1 != 1024 || c->p.l1 != 2))
-            throw std::invalid_argument("FFT path is specialised for N1 = 1024, l1 = 2");
+        if (c->p.fft && (c->p.N1 != 1024 || c->p.l1 != 2 || c->p.Bg1Bits != kBrBg))
+            throw std::invalid_argument("FFT path is specialised for N1 = 1024, l1 = 2, Bg1 = 2^10");
         c->device = device;
         c->set_device();
+        VSP_CUDA_CHECK(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device));
         VSP_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         // twiddles of the 512-point negacyclic transform
-        double2 tw1[3][15];
+        double2 tw1[3][15], tw1t[3][15];
         std::vector<double2> tw2all;
         for (int root = 0; root < 3; root++) {
             std::vector<double2> tw2;
-            twiddles(root, tw1[root], tw2);
+            twiddles(root, tw1[root], tw1t[root], tw2);
             tw2all.insert(tw2all.end(), tw2.begin(), tw2.end());
         }
         VSP_CUDA_CHECK(cudaMemcpyToSymbol(c_tw1, tw1, sizeof(tw1)));
+        VSP_CUDA_CHECK(cudaMemcpyToSymbol(c_tw1t, tw1t, sizeof(tw1t)));
         VSP_CUDA_CHECK(cudaMalloc(&c->d_tw2, tw2all.size() * sizeof(double2)));
         VSP_CUDA_CHECK(cudaMemcpy(c->d_tw2, tw2all.data(), tw2all.size() * sizeof(double2),
                                   cudaMemcpyHostToDevice));
