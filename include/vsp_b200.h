@@ -119,6 +119,40 @@ int vsp_rom_read(vsp_ctx* ctx, uint32_t depth_bytes, const uint32_t* luts, uint3
 int vsp_blind_rotate_lvl2_batch(vsp_ctx* ctx, const uint32_t* in, const uint64_t* h,
                                 uint64_t* out, size_t T);
 
+/* ---- netlist runner (hvp::netlist::Evaluator<TfheBackend>, engine.hpp:107-405) ------
+ * The netlist is uploaded as flat arrays (Netlist, netlist.hpp:44-63): cell kinds in
+ * hvp::netlist::CellKind order (0..9 gates as GateKind, 10 DFF, 11 ROM, 12 RAM,
+ * 13 CONST0, 14 CONST1), cell ids, CSR lists of input / output nets per cell (pin order
+ * of netlist.hpp:38-43), and the nets driven by module input ports.  The DAG is built
+ * and levelled exactly as buildDag (netlist.cpp:348-432); each cycle evaluates it one
+ * ASAP level per batched launch and then latches the DFFs (engine.hpp:263-351).  Value
+ * table, DFF state, ROM and RAM stay device-resident. */
+typedef struct vsp_netlist vsp_netlist;
+
+vsp_netlist* vsp_netlist_create(vsp_ctx* ctx, int32_t net_count, int32_t cells,
+                                const int32_t* kinds, const int32_t* ids, const int32_t* in_off,
+                                const int32_t* in_nets, const int32_t* out_off,
+                                const int32_t* out_nets, const int32_t* input_nets,
+                                int32_t n_inputs);
+void vsp_netlist_destroy(vsp_netlist* nl);
+/* out6: dag nodes, dffs, gMax, depth, rom cell, ram cell; levels[dag node] optional. */
+int vsp_netlist_info(vsp_netlist* nl, int32_t* out6, int32_t* levels);
+/* Evaluator::setInput (engine.hpp:160-163) by index into input_nets. */
+int vsp_netlist_set_input(vsp_netlist* nl, int32_t input_index, const uint32_t* tlwe);
+/* Evaluator::output (engine.hpp:165-176) for any net. */
+int vsp_netlist_get_net(vsp_netlist* nl, int32_t net, uint32_t* tlwe);
+/* dffState / setDffStateRaw (engine.hpp:185-194); either pointer may be NULL. */
+int vsp_netlist_dff(vsp_netlist* nl, uint32_t* get, const uint32_t* set);
+/* setRom / setRam / ram (engine.hpp:204-221). */
+int vsp_netlist_set_rom(vsp_netlist* nl, uint32_t depth_bytes, const uint32_t* luts,
+                        uint32_t nluts);
+int vsp_netlist_ram(vsp_netlist* nl, uint32_t v, uint32_t w, uint32_t* get, const uint32_t* set);
+/* Evaluator::run (engine.hpp:238-247); stats: 4 doubles per cycle (evaluated cells,
+ * gMax, depth, seconds) or NULL. */
+int vsp_netlist_run(vsp_netlist* nl, uint64_t cycles, double* stats);
+uint64_t vsp_netlist_cycle(vsp_netlist* nl);
+int vsp_netlist_set_cycle(vsp_netlist* nl, uint64_t cycle);
+
 /* OpCounters (counters.hpp:11-28): cmux, blindRotate, identityKeySwitch,
  * privateKeySwitch, circuitBootstrap — counted per batched operation exactly as
  * the reference increments them per call. */

@@ -1,0 +1,269 @@
+// Level-batched netlist runner (replaces hvp::netlist::Evaluator<TfheBackend>,
+// engine.hpp:107-405, engine.cpp:113-148).  Included by vsp_capi.cu after the launch
+// helpers.
+//
+// The reference list-schedules individual cells onto host threads (engine.hpp:263-351).
+// Every cell's output is a deterministic function of its inputs, so evaluating the
+// DAG one ASAP level at a time (Dag::level, netlist.cpp:387-406) yields bit-identical
+// values; each level's gates become ONE batched gate-bootstrap launch sequence, and
+// the memory ports of the level run the batched CMUX-memory pipeline.  The value
+// table, DFF state and the RAM image stay resident in HBM across cycles.
+#pragma once
+
+namespace vsp {
+
+// hvp::netlist::CellKind order (netlist.hpp:12-28)
+enum CellKindDev : int {
+    cAnd = 0, cAndNot, cMux, cNand, cNor, cNot, cOr, cOrNot, cXnor, cXor,
+    cDff, cRom, cRam, cConst0, cConst1
+};
+
+__global__ void gather_tlwe_kernel(const int* __restrict__ nets, int count,
+                                   const uint32_t* __restrict__ values, uint32_t* __restrict__ out,
+                                   int n)
+{
+    const int c = blockIdx.x;
+    if (c >= count)
+        return;
+    const int net = nets[c];
+    for (int k = threadIdx.x; k <= n; k += blockDim.x)
+        out[(size_t)c * (n + 1) + k] = net >= 0 ? values[(size_t)net * (n + 1) + k] : 0u;
+}
+
+__global__ void scatter_tlwe_kernel(const int* __restrict__ nets, int count,
+                                    const uint32_t* __restrict__ src, uint32_t* __restrict__ values,
+                                    int n)
+{
+    const int c = blockIdx.x;
+    if (c >= count)
+        return;
+    const int net = nets[c];
+    if (net < 0)
+        return;
+    for (int k = threadIdx.x; k <= n; k += blockDim.x)
+        values[(size_t)net * (n + 1) + k] = src[(size_t)c * (n + 1) + k];
+}
+
+}  // namespace vsp
+
+struct vsp_netlist {
+    vsp_ctx* ctx = nullptr;
+    int nets = 0;
+    std::vector<int> kind, id, in_off, in_nets, out_off, out_nets;
+    // DAG (buildDag, netlist.cpp:348-432)
+    std::vector<int> dag_cells, level, height, dff_cells;
+    std::vector<int> node_of_cell;
+    int rom_cell = -1, ram_cell = -1, gmax = 0, depth = 0;
+    // per level: gate cells (kinds 0..9) and memory ports
+    std::vector<std::vector<int>> level_gates, level_mem;
+    std::vector<int> const_cells;
+    // device state
+    DevBuf values, dff, gin, gout, nets_buf, inputs_store;
+    std::vector<int> input_nets;     // nets driven by module inputs (setInput targets)
+    std::vector<uint8_t> is_input;   // net -> is module input
+    std::vector<int> dff_q, dff_d;   // per DFF: output net (Q), input net (D)
+    bool table_valid = false;
+    uint64_t cycle = 0;
+    // memory ports
+    DevBuf ram, rom;
+    uint32_t ram_v = 0, ram_w = 0, rom_depth = 0, rom_nluts = 0;
+    bool has_ram = false, has_rom = false;
+};
+
+namespace {
+
+[[noreturn]] void nl_fail(const std::string& m) { throw std::runtime_error("netlist: " + m); }
+
+void build_dag(vsp_netlist* nl)
+{
+    const int C = (int)nl->kind.size();
+    nl->node_of_cell.assign(C, -1);
+    for (int i = 0; i < C; i++) {
+        if (nl->kind[i] == cDff) {
+            nl->dff_cells.push_back(i);
+            continue;
+        }
+        if (nl->kind[i] == cRom)
+            nl->rom_cell = i;
+        if (nl->kind[i] == cRam)
+            nl->ram_cell = i;
+        nl->node_of_cell[i] = (int)nl->dag_cells.size();
+        nl->dag_cells.push_back(i);
+    }
+    std::vector<int> producer(nl->nets, -1);
+    for (int i = 0; i < C; i++)
+        if (nl->node_of_cell[i] >= 0)
+            for (int k = nl->out_off[i]; k < nl->out_off[i + 1]; k++)
+                producer[nl->out_nets[k]] = nl->node_of_cell[i];
+    const int n = (int)nl->dag_cells.size();
+    std::vector<std::vector<int>> consumers(n);
+    std::vector<int> indeg(n, 0);
+    for (int node = 0; node < n; node++) {
+        const int c = nl->dag_cells[node];
+        for (int k = nl->in_off[c]; k < nl->in_off[c + 1]; k++) {
+            const int p = producer[nl->in_nets[k]];
+            if (p >= 0) {
+                consumers[p].push_back(node);
+                indeg[node]++;
+            }
+        }
+    }
+    // Kahn's algorithm; level = longest path from the sources
+    nl->level.assign(n, 0);
+    std::vector<int> q, topo;
+    for (int i = 0; i < n; i++)
+        if (indeg[i] == 0)
+            q.push_back(i);
+    for (size_t h = 0; h < q.size(); h++) {
+        const int node = q[h];
+        topo.push_back(node);
+        for (int cns : consumers[node]) {
+            nl->level[cns] = std::max(nl->level[cns], nl->level[node] + 1);
+            if (--indeg[cns] == 0)
+                q.push_back(cns);
+        }
+    }
+    if ((int)topo.size() != n) {
+        for (int i = 0; i < n; i++)
+            if (indeg[i] > 0)
+                nl_fail("combinational cycle through cell " + std::to_string(nl->id[nl->dag_cells[i]]));
+    }
+    nl->height.assign(n, 0);
+    for (auto it = topo.rbegin(); it != topo.rend(); ++it)
+        for (int cns : consumers[*it])
+            nl->height[*it] = std::max(nl->height[*it], nl->height[cns] + 1);
+    int maxLevel = -1;
+    std::vector<int> width;
+    for (int i = 0; i < n; i++) {
+        maxLevel = std::max(maxLevel, nl->level[i]);
+        if ((int)width.size() <= nl->level[i])
+            width.resize(nl->level[i] + 1, 0);
+        width[nl->level[i]]++;
+    }
+    nl->gmax = 0;
+    for (int w : width)
+        nl->gmax = std::max(nl->gmax, w);
+    nl->depth = maxLevel + 1;
+    nl->level_gates.assign(std::max(nl->depth, 0), {});
+    nl->level_mem.assign(std::max(nl->depth, 0), {});
+    for (int node = 0; node < n; node++) {
+        const int c = nl->dag_cells[node];
+        const int k = nl->kind[c];
+        if (k <= cXor)
+            nl->level_gates[nl->level[node]].push_back(c);
+        else if (k == cRom || k == cRam)
+            nl->level_mem[nl->level[node]].push_back(c);
+        else
+            nl->const_cells.push_back(c);
+    }
+}
+
+// tlweTrivial (ops.cpp:212-217): a = 0, b = +-mu
+std::vector<uint32_t> trivial_tlwe(uint32_t n, bool m)
+{
+    std::vector<uint32_t> t(n + 1, 0);
+    t[n] = m ? kMu32 : 0u - kMu32;
+    return t;
+}
+
+void upload_ints(vsp_ctx* c, DevBuf& buf, const std::vector<int>& v, cudaStream_t st)
+{
+    int* d = buf.as<int>(std::max<size_t>(v.size(), 1));
+    if (!v.empty())
+        VSP_CUDA_CHECK(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    (void)c;
+}
+
+void run_cycle(vsp_netlist* nl, cudaStream_t st)
+{
+    vsp_ctx* c = nl->ctx;
+    const uint32_t n = c->p.n;
+    const size_t n1 = n + 1;
+    uint32_t* vals = nl->values.as<uint32_t>((size_t)nl->nets * n1);
+    // sources: module inputs and DFF outputs (engine.hpp:271-274)
+    if (!nl->input_nets.empty()) {
+        upload_ints(c, nl->nets_buf, nl->input_nets, st);
+        scatter_tlwe_kernel<<<(unsigned)nl->input_nets.size(), 128, 0, st>>>(
+            nl->nets_buf.as<int>(0), (int)nl->input_nets.size(), nl->inputs_store.as<uint32_t>(0),
+            vals, (int)n);
+        c->launches++;
+    }
+    if (!nl->dff_q.empty()) {
+        upload_ints(c, nl->nets_buf, nl->dff_q, st);
+        scatter_tlwe_kernel<<<(unsigned)nl->dff_q.size(), 128, 0, st>>>(
+            nl->nets_buf.as<int>(0), (int)nl->dff_q.size(), nl->dff.as<uint32_t>(0), vals, (int)n);
+        c->launches++;
+    }
+    VSP_CUDA_CHECK(cudaGetLastError());
+    for (int L = 0; L < nl->depth; L++) {
+        const auto& gates = nl->level_gates[L];
+        if (!gates.empty()) {
+            const int G = (int)gates.size();
+            std::vector<int> gnets((size_t)G * 3, -1), onets(G);
+            std::vector<int32_t> kinds(G);
+            for (int g = 0; g < G; g++) {
+                const int cell = gates[g];
+                kinds[g] = nl->kind[cell];  // CellKind 0..9 == GateKind 0..9
+                for (int k = nl->in_off[cell], s = 0; k < nl->in_off[cell + 1]; k++, s++)
+                    gnets[(size_t)g * 3 + s] = nl->in_nets[k];
+                onets[g] = nl->out_nets[nl->out_off[cell]];
+            }
+            upload_ints(c, nl->nets_buf, gnets, st);
+            uint32_t* gin = nl->gin.as<uint32_t>((size_t)G * 3 * n1);
+            uint32_t* gout = nl->gout.as<uint32_t>((size_t)G * n1);
+            gather_tlwe_kernel<<<G * 3, 128, 0, st>>>(nl->nets_buf.as<int>(0), G * 3, vals, gin,
+                                                      (int)n);
+            c->launches++;
+            hom_gate_dev(c, kinds.data(), gin, gout, (size_t)G, st);
+            upload_ints(c, nl->nets_buf, onets, st);
+            scatter_tlwe_kernel<<<G, 128, 0, st>>>(nl->nets_buf.as<int>(0), G, gout, vals, (int)n);
+            c->launches++;
+            VSP_CUDA_CHECK(cudaGetLastError());
+        }
+        for (int cell : nl->level_mem[L]) {
+            std::vector<int> ins(nl->in_nets.begin() + nl->in_off[cell],
+                                 nl->in_nets.begin() + nl->in_off[cell + 1]);
+            std::vector<int> outs(nl->out_nets.begin() + nl->out_off[cell],
+                                  nl->out_nets.begin() + nl->out_off[cell + 1]);
+            upload_ints(c, nl->nets_buf, ins, st);
+            uint32_t* gin = nl->gin.as<uint32_t>(ins.size() * n1);
+            uint32_t* gout = nl->gout.as<uint32_t>(outs.size() * n1);
+            gather_tlwe_kernel<<<(unsigned)ins.size(), 128, 0, st>>>(nl->nets_buf.as<int>(0),
+                                                                      (int)ins.size(), vals, gin,
+                                                                      (int)n);
+            c->launches++;
+            if (nl->kind[cell] == cRom) {  // engine.hpp:361-366
+                if (!nl->has_rom)
+                    throw std::runtime_error("ROM image not bound");
+                rom_read_dev(c, nl->rom.as<uint32_t>(0), (int)nl->rom_nluts, nl->rom_depth, gin,
+                             (int)ins.size(), gout, st);
+            }
+            else {  // engine.hpp:367-376: addr[v], wdata[w], wflag
+                if (!nl->has_ram)
+                    throw std::runtime_error("RAM image not bound");
+                const int w = (int)outs.size();
+                const int v = (int)ins.size() - w - 1;
+                if (v != (int)nl->ram_v || w != (int)nl->ram_w)
+                    throw std::invalid_argument("ramCycle: address width mismatch");
+                ram_cycle_dev(c, nl->ram.as<uint32_t>(0), v, w, gin, gin + (size_t)(v + w) * n1,
+                              gin + (size_t)v * n1, gout, st);
+            }
+            upload_ints(c, nl->nets_buf, outs, st);
+            scatter_tlwe_kernel<<<(unsigned)outs.size(), 128, 0, st>>>(
+                nl->nets_buf.as<int>(0), (int)outs.size(), gout, vals, (int)n);
+            c->launches++;
+            VSP_CUDA_CHECK(cudaGetLastError());
+        }
+    }
+    nl->table_valid = true;
+    // synchronous DFF latch (engine.hpp:341-345): sample every D, then update all Qs
+    if (!nl->dff_d.empty()) {
+        upload_ints(c, nl->nets_buf, nl->dff_d, st);
+        gather_tlwe_kernel<<<(unsigned)nl->dff_d.size(), 128, 0, st>>>(
+            nl->nets_buf.as<int>(0), (int)nl->dff_d.size(), vals, nl->dff.as<uint32_t>(0), (int)n);
+        c->launches++;
+        VSP_CUDA_CHECK(cudaGetLastError());
+    }
+}
+
+}  // namespace

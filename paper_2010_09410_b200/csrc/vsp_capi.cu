@@ -726,6 +726,8 @@ void rom_read_dev(vsp_ctx* c, const uint32_t* d_luts, int nluts, uint32_t depth_
 
 }  // namespace
 
+#include "runner.cuh"
+
 // DFMA throughput probe: 16 independent FMA chains per thread.
 __global__ void fp64_probe_kernel(double* out, int iters, double m)
 {
@@ -1235,6 +1237,242 @@ int vsp_blind_rotate_lvl2_batch(vsp_ctx* c, const uint32_t* in, const uint64_t* 
         VSP_CUDA_CHECK(cudaMemcpyAsync(out, d_acc, T * 2 * N2 * 8, cudaMemcpyDeviceToHost, c->stream));
         VSP_CUDA_CHECK(cudaStreamSynchronize(c->stream));
     });
+}
+
+// ---- netlist runner (hvp::netlist::Evaluator<TfheBackend>) ---------------------
+
+vsp_netlist* vsp_netlist_create(vsp_ctx* c, int32_t net_count, int32_t cells, const int32_t* kinds,
+                                const int32_t* ids, const int32_t* in_off, const int32_t* in_nets,
+                                const int32_t* out_off, const int32_t* out_nets,
+                                const int32_t* input_nets, int32_t n_inputs)
+{
+    vsp_netlist* out = nullptr;
+    guard([&] {
+        std::lock_guard<std::mutex> lk(c->mu);
+        c->set_device();
+        auto nl = std::make_unique<vsp_netlist>();
+        nl->ctx = c;
+        nl->nets = net_count;
+        nl->kind.assign(kinds, kinds + cells);
+        nl->id.assign(ids, ids + cells);
+        nl->in_off.assign(in_off, in_off + cells + 1);
+        nl->out_off.assign(out_off, out_off + cells + 1);
+        nl->in_nets.assign(in_nets, in_nets + in_off[cells]);
+        nl->out_nets.assign(out_nets, out_nets + out_off[cells]);
+        for (int i = 0; i < cells; i++)
+            if (nl->kind[i] < 0 || nl->kind[i] > cConst1)
+                throw std::invalid_argument("netlist: unknown cell kind");
+        for (int x : nl->in_nets)
+            if (x < 0 || x >= net_count)
+                throw std::invalid_argument("netlist: bad net");
+        for (int x : nl->out_nets)
+            if (x < 0 || x >= net_count)
+                throw std::invalid_argument("netlist: bad net");
+        build_dag(nl.get());
+        for (int ci : nl->dff_cells) {
+            nl->dff_q.push_back(nl->out_nets[nl->out_off[ci]]);
+            nl->dff_d.push_back(nl->in_nets[nl->in_off[ci]]);
+        }
+        const size_t n1 = c->p.n + 1;
+        nl->input_nets.assign(input_nets, input_nets + n_inputs);
+        nl->is_input.assign(net_count, 0);
+        for (int x : nl->input_nets)
+            nl->is_input[x] = 1;
+        // initial state: every DFF and module input holds constant(false) (engine.hpp:116-122)
+        const std::vector<uint32_t> f = trivial_tlwe(c->p.n, false), t = trivial_tlwe(c->p.n, true);
+        std::vector<uint32_t> init;
+        auto fill = [&](size_t count) {
+            init.resize(count * n1);
+            for (size_t i = 0; i < count; i++)
+                std::copy(f.begin(), f.end(), init.begin() + i * n1);
+        };
+        fill(std::max<size_t>(nl->dff_cells.size(), 1));
+        uint32_t* d_dff = nl->dff.as<uint32_t>(init.size());
+        VSP_CUDA_CHECK(cudaMemcpy(d_dff, init.data(), init.size() * 4, cudaMemcpyHostToDevice));
+        fill(std::max<int>(n_inputs, 1));
+        uint32_t* d_in = nl->inputs_store.as<uint32_t>(init.size());
+        VSP_CUDA_CHECK(cudaMemcpy(d_in, init.data(), init.size() * 4, cudaMemcpyHostToDevice));
+        fill((size_t)net_count);
+        uint32_t* d_vals = nl->values.as<uint32_t>(init.size());
+        // constants are written once: nothing else drives their nets (engine.hpp:357-360)
+        for (int ci : nl->const_cells) {
+            const auto& v = nl->kind[ci] == cConst1 ? t : f;
+            std::copy(v.begin(), v.end(), init.begin() + (size_t)nl->out_nets[nl->out_off[ci]] * n1);
+        }
+        VSP_CUDA_CHECK(cudaMemcpy(d_vals, init.data(), init.size() * 4, cudaMemcpyHostToDevice));
+        out = nl.release();
+    });
+    return out;
+}
+
+void vsp_netlist_destroy(vsp_netlist* nl)
+{
+    if (!nl)
+        return;
+    cudaSetDevice(nl->ctx->device);
+    cudaStreamSynchronize(nl->ctx->stream);
+    for (DevBuf* b : {&nl->values, &nl->dff, &nl->gin, &nl->gout, &nl->nets_buf, &nl->inputs_store,
+                      &nl->ram, &nl->rom})
+        b->release();
+    delete nl;
+}
+
+// out: [dag nodes, dffs, gMax, depth, rom cell, ram cell]; levels (optional): per DAG node
+// in Netlist::cells order (non-DFF cells), like Dag::level.
+int vsp_netlist_info(vsp_netlist* nl, int32_t* out6, int32_t* levels)
+{
+    return guard([&] {
+        out6[0] = (int)nl->dag_cells.size();
+        out6[1] = (int)nl->dff_cells.size();
+        out6[2] = nl->gmax;
+        out6[3] = nl->depth;
+        out6[4] = nl->rom_cell;
+        out6[5] = nl->ram_cell;
+        if (levels)
+            for (size_t i = 0; i < nl->level.size(); i++)
+                levels[i] = nl->level[i];
+    });
+}
+
+int vsp_netlist_set_input(vsp_netlist* nl, int32_t input_index, const uint32_t* tlwe)
+{
+    return guard([&] {
+        vsp_ctx* c = nl->ctx;
+        std::lock_guard<std::mutex> lk(c->mu);
+        c->set_device();
+        if (input_index < 0 || input_index >= (int)nl->input_nets.size())
+            throw std::out_of_range("netlist input index");
+        const size_t n1 = c->p.n + 1;
+        VSP_CUDA_CHECK(cudaMemcpyAsync(nl->inputs_store.as<uint32_t>(0) + input_index * n1, tlwe,
+                                       n1 * 4, cudaMemcpyHostToDevice, c->stream));
+        VSP_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+// Evaluator::output semantics (engine.hpp:165-176): DFF-driven nets read the DFF state,
+// module inputs their current value, other nets need an evaluated cycle.
+int vsp_netlist_get_net(vsp_netlist* nl, int32_t net, uint32_t* tlwe)
+{
+    return guard([&] {
+        vsp_ctx* c = nl->ctx;
+        std::lock_guard<std::mutex> lk(c->mu);
+        c->set_device();
+        if (net < 0 || net >= nl->nets)
+            throw std::out_of_range("net index");
+        const size_t n1 = c->p.n + 1;
+        const uint32_t* src = nullptr;
+        for (size_t i = 0; i < nl->dff_q.size() && !src; i++)
+            if (nl->dff_q[i] == net)
+                src = nl->dff.as<uint32_t>(0) + i * n1;
+        for (size_t i = 0; i < nl->input_nets.size() && !src; i++)
+            if (nl->input_nets[i] == net)
+                src = nl->inputs_store.as<uint32_t>(0) + i * n1;
+        if (!src) {
+            if (!nl->table_valid)
+                throw std::runtime_error("output needs an evaluated cycle");
+            src = nl->values.as<uint32_t>(0) + (size_t)net * n1;
+        }
+        VSP_CUDA_CHECK(cudaMemcpyAsync(tlwe, src, n1 * 4, cudaMemcpyDeviceToHost, c->stream));
+        VSP_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int vsp_netlist_dff(vsp_netlist* nl, uint32_t* get, const uint32_t* set)
+{
+    return guard([&] {
+        vsp_ctx* c = nl->ctx;
+        std::lock_guard<std::mutex> lk(c->mu);
+        c->set_device();
+        const size_t bytes = nl->dff_cells.size() * (c->p.n + 1) * 4;
+        if (bytes == 0)
+            return;
+        if (set)
+            VSP_CUDA_CHECK(cudaMemcpyAsync(nl->dff.as<uint32_t>(0), set, bytes,
+                                           cudaMemcpyHostToDevice, c->stream));
+        if (get)
+            VSP_CUDA_CHECK(cudaMemcpyAsync(get, nl->dff.as<uint32_t>(0), bytes,
+                                           cudaMemcpyDeviceToHost, c->stream));
+        VSP_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int vsp_netlist_set_rom(vsp_netlist* nl, uint32_t depth_bytes, const uint32_t* luts, uint32_t nluts)
+{
+    return guard([&] {
+        vsp_ctx* c = nl->ctx;
+        std::lock_guard<std::mutex> lk(c->mu);
+        c->set_device();
+        if (nl->rom_cell < 0)
+            throw std::runtime_error("netlist has no ROM port");
+        const size_t words = (size_t)nluts * 2 * c->p.N1;
+        VSP_CUDA_CHECK(cudaMemcpy(nl->rom.as<uint32_t>(words), luts, words * 4, cudaMemcpyHostToDevice));
+        nl->rom_depth = depth_bytes;
+        nl->rom_nluts = nluts;
+        nl->has_rom = true;
+    });
+}
+
+int vsp_netlist_ram(vsp_netlist* nl, uint32_t v, uint32_t w, uint32_t* get, const uint32_t* set)
+{
+    return guard([&] {
+        vsp_ctx* c = nl->ctx;
+        std::lock_guard<std::mutex> lk(c->mu);
+        c->set_device();
+        if (nl->ram_cell < 0)
+            throw std::runtime_error("netlist has no RAM port");
+        const size_t words = ((size_t)w << v) * 2 * c->p.N1;
+        if (set) {
+            VSP_CUDA_CHECK(cudaMemcpy(nl->ram.as<uint32_t>(words), set, words * 4,
+                                      cudaMemcpyHostToDevice));
+            nl->ram_v = v;
+            nl->ram_w = w;
+            nl->has_ram = true;
+        }
+        if (get) {
+            if (!nl->has_ram || v != nl->ram_v || w != nl->ram_w)
+                throw std::runtime_error("RAM image not bound");
+            VSP_CUDA_CHECK(cudaMemcpy(get, nl->ram.as<uint32_t>(0), words * 4, cudaMemcpyDeviceToHost));
+        }
+    });
+}
+
+// Evaluator::run (engine.hpp:238-247).  stats (optional, 4 per cycle): evaluated cells,
+// gMax, depth, seconds (device time of the cycle).
+int vsp_netlist_run(vsp_netlist* nl, uint64_t cycles, double* stats)
+{
+    return guard([&] {
+        vsp_ctx* c = nl->ctx;
+        std::lock_guard<std::mutex> lk(c->mu);
+        c->set_device();
+        cudaEvent_t a, b;
+        VSP_CUDA_CHECK(cudaEventCreate(&a));
+        VSP_CUDA_CHECK(cudaEventCreate(&b));
+        for (uint64_t i = 0; i < cycles; i++) {
+            VSP_CUDA_CHECK(cudaEventRecord(a, c->stream));
+            run_cycle(nl, c->stream);
+            VSP_CUDA_CHECK(cudaEventRecord(b, c->stream));
+            VSP_CUDA_CHECK(cudaEventSynchronize(b));
+            float ms = 0;
+            VSP_CUDA_CHECK(cudaEventElapsedTime(&ms, a, b));
+            if (stats) {
+                stats[4 * i + 0] = (double)nl->dag_cells.size();
+                stats[4 * i + 1] = nl->gmax;
+                stats[4 * i + 2] = nl->depth;
+                stats[4 * i + 3] = ms * 1e-3;
+            }
+            nl->cycle++;
+        }
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+    });
+}
+
+uint64_t vsp_netlist_cycle(vsp_netlist* nl) { return nl->cycle; }
+
+int vsp_netlist_set_cycle(vsp_netlist* nl, uint64_t cycle)
+{
+    nl->cycle = cycle;
+    return 0;
 }
 
 int vsp_counters(vsp_ctx* c, uint64_t out[5])

@@ -1,0 +1,144 @@
+"""GPU netlist runner vs the reference Evaluator<TfheBackend> (oracle/_ref) and vs the
+plaintext backend: bit-exact DFF state and outputs on test-det, decrypted equality on
+tfhe-80 (SPEC.md:363-368 backend equivalence)."""
+import ctypes
+
+import numpy as np
+import pytest
+
+import paper_2010_09410_b200 as vsp
+from oracle import pyoracle
+from oracle.pyoracle import CpuTfhe
+from paper_2010_09410_b200 import netlist as N
+from tests.helpers import oracle_keys
+
+pytestmark = pytest.mark.gpu
+
+
+def words_to_image(words, v, w):
+    img = np.zeros((w << v) // 8, np.uint8)
+    for A, x in enumerate(words):
+        for j in range(w):
+            if (x >> j) & 1:
+                b = A * w + j
+                img[b // 8] |= 1 << (b % 8)
+    return img
+
+
+class RefEval:
+    def __init__(self, r: CpuTfhe, text: str):
+        self.r, self.L = r, r.L
+        self.h = ctypes.c_void_p(self.L.ref_eval_new(r.h, text.encode(), 4))
+        assert self.h.value, self.L.ref_last_error()
+
+    def set_input(self, port, idx, ct):
+        assert self.L.ref_eval_set_input(self.h, port.encode(), idx, ct.ctypes.data, self.r.n) == 0
+
+    def output(self, port, idx):
+        out = np.zeros(self.r.n + 1, np.uint32)
+        assert self.L.ref_eval_output(self.h, port.encode(), idx, out.ctypes.data) == 0
+        return out
+
+    def dff(self):
+        cnt = self.L.ref_eval_dff_count(self.h)
+        out = np.zeros((cnt, self.r.n + 1), np.uint32)
+        assert self.L.ref_eval_get_dff(self.h, out.ctypes.data_as(ctypes.c_void_p),
+                                       ctypes.c_uint32(self.r.n)) == 0
+        return out
+
+    def set_ram(self, ram, v, w):
+        assert self.L.ref_eval_set_ram(self.h, v, w, ram.ctypes.data_as(ctypes.c_void_p),
+                                       self.r.N1) == 0
+
+    def get_ram(self, shape):
+        out = np.zeros(shape, np.uint32)
+        assert self.L.ref_eval_get_ram(self.h, out.ctypes.data_as(ctypes.c_void_p)) == 0
+        return out
+
+    def set_rom(self, luts, depth):
+        assert self.L.ref_eval_set_rom(self.h, depth, luts.ctypes.data_as(ctypes.c_void_p),
+                                       luts.shape[0], self.r.N1) == 0
+
+    def run(self, cycles):
+        assert self.L.ref_eval_run(self.h, cycles, 4, 0, None) == 0, self.L.ref_last_error()
+
+
+@pytest.mark.skipif(not pyoracle.available("ref"), reason="reference not built")
+def test_runner_matches_reference_evaluator_testdet():
+    seed = 515253
+    r = CpuTfhe("ref", "test-det", seed=seed)
+    r.keygen(True)
+    e = vsp.Engine("test-det")
+    e.upload_keys(oracle_keys("test-det", seed, True))
+    nl = N.synthetic_netlist(seed=3, scale=0.03, levels=6, dffs=40, ram=(3, 4))
+    text = N.netlist_to_json(nl)
+    ev = N.Evaluator(nl, e)
+    rev = RefEval(r, text)
+    rng = np.random.default_rng(1)
+    v, w = 3, 4
+    words = [int(x) for x in rng.integers(0, 16, 8)]
+    ram = r.encrypt_ram(words_to_image(words, v, w), v, w)
+    ev.set_ram(ram, v, w)
+    rev.set_ram(ram, v, w)
+    rom_img = rng.integers(0, 256, 512).astype(np.uint8)
+    luts = r.encrypt_rom(rom_img)
+    ev.set_rom(luts, 512)
+    rev.set_rom(luts, 512)
+    for i in range(len(nl.inputs[0].bits)):
+        ct = r.encrypt(int(rng.integers(0, 2)))
+        ev.set_input("in", i, ct)
+        rev.set_input("in", i, ct)
+    init = np.stack([r.encrypt(int(b)) for b in rng.integers(0, 2, ev.n_dffs)])
+    ev.set_dff_state_raw(init)
+    assert rev.L.ref_eval_set_dff(rev.h, init.ctypes.data_as(ctypes.c_void_p),
+                                  ctypes.c_uint32(r.n)) == 0
+    stats = []
+    for cyc in range(2):
+        ev.run(1, N.RunOptions(stats=stats))
+        rev.run(1)
+        assert np.array_equal(ev.dff_state(), rev.dff()), f"DFF state differs at cycle {cyc}"
+        for k in range(16):
+            assert np.array_equal(ev.output("out", k), rev.output("out", k))
+    assert np.array_equal(ev.ram(), rev.get_ram(ram.shape))
+    assert stats[0].evaluated_total == ev.dag_nodes and stats[0].depth == ev.depth
+    assert ev.cycle == 2
+
+
+def test_runner_backend_equivalence_tfhe80():
+    """Decrypted TFHE outputs == PlainBackend outputs every cycle (no memory ports)."""
+    p = vsp.ParameterSet("tfhe-80")
+    k = vsp.keygen(p, 31, False)
+    e = vsp.Engine(p)
+    e.upload_keys(k)
+    nl = N.synthetic_netlist(seed=5, scale=0.04, levels=8, dffs=32, rom=False, ram=None)
+    ev = N.Evaluator(nl, e)
+    pe = N.PlainEvaluator(nl)
+    rng = np.random.default_rng(2)
+    bits = rng.integers(0, 2, ev.n_dffs)
+    ev.set_dff_state_raw(vsp.encrypt(p, k["lv0"], bits, 3))
+    for i, di in enumerate(pe.dff):
+        pe.dff[di] = int(bits[i])
+    for cyc in range(3):
+        ib = rng.integers(0, 2, len(nl.inputs[0].bits))
+        cts = vsp.encrypt(p, k["lv0"], ib, 100 + cyc)
+        for i, b in enumerate(ib):
+            ev.set_input("in", i, cts[i])
+            pe.set_input("in", i, int(b))
+        ev.run(1)
+        pe.run(1)
+        got = vsp.decrypt(k["lv0"], ev.dff_state())
+        want = np.array([pe.dff[i] for i in sorted(pe.dff)], np.uint8)
+        assert np.array_equal(got, want), f"cycle {cyc}"
+        outs = vsp.decrypt(k["lv0"], np.stack([ev.output("out", j) for j in range(16)]))
+        assert list(outs) == [pe.output("out", j) for j in range(16)]
+
+
+def test_runner_errors():
+    e = vsp.Engine("test-det")
+    e.upload_keys(oracle_keys("test-det", 515253, True))
+    nl = N.synthetic_netlist(seed=4, scale=0.01, levels=3, dffs=16, ram=(2, 2))
+    ev = N.Evaluator(nl, e)
+    with pytest.raises(RuntimeError, match="needs an evaluated cycle|ROM image not bound"):
+        ev.output("out", 0) if False else ev.run(1)
+    with pytest.raises(RuntimeError):
+        ev.set_input("nope", 0, np.zeros(17, np.uint32))
