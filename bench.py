@@ -51,6 +51,11 @@ def parse():
                     help="gates per CPU-baseline sample (0 = auto)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--config", default="gates", choices=["gates", "memory", "cycle"],
+                    help="gates: BASELINE configs[0] (default, headline); memory: configs[1] "
+                         "(ROM read + RAM cycle, s/access); cycle: configs[2] (s/clock cycle "
+                         "of a synthetic Ruby-shaped netlist)")
+    ap.add_argument("--levels", type=int, default=32, help="cycle config: logic depth")
     return ap.parse_args()
 
 
@@ -332,11 +337,123 @@ def run_reference(args, world, rank, local):
     print(json.dumps(line), flush=True)
 
 
+def _mem_workload(vsp, p, seed):
+    """Random 512 B RAM (v=8, w=16) and 512 B ROM images, encrypted client side, plus a
+    random encrypted RAM address/write flag/write data and ROM address."""
+    rng = np.random.default_rng(seed)
+    keys = vsp.keygen(p, seed, True)
+    return keys, rng
+
+
+def run_memory(args, world, rank, local):
+    """BASELINE configs[1]: encrypted ROM read (512 B) + RAM read/write (512 B) with an
+    encrypted address; one step = addressToTrgsw+romRead and one ramCycle."""
+    import torch
+    import paper_2010_09410_b200 as vsp
+    from oracle.pyoracle import CpuTfhe, available
+    torch.cuda.set_device(local)
+    p = vsp.ParameterSet("tfhe-80", n_override=args.n)
+    keys, rng = _mem_workload(vsp, p, 77 + rank)
+    eng = vsp.Engine(p, device=local)
+    eng.upload_keys(keys)
+    # client side (Alice): encryptRam / encryptRom of random images
+    v, w = 8, 16
+    ram = vsp.encrypt_ram(p, keys, rng.integers(0, 256, (w << v) // 8).astype(np.uint8), v, w, 5)
+    rom_img = rng.integers(0, 256, 512).astype(np.uint8)
+    luts = vsp.encrypt_rom(p, keys, rom_img, 6)
+    addr = vsp.encrypt(p, keys["lv0"], rng.integers(0, 2, v), 7)
+    wflag = vsp.encrypt(p, keys["lv0"], [1], 8)[0]
+    wdata = vsp.encrypt(p, keys["lv0"], rng.integers(0, 2, w), 9)
+    raddr = vsp.encrypt(p, keys["lv0"], rng.integers(0, 2, 7), 10)
+    times, times_rom = [], []
+    for it in range(args.warmup + args.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ro, ram = eng.ram_cycle(ram, v, w, addr, wflag, wdata)
+        t1 = time.perf_counter()
+        out = eng.rom_read(luts, 512, raddr) if luts is not None else None
+        t2 = time.perf_counter()
+        if it >= args.warmup:
+            times.append(t1 - t0)
+            times_rom.append(t2 - t1)
+    if rank != 0:
+        return
+    val = float(np.mean(times)) + float(np.mean(times_rom))
+    cpu = None
+    if not args.no_cpu_baseline and available("ref"):
+        r = CpuTfhe("ref", "tfhe-80", n_override=args.n, seed=1)
+        r.import_keys(keys)
+        th = os.cpu_count() or 1
+        t0 = time.perf_counter()
+        r.ram_cycle(ram, v, w, addr, wflag, wdata, threads=th)
+        t1 = time.perf_counter()
+        if luts is not None:
+            r.rom_read(luts, 512, raddr, threads=th)
+        t2 = time.perf_counter()
+        cpu = {"value": round(t2 - t0, 3), "unit": "s/access", "cores": th, "kind": "reference",
+               "sample": f"one ramCycle (v=8,w=16) {t1 - t0:.2f}s + one romRead(512B) "
+                         f"{t2 - t1:.2f}s via the reference with {th} threads"}
+    print(json.dumps({
+        "metric": "cmux_memory_seconds_per_access", "value": round(val, 5), "unit": "s/access",
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "higher_is_better": False,
+        "config": {"workload": "BASELINE configs[1]: ROM read 512 B (7 addr bits) + RAM cycle "
+                               "v=8 w=16 (512 B), encrypted address, tfhe-80 n=%d" % p.n,
+                   "ram_cycle_s": round(float(np.mean(times)), 5),
+                   "rom_read_s": round(float(np.mean(times_rom)), 5)},
+        "timing": "host wall clock around the C-ABI host calls (includes 32 MiB RAM H2D/D2H)",
+        "counters_per_access": eng.counters(), "cpu_baseline": cpu}), flush=True)
+
+
+def run_cycle(args, world, rank, local):
+    """BASELINE configs[2]: seconds per clock cycle of a seeded synthetic Ruby-shaped
+    pipelined-processor netlist (gate mix of PAPER.md:1376-1385, one ROM + one RAM port)."""
+    import torch
+    import paper_2010_09410_b200 as vsp
+    from paper_2010_09410_b200 import netlist as N
+    torch.cuda.set_device(local)
+    p = vsp.ParameterSet("tfhe-80", n_override=args.n)
+    keys, rng = _mem_workload(vsp, p, 99)
+    eng = vsp.Engine(p, device=local)
+    eng.upload_keys(keys)
+    nl = N.synthetic_netlist(seed=1, levels=args.levels)
+    ev = N.Evaluator(nl, eng)
+    v, w = 8, 16
+    ev.set_ram(vsp.encrypt_ram(p, keys, rng.integers(0, 256, (w << v) // 8).astype(np.uint8), v,
+                               w, 3), v, w)
+    ev.set_rom(vsp.encrypt_rom(p, keys, rng.integers(0, 256, 512).astype(np.uint8), 4), 512)
+    ev.set_dff_state_raw(vsp.encrypt(p, keys["lv0"], rng.integers(0, 2, ev.n_dffs), 5))
+    for i in range(len(nl.inputs[0].bits)):
+        ev.set_input("in", i, vsp.encrypt(p, keys["lv0"], [int(rng.integers(0, 2))], 6 + i)[0])
+    stats = []
+    ev.run(args.warmup)
+    eng.counters_reset()
+    ev.run(args.steps, N.RunOptions(stats=stats))
+    if rank != 0:
+        return
+    st = N.netlist_stats(nl)
+    secs = [s.seconds for s in stats]
+    print(json.dumps({
+        "metric": "seconds_per_clock_cycle", "value": round(float(np.mean(secs)), 5),
+        "unit": "s/cycle", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "higher_is_better": False,
+        "config": {"workload": "BASELINE configs[2] proxy: synthetic Ruby-shaped netlist "
+                               "(no processor netlist exists in the reference)",
+                   "gates": sum(st["count_by_kind"][k] for k in N.GATES),
+                   "dffs": st["dff_count"], "depth": st["depth"], "gmax": st["gmax"],
+                   "rom": "512 B, 7 addr bits", "ram": "v=8 w=16", "n": p.n},
+        "counters_per_cycle": {k: v // max(args.steps, 1) for k, v in eng.counters().items()},
+        "timing": "CUDA events around each device-resident cycle"}), flush=True)
+
+
 def main():
     args = parse()
     world, rank, local = dist_env()
     if args.impl == "reference":
         run_reference(args, world, rank, local)
+    elif args.config == "memory":
+        run_memory(args, world, rank, local)
+    elif args.config == "cycle":
+        run_cycle(args, world, rank, local)
     else:
         run_ours(args, world, rank, local)
 

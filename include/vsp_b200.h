@@ -191,6 +191,15 @@ int vsp_client_keygen(const vsp_params* params, uint64_t seed, int with_cb, uint
 int vsp_client_tlwe_encrypt(const vsp_params* params, const uint32_t* lv0, uint64_t seed,
                             const uint8_t* bits, size_t count, uint32_t* out);
 
+/* trlweEncrypt (ops.cpp:458-468) of count N1-bit polynomials (alpha1 noise): the cells
+ * of encryptRam / LUTs of encryptRom (mem.cpp:202-263).  out: count x 2*N1. */
+int vsp_client_trlwe_encrypt(const vsp_params* params, const uint32_t* lv1, uint64_t seed,
+                             const uint8_t* bits, size_t count, uint32_t* out);
+
+/* trlwePhaseAt (ops.cpp:494-505) of coefficient k for count TRLWEs. */
+int vsp_client_trlwe_phase_at(const uint32_t* lv1, uint32_t N, const uint32_t* ct, size_t count,
+                              uint32_t k, uint32_t* phases);
+
 /* tlwePhase / tlweDecrypt (ops.cpp:442-456); bits and/or phases may be NULL. */
 int vsp_client_tlwe_decrypt(const uint32_t* key, uint32_t dim, const uint32_t* ct,
                             size_t count, uint8_t* bits, uint32_t* phases);

@@ -72,6 +72,8 @@ def lib() -> ctypes.CDLL:
         L.vsp_client_keygen.argtypes = [ctypes.POINTER(VspParams), u64, ctypes.c_int] + [vp] * 8
         L.vsp_client_tlwe_encrypt.argtypes = [ctypes.POINTER(VspParams), vp, u64, vp, sz, vp]
         L.vsp_client_tlwe_decrypt.argtypes = [vp, u32, vp, sz, vp, vp]
+        L.vsp_client_trlwe_encrypt.argtypes = [ctypes.POINTER(VspParams), vp, u64, vp, sz, vp]
+        L.vsp_client_trlwe_phase_at.argtypes = [vp, u32, vp, sz, u32, vp]
         _lib = L
     return _lib
 
@@ -173,6 +175,63 @@ def phase(key: np.ndarray, ct: np.ndarray) -> np.ndarray:
     _ccheck(lib().vsp_client_tlwe_decrypt(_ptr(np.ascontiguousarray(key, np.uint32)),
                                           len(key), _ptr(flat), flat.shape[0], None, _ptr(ph)))
     return ph.reshape(ct.shape[:-1])
+
+
+def trlwe_encrypt(params: ParameterSet, lv1: np.ndarray, bit_polys, seed: int) -> np.ndarray:
+    """trlweEncrypt (ops.cpp:458-468) of (count, N1) bits -> (count, 2*N1)."""
+    b = np.ascontiguousarray(np.asarray(bit_polys, np.uint8).reshape(-1, params.N1))
+    out = np.zeros((b.shape[0], 2 * params.N1), np.uint32)
+    _ccheck(lib().vsp_client_trlwe_encrypt(ctypes.byref(params.c), _ptr(lv1), seed, _ptr(b),
+                                           b.shape[0], _ptr(out)))
+    return out
+
+
+def trlwe_decrypt_at(lv1: np.ndarray, ct: np.ndarray, k: int = 0) -> np.ndarray:
+    """trlweDecryptAt (ops.cpp:507-510) for (count, 2N) TRLWEs."""
+    ct = np.ascontiguousarray(np.atleast_2d(ct), np.uint32)
+    N = ct.shape[1] // 2
+    ph = np.zeros(ct.shape[0], np.uint32)
+    _ccheck(lib().vsp_client_trlwe_phase_at(_ptr(np.ascontiguousarray(lv1, np.uint32)), N,
+                                            _ptr(ct), ct.shape[0], k, _ptr(ph)))
+    return (ph.view(np.int32) >= 0).astype(np.uint8)
+
+
+def encrypt_ram(params: ParameterSet, keys: dict, image: np.ndarray, v: int, w: int,
+                seed: int) -> np.ndarray:
+    """encryptRam (mem.cpp:202-222): cell j*2^v + A carries bit A*w + j at coefficient 0."""
+    image = np.asarray(image, np.uint8)
+    if image.size != (w << v) // 8:
+        raise ValueError("encryptRam: image size mismatch")
+    bits = np.unpackbits(image, bitorder="little")
+    polys = np.zeros(((w << v), params.N1), np.uint8)
+    for j in range(w):
+        polys[j << v:(j + 1) << v, 0] = bits[np.arange(1 << v) * w + j]
+    return trlwe_encrypt(params, keys["lv1"], polys, seed)
+
+
+def decrypt_ram(keys: dict, ram: np.ndarray, v: int, w: int) -> np.ndarray:
+    """decryptRam (mem.cpp:224-234)."""
+    dec = trlwe_decrypt_at(keys["lv1"], ram, 0)
+    bits = np.zeros(w << v, np.uint8)
+    for j in range(w):
+        bits[np.arange(1 << v) * w + j] = dec[j << v:(j + 1) << v]
+    return np.packbits(bits, bitorder="little")
+
+
+def encrypt_rom(params: ParameterSet, keys: dict, image: np.ndarray, seed: int) -> np.ndarray:
+    """encryptRom (mem.cpp:236-263): LUT t coefficient c carries ROM bit t*N1 + c."""
+    image = np.asarray(image, np.uint8)
+    blocks = image.size // 4
+    if image.size == 0 or image.size % 4 or blocks & (blocks - 1):
+        raise ValueError("encryptRom: image must hold a power-of-two number of 32-bit blocks")
+    vrom = blocks.bit_length() - 1
+    low = min(vrom, (params.N1 // 32).bit_length() - 1)
+    nluts = 1 << (vrom - low)
+    bits = np.unpackbits(image, bitorder="little")
+    polys = np.zeros((nluts, params.N1), np.uint8)
+    flat = polys.reshape(-1)
+    flat[:min(bits.size, flat.size)] = bits[:flat.size]
+    return trlwe_encrypt(params, keys["lv1"], polys, seed)
 
 
 # ---------------------------------------------------------------------------

@@ -367,6 +367,48 @@ int vsp_client_tlwe_encrypt(const vsp_params* pp, const uint32_t* lv0, uint64_t 
     });
 }
 
+// trlweEncrypt (ops.cpp:458-468) of count bit polynomials (N1 bits each) under lv1 with
+// alpha1 noise, one CSPRNG stream; out: count x 2*N1 (a then b).  Used for the RAM/ROM
+// images of encryptRam / encryptRom (mem.cpp:202-263).
+int vsp_client_trlwe_encrypt(const vsp_params* pp, const uint32_t* lv1, uint64_t seed,
+                             const uint8_t* bits, size_t count, uint32_t* out)
+{
+    return cguard([&] {
+        const vsp_params& p = *pp;
+        const Alphas al = alphas_for(p);
+        const size_t N = p.N1;
+        Csprng rng(seed);
+        std::vector<ZeroEnc<uint32_t>> jobs;
+        jobs.reserve(count);
+        for (size_t c = 0; c < count; c++) {
+            uint32_t* o = out + c * 2 * N;
+            draw_zero(rng, o, o + N, N, al.a1);
+            jobs.push_back({o, o + N, N});
+        }
+        finalize_parallel(jobs, lv1);
+        for (size_t c = 0; c < count; c++)
+            for (size_t i = 0; i < N; i++)
+                out[c * 2 * N + N + i] += bits[c * N + i] ? kMu32 : 0u - kMu32;
+    });
+}
+
+// trlwePhaseAt (ops.cpp:494-505) of coefficient k for count TRLWEs (N = dim).
+int vsp_client_trlwe_phase_at(const uint32_t* lv1, uint32_t N, const uint32_t* ct, size_t count,
+                              uint32_t k, uint32_t* phases)
+{
+    return cguard([&] {
+        for (size_t c = 0; c < count; c++) {
+            const uint32_t* a = ct + c * 2 * N;
+            uint32_t acc = 0;
+            for (uint32_t j = 0; j <= k; j++)
+                acc += a[k - j] * lv1[j];
+            for (uint32_t j = k + 1; j < N; j++)
+                acc -= a[k + N - j] * lv1[j];
+            phases[c] = a[N + k] - acc;
+        }
+    });
+}
+
 // tlwePhase / tlweDecrypt (ops.cpp:442-456) for count ciphertexts of dimension dim.
 int vsp_client_tlwe_decrypt(const uint32_t* key, uint32_t dim, const uint32_t* ct, size_t count,
                             uint8_t* bits, uint32_t* phases)

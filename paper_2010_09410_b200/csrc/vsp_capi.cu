@@ -216,22 +216,43 @@ void validate(const Params& p)  // ParameterSet::validate (params.cpp:17-29)
 constexpr int kBrSlots = 2;
 constexpr int kBrBg = 10;  // the FFT path is specialised for Bg1 = 2^10 (tfhe-80)
 
-// Warps (= tasks) per CTA of the blind-rotation kernel: every task costs the same, so
-// choose W in {6, 7, 8} minimising waves x W for T tasks on the device's SMs.
+// Warps (= tasks) per CTA of the blind-rotation kernel.  Every task costs the same, so
+// time ~ waves(W) x t(W), t(W) = duration of one wave with W tasks per SM, measured on
+// B200 at n = 630 (scripts/br_occupancy.py -> profiles/r01_br_occupancy.json):
+// 1-3 tasks/SM are latency-bound (~5.7 ms: 630 dependent steps), 8 tasks/SM 8.7 ms.
+// Narrow netlist levels therefore get one task per SM, wide batches 7-8.
 int br_warps_for(int T, int sms)
 {
-    int best = 8;
-    long best_cost = -1;
-    for (int w = 8; w >= 6; w--) {
+    static const double t[9] = {0, 5.7, 5.7, 5.9, 6.5, 8.3, 8.7, 8.8, 8.7};
+    int best = 1;
+    double best_cost = 1e30;
+    for (int w = 1; w <= 8; w++) {
         const long waves = (T + (long)sms * w - 1) / ((long)sms * w);
-        const long cost = waves * w;
-        if (best_cost < 0 || cost < best_cost) {
+        const double cost = (double)waves * t[w];
+        if (cost < best_cost - 1e-9) {
             best_cost = cost;
             best = w;
         }
     }
     return best;
 }
+
+template <int W>
+void launch_br_w(vsp_ctx* c, const uint32_t* d_tasks, uint32_t* d_trlwe, int T, cudaStream_t st)
+{
+    br1024_kernel<W, kBrSlots, kBrBg><<<(T + W - 1) / W, W * 32, sizeof(Br1024Smem<W, kBrSlots>),
+                                        st>>>(d_tasks, c->d_bk1fd, c->d_tw2, d_trlwe, T,
+                                              (int)c->p.n);
+}
+
+template <int W>
+void set_br_attr()
+{
+    VSP_CUDA_CHECK(cudaFuncSetAttribute(br1024_kernel<W, kBrSlots, kBrBg>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)sizeof(Br1024Smem<W, kBrSlots>)));
+}
+
 constexpr int kChainWarps = 8;
 
 void launch_br(vsp_ctx* c, const uint32_t* d_tasks, uint32_t* d_trlwe, int T, cudaStream_t st)
@@ -242,18 +263,16 @@ void launch_br(vsp_ctx* c, const uint32_t* d_tasks, uint32_t* d_trlwe, int T, cu
     if (p.fft) {
         const int W = br_warps_for(T, c->sms);
         timed(c, "br1024", st, [&] {
-            if (W == 8)
-                br1024_kernel<8, kBrSlots, kBrBg><<<(T + 7) / 8, 256, sizeof(Br1024Smem<8, kBrSlots>),
-                                                    st>>>(d_tasks, c->d_bk1fd, c->d_tw2, d_trlwe,
-                                                          T, (int)p.n);
-            else if (W == 7)
-                br1024_kernel<7, kBrSlots, kBrBg><<<(T + 6) / 7, 224, sizeof(Br1024Smem<7, kBrSlots>),
-                                                    st>>>(d_tasks, c->d_bk1fd, c->d_tw2, d_trlwe,
-                                                          T, (int)p.n);
-            else
-                br1024_kernel<6, kBrSlots, kBrBg><<<(T + 5) / 6, 192, sizeof(Br1024Smem<6, kBrSlots>),
-                                                    st>>>(d_tasks, c->d_bk1fd, c->d_tw2, d_trlwe,
-                                                          T, (int)p.n);
+            switch (W) {
+            case 8: launch_br_w<8>(c, d_tasks, d_trlwe, T, st); break;
+            case 7: launch_br_w<7>(c, d_tasks, d_trlwe, T, st); break;
+            case 6: launch_br_w<6>(c, d_tasks, d_trlwe, T, st); break;
+            case 5: launch_br_w<5>(c, d_tasks, d_trlwe, T, st); break;
+            case 4: launch_br_w<4>(c, d_tasks, d_trlwe, T, st); break;
+            case 3: launch_br_w<3>(c, d_tasks, d_trlwe, T, st); break;
+            case 2: launch_br_w<2>(c, d_tasks, d_trlwe, T, st); break;
+            default: launch_br_w<1>(c, d_tasks, d_trlwe, T, st); break;
+            }
         });
     }
     else {
@@ -328,15 +347,14 @@ void launch_iks(vsp_ctx* c, const uint32_t* d_trlwe, const int2* d_gtask, const 
 // every new context; cudaFuncSetAttribute applies to the current device.
 void configure_kernels()
 {
-    VSP_CUDA_CHECK(cudaFuncSetAttribute(br1024_kernel<8, kBrSlots, kBrBg>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)sizeof(Br1024Smem<8, kBrSlots>)));
-    VSP_CUDA_CHECK(cudaFuncSetAttribute(br1024_kernel<7, kBrSlots, kBrBg>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)sizeof(Br1024Smem<7, kBrSlots>)));
-    VSP_CUDA_CHECK(cudaFuncSetAttribute(br1024_kernel<6, kBrSlots, kBrBg>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)sizeof(Br1024Smem<6, kBrSlots>)));
+    set_br_attr<8>();
+    set_br_attr<7>();
+    set_br_attr<6>();
+    set_br_attr<5>();
+    set_br_attr<4>();
+    set_br_attr<3>();
+    set_br_attr<2>();
+    set_br_attr<1>();
     VSP_CUDA_CHECK(cudaFuncSetAttribute(br2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)sizeof(Br2Smem)));
     VSP_CUDA_CHECK(cudaFuncSetAttribute(cmux_chain1024_kernel<kChainWarps>,

@@ -1,0 +1,24 @@
+"""Measure blind-rotation time vs tasks per SM (W) to calibrate br_warps_for()."""
+import json, sys, time
+import numpy as np, torch
+sys.path.insert(0, ".")
+import paper_2010_09410_b200 as vsp
+p = vsp.ParameterSet("tfhe-80", 630)
+k = vsp.keygen(p, 5, False)
+e = vsp.Engine(p); e.upload_keys(k)
+res = {}
+for T in [1, 8, 74, 148, 296, 444, 592, 740, 888, 1036, 1184]:
+    ins = np.zeros((T, 3, p.n + 1), np.uint32)
+    ins[:, :2] = vsp.encrypt(p, k["lv0"], np.ones(2 * T, np.uint8), 1).reshape(T, 2, p.n + 1)
+    d_in = torch.from_numpy(ins.view(np.int32)).cuda(); d_out = torch.empty((T, p.n + 1), dtype=torch.int32, device="cuda")
+    s = torch.cuda.current_stream()
+    kinds = ["NAND"] * T
+    e.hom_gate_batch_dev(kinds, d_in.data_ptr(), d_out.data_ptr(), T, s.cuda_stream); torch.cuda.synchronize()
+    e.profile_reset(); e.profile_enable(True)
+    for _ in range(3):
+        e.hom_gate_batch_dev(kinds, d_in.data_ptr(), d_out.data_ptr(), T, s.cuda_stream)
+    torch.cuda.synchronize(); e.profile_enable(False)
+    ms, n = e.profile_read("br1024")
+    res[T] = ms / n
+    print(T, round(ms / n, 3), "ms per BR launch", flush=True)
+json.dump(res, open("gpurun_out/br_occupancy.json", "w"))

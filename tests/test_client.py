@@ -34,3 +34,23 @@ def test_client_encrypt_decrypt_roundtrip():
     ph = vsp.phase(k["lv0"], ct).astype(np.int64)
     ph = np.where(ph >= 2**31, ph - 2**32, ph)
     assert np.all(np.abs(np.abs(ph) - vsp.MU32) < 2**29 // 8)
+
+
+def test_client_ram_rom_encryption_layout_matches_reference():
+    """encryptRam / encryptRom layouts (mem.cpp:202-263) against the restatement."""
+    from oracle.pyoracle import CpuTfhe
+    p = vsp.ParameterSet("test-det")
+    k = vsp.keygen(p, 3, False)
+    o = CpuTfhe("orc", "test-det", seed=3)
+    o.keygen(False)
+    img = np.random.default_rng(1).integers(0, 256, 64).astype(np.uint8)
+    ram = vsp.encrypt_ram(p, k, img, 6, 8, 9)
+    assert np.array_equal(vsp.decrypt_ram(k, ram, 6, 8), img)
+    assert np.array_equal(o.decrypt_ram(ram, 6, 8), img)
+    rimg = np.random.default_rng(2).integers(0, 256, 512).astype(np.uint8)
+    rom = vsp.encrypt_rom(p, k, rimg, 3)
+    ref = o.encrypt_rom(rimg, trivial=True)
+    assert rom.shape == ref.shape
+    for t in range(rom.shape[0]):
+        for c in range(0, p.N1, 7):
+            assert vsp.trlwe_decrypt_at(k["lv1"], rom[t], c)[0] == o.trlwe_decrypt_at(ref[t], c)
