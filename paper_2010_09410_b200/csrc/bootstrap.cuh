@@ -411,4 +411,132 @@ __global__ void __launch_bounds__(256) iks_kernel(
     }
 }
 
+// ---------------------------------------------------------------------------
+// Identity key switch, base 2^2 x 8 (tfhe-80), register-tiled over gates.
+//
+// The 3 candidate KSK rows of one (i, j) are loaded ONCE per CTA into registers (lane =
+// output coordinate k, coalesced) and reused by GT gates; each gate's 2-bit digit is
+// warp-uniform (every lane works on the same gate), so the row choice is a uniform
+// branch and the inner work is one u32 add per (gate, k) -- no per-element selects.
+// Warp w of the CTA owns coordinates k = 32*KPT*w + 32*kk + lane; 4 warps cover
+// 128*KPT >= n+1 coordinates.  blockIdx.y splits the input index i; the slices combine
+// with u32 atomicAdd into `out` (pre-set by iks_init_kernel), associative mod 2^32 so
+// bit-exact.  Loads for step (i, j+1) are issued before the adds of step (i, j).
+template <int KPT, int GT>
+__global__ void __launch_bounds__(128) iks_b2_kernel(
+    const uint32_t* __restrict__ trlwe, const int2* __restrict__ gtask,
+    const int* __restrict__ glist, const int* __restrict__ seidx, int Gl,
+    const uint32_t* __restrict__ ksk, uint32_t* __restrict__ out, int n, int N)
+{
+    constexpr int T = 8;  // ksLen
+    extern __shared__ __align__(16) uint16_t dig16[];  // [islice][GT]
+    const int g0 = blockIdx.x * GT;
+    const int ng = min(GT, Gl - g0);
+    const int islice = N / gridDim.y;
+    const int i0 = blockIdx.y * islice;
+    constexpr uint32_t kOffset = 1u << 15;  // 2^(32 - (1 + 2*8)), ops.cpp:661-662
+
+    for (int idx = threadIdx.x; idx < islice * GT; idx += blockDim.x) {
+        const int ii = idx / GT, g = idx % GT;
+        uint32_t w = 0;
+        if (g < ng) {
+            const int gate = glist[g0 + g];
+            uint32_t a;
+            iks_level1_coef(trlwe, gtask[gate], N, seidx ? seidx[gate] : 0, i0 + ii, a);
+            w = (a + kOffset) >> 16;  // digits j = 0..7 at bits 14-2j (top 16 bits of v)
+        }
+        dig16[idx] = (uint16_t)w;
+    }
+    __syncthreads();
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int kbase = warp * 32 * KPT + lane;
+    const size_t rs = (size_t)n + 1;
+
+    uint32_t acc[GT][KPT];
+#pragma unroll
+    for (int g = 0; g < GT; g++)
+#pragma unroll
+        for (int kk = 0; kk < KPT; kk++)
+            acc[g][kk] = 0u;
+
+    // Row pointers of digit d = 1..3 at this lane's first coordinate.  Coordinates past n
+    // read into the next row (or the zeroed tail pad of the key buffer) and are never
+    // stored, so the loads need no clamp and use immediate offsets 32*kk.
+    const uint32_t* p0 = ksk + (size_t)i0 * T * 3 * rs + kbase;
+    const uint32_t* p1 = p0 + rs;
+    const uint32_t* p2 = p0 + 2 * rs;
+    const size_t step = 3 * rs;
+    uint32_t ra[3][KPT], rb[3][KPT];
+    auto load = [&](uint32_t (&r)[3][KPT]) {
+#pragma unroll
+        for (int kk = 0; kk < KPT; kk++) {
+            r[0][kk] = __ldg(p0 + 32 * kk);
+            r[1][kk] = __ldg(p1 + 32 * kk);
+            r[2][kk] = __ldg(p2 + 32 * kk);
+        }
+        p0 += step;
+        p1 += step;
+        p2 += step;
+    };
+    auto consume = [&](const uint32_t (&cur)[3][KPT], int s) {
+        const int ii = s >> 3, j = s & 7;
+        const uint4* dp = reinterpret_cast<const uint4*>(dig16 + ii * GT);
+        uint32_t dw[GT / 2];
+#pragma unroll
+        for (int q = 0; q < GT / 8; q++) {
+            const uint4 v = dp[q];
+            dw[4 * q] = v.x;
+            dw[4 * q + 1] = v.y;
+            dw[4 * q + 2] = v.z;
+            dw[4 * q + 3] = v.w;
+        }
+        const int sh = 14 - 2 * j;
+#pragma unroll
+        for (int g = 0; g < GT; g++) {
+            const uint32_t d = (dw[g >> 1] >> ((g & 1) * 16 + sh)) & 3u;
+            if (d == 0)
+                continue;
+            if (d == 1) {
+#pragma unroll
+                for (int kk = 0; kk < KPT; kk++)
+                    acc[g][kk] += cur[0][kk];
+            }
+            else if (d == 2) {
+#pragma unroll
+                for (int kk = 0; kk < KPT; kk++)
+                    acc[g][kk] += cur[1][kk];
+            }
+            else {
+#pragma unroll
+                for (int kk = 0; kk < KPT; kk++)
+                    acc[g][kk] += cur[2][kk];
+            }
+        }
+    };
+
+    const int steps = islice * T;  // even (T = 8)
+    load(ra);
+#pragma unroll 1
+    for (int s = 0; s < steps; s += 2) {
+        load(rb);
+        consume(ra, s);
+        if (s + 2 < steps)
+            load(ra);
+        consume(rb, s + 1);
+    }
+#pragma unroll
+    for (int g = 0; g < GT; g++) {
+        if (g >= ng)
+            break;
+        const int gate = glist[g0 + g];
+#pragma unroll
+        for (int kk = 0; kk < KPT; kk++) {
+            const int k = kbase + 32 * kk;
+            if (k <= n && acc[g][kk] != 0u)
+                atomicAdd(out + (size_t)gate * rs + k, 0u - acc[g][kk]);  // RED.ADD
+        }
+    }
+}
+
 }  // namespace vsp

@@ -308,7 +308,28 @@ void launch_iks(vsp_ctx* c, const uint32_t* d_trlwe, const int2* d_gtask, const 
     timed(c, "iks", st, [&] {
         iks_init_kernel<<<Gl, 128, 0, st>>>(d_trlwe, d_gtask, d_glist, d_seidx, Gl, d_out, p.n,
                                             p.N1);
-        if (p.ksBaseBits == 2 && p.ksLen <= 8) {
+        const int kpt4 = (int)((p.n + 1 + 127) / 128);
+        if (p.ksBaseBits == 2 && p.ksLen == 8 && kpt4 >= 1 && kpt4 <= 5) {
+            constexpr int GT = 16;
+            const int tiles = (Gl + GT - 1) / GT;
+            int split = 1;
+            while (split < 64 && split * 2 <= (int)p.N1 && tiles * split < 6 * c->sms)
+                split *= 2;
+            const dim3 grid(tiles, split);
+            const size_t smem = (size_t)(p.N1 / split) * GT * sizeof(uint16_t);
+#define VSP_IKS_B2(K)                                                                       \
+    iks_b2_kernel<K, GT><<<grid, 128, smem, st>>>(d_trlwe, d_gtask, d_glist, d_seidx, Gl, \
+                                                  c->d_ksk, d_out, p.n, p.N1)
+            switch (kpt4) {
+            case 1: VSP_IKS_B2(1); break;
+            case 2: VSP_IKS_B2(2); break;
+            case 3: VSP_IKS_B2(3); break;
+            case 4: VSP_IKS_B2(4); break;
+            default: VSP_IKS_B2(5); break;
+            }
+#undef VSP_IKS_B2
+        }
+        else if (p.ksBaseBits == 2 && p.ksLen <= 8) {
             constexpr int GT = 32;
             const int tiles = (Gl + GT - 1) / GT;
             const int split = iks_split(tiles, (int)p.N1);
@@ -883,8 +904,11 @@ int vsp_upload_keys(vsp_ctx* c, const uint32_t* bk1, const uint32_t* ksk, const 
         }
         if (c->d_ksk)
             cudaFree(c->d_ksk);
-        VSP_CUDA_CHECK(cudaMalloc(&c->d_ksk, c->ksk_words() * 4));
+        // zeroed tail pad: iks_b2_kernel reads up to 640 words past the last row start
+        constexpr size_t kKskPad = 1024;
+        VSP_CUDA_CHECK(cudaMalloc(&c->d_ksk, (c->ksk_words() + kKskPad) * 4));
         VSP_CUDA_CHECK(cudaMemcpy(c->d_ksk, ksk, c->ksk_words() * 4, cudaMemcpyHostToDevice));
+        VSP_CUDA_CHECK(cudaMemset(c->d_ksk + c->ksk_words(), 0, kKskPad * 4));
         c->has_cb = false;
         if (has_cb) {
             const size_t bk2_words = (size_t)p.n * 2 * p.l2 * 2 * p.N2;
