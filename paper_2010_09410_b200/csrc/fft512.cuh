@@ -52,7 +52,19 @@ __host__ __device__ constexpr bool tw_form_a(int root, int d, int b)
     return m <= 16 || m >= 48;
 }
 constexpr int kFftXbufStride = 544;  // 512 + 32 swizzle pad (double2 units)
-constexpr int kTw2Entries = 23;      // 1+2+4+8 (stages 4-7) + 8 (stage 8)
+// Per-lane twiddle table: stage d (4..7) of the second pass splits block
+// b = (L' << (d-4)) | jt (L' = lane >> 1, jt = top d-4 bits of the register index) and
+// zeta_{d,b} = zeta_{d,L'<<(d-4)} * exp(i pi br(jt) / 2^(d-4)) = entry[d][m] * i^q with
+// k = br(jt) << (7-d) = 4q + m: only the q = 0 values are stored (1, 1, 2, 4 for
+// stages 4-7 and 4 for stage 8); multiplying by i is a swap/negate folded into the
+// butterfly.  12 loads per transform instead of 23 (the kernels are shared-memory bound).
+constexpr int kTw2Entries = 12;
+
+__host__ __device__ constexpr int tw_k(int d, int jt) { return bitrev_const(jt, d - 4) << (7 - d); }
+__host__ __device__ constexpr int tw_entry(int d, int m)
+{
+    return d == 4 ? 0 : d == 5 ? 1 : d == 6 ? 2 + (m >> 1) : d == 7 ? 4 + m : 8 + m;
+}
 
 __device__ __forceinline__ void bf_fwd(double2& u, double2& v, const double2 w)
 {
@@ -62,6 +74,26 @@ __device__ __forceinline__ void bf_fwd(double2& u, double2& v, const double2 w)
     v.y = u.y - ty;
     u.x = u.x + tx;
     u.y = u.y + ty;
+}
+
+// Forward butterfly with twiddle i*w.
+__device__ __forceinline__ void bf_fwd_i(double2& u, double2& v, const double2 w)
+{
+    const double tx = w.x * v.x - w.y * v.y;
+    const double ty = w.x * v.y + w.y * v.x;
+    v.x = u.x + ty;
+    v.y = u.y - tx;
+    u.x = u.x - ty;
+    u.y = u.y + tx;
+}
+
+template <int Q>
+__device__ __forceinline__ void bf_fwd_q(double2& u, double2& v, const double2 w)
+{
+    if (Q)
+        bf_fwd_i(u, v, w);
+    else
+        bf_fwd(u, v, w);
 }
 
 // Forward butterfly with a tangent-form twiddle: 6 FMAs instead of 2 MUL + 2 FMA + 4 ADD.
@@ -94,6 +126,25 @@ __device__ __forceinline__ void bf_inv(double2& a, double2& b, const double2 w)
     b.y = dy * w.x - dx * w.y;
 }
 
+// Inverse butterfly with twiddle i*w: (a, b) -> (a + b, (a - b) conj(w) (-i)).
+__device__ __forceinline__ void bf_inv_i(double2& a, double2& b, const double2 w)
+{
+    const double dx = a.x - b.x, dy = a.y - b.y;
+    a.x = a.x + b.x;
+    a.y = a.y + b.y;
+    b.y = -(dx * w.x + dy * w.y);
+    b.x = dy * w.x - dx * w.y;
+}
+
+template <int Q>
+__device__ __forceinline__ void bf_inv_q(double2& a, double2& b, const double2 w)
+{
+    if (Q)
+        bf_inv_i(a, b, w);
+    else
+        bf_inv(a, b, w);
+}
+
 // An opaque zero: keeps the compiler from hoisting the per-stage twiddle loads out of
 // the blind-rotation loop (which would pin ~60 registers for the whole kernel).
 __device__ __forceinline__ int opaque_zero()
@@ -110,10 +161,86 @@ __device__ __forceinline__ double2 shfl_xor_d2(double2 v, int m)
     return v;
 }
 
-// Forward transform in place.  xbuf: per-warp smem, kFftXbufStride double2.
-// tw2: smem table [kTw2Entries][32] double2.
-template <int ROOT = 0>
-__device__ __forceinline__ void fft512_fwd(double2 (&v)[16], double2* xbuf,
+// The one data exchange of the transform: lane L's value j sits at position L + 32 j
+// before it and at (L & 1) + 2 j + 32 (L >> 1) after it (stride-34 padding keeps both
+// phases bank-conflict free).  HALF moves the real parts, then the imaginary parts,
+// through a 16 x 34 double buffer (4.3 KB per warp instead of 8.7 KB).
+template <bool HALF>
+__device__ __forceinline__ void xpose_fwd(double2 (&v)[16], void* buf, int lane)
+{
+    const int rbase = (lane & 1) + 34 * (lane >> 1);
+    if constexpr (HALF) {
+        double* xb = static_cast<double*>(buf);
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 16; j++)
+            xb[lane + 34 * j] = v[j].x;
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 16; j++)
+            v[j].x = xb[rbase + 2 * j];
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 16; j++)
+            xb[lane + 34 * j] = v[j].y;
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 16; j++)
+            v[j].y = xb[rbase + 2 * j];
+    }
+    else {
+        double2* xb = static_cast<double2*>(buf);
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 16; j++)
+            xb[lane + 34 * j] = v[j];
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 16; j++)
+            v[j] = xb[rbase + 2 * j];
+    }
+}
+
+template <bool HALF>
+__device__ __forceinline__ void xpose_inv(double2 (&v)[16], void* buf, int lane)
+{
+    const int rbase = (lane & 1) + 34 * (lane >> 1);
+    if constexpr (HALF) {
+        double* xb = static_cast<double*>(buf);
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 16; j++)
+            xb[rbase + 2 * j] = v[j].x;
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 16; j++)
+            v[j].x = xb[lane + 34 * j];
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 16; j++)
+            xb[rbase + 2 * j] = v[j].y;
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 16; j++)
+            v[j].y = xb[lane + 34 * j];
+    }
+    else {
+        double2* xb = static_cast<double2*>(buf);
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 16; j++)
+            xb[rbase + 2 * j] = v[j];
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 16; j++)
+            v[j] = xb[lane + 34 * j];
+    }
+}
+
+// Forward transform in place.  xbuf: per-warp smem, kFftXbufStride double2 (HALF:
+// kFftXbufStride doubles).  tw2: smem table [kTw2Entries][32] double2.
+template <int ROOT = 0, bool HALF = false>
+__device__ __forceinline__ void fft512_fwd(double2 (&v)[16], void* xbuf,
                                            const double2* tw2, int lane)
 {
     const double2* tw1t = &c_tw1t[ROOT][0] + opaque_zero();
@@ -131,22 +258,20 @@ __device__ __forceinline__ void fft512_fwd(double2 (&v)[16], double2* xbuf,
                     bf_fwd_tan<false>(v[j], v[j + h], kt);
             }
     }
-    __syncwarp();
-#pragma unroll
-    for (int j = 0; j < 16; j++)
-        xbuf[lane + 34 * j] = v[j];
-    __syncwarp();
-    const int rbase = (lane & 1) + 34 * (lane >> 1);
-#pragma unroll
-    for (int j = 0; j < 16; j++)
-        v[j] = xbuf[rbase + 2 * j];
+    xpose_fwd<HALF>(v, xbuf, lane);
 #pragma unroll
     for (int d = 4; d < 8; d++) {
         const int h = 8 >> (d - 4);
 #pragma unroll
         for (int j = 0; j < 16; j++)
-            if ((j & h) == 0)
-                bf_fwd(v[j], v[j + h], tw2[((1 << (d - 4)) - 1 + (j >> (8 - d))) * 32 + lane]);
+            if ((j & h) == 0) {
+                const int k = tw_k(d, j >> (8 - d));
+                const double2 w = tw2[tw_entry(d, k & 3) * 32 + lane];
+                if (k >> 2)
+                    bf_fwd_q<1>(v[j], v[j + h], w);
+                else
+                    bf_fwd_q<0>(v[j], v[j + h], w);
+            }
     }
     const bool odd = lane & 1;
 #pragma unroll
@@ -155,22 +280,32 @@ __device__ __forceinline__ void fft512_fwd(double2 (&v)[16], double2* xbuf,
         const double2 recv = shfl_xor_d2(send, 1);
         double2 u = odd ? recv : v[k];
         double2 w = odd ? v[k + 8] : recv;
-        bf_fwd(u, w, tw2[(15 + k) * 32 + lane]);
+        const int br = bitrev_const(k, 3);
+        const double2 t = tw2[tw_entry(8, br & 3) * 32 + lane];
+        if (br >> 2)
+            bf_fwd_q<1>(u, w, t);
+        else
+            bf_fwd_q<0>(u, w, t);
         v[k] = u;
         v[k + 8] = w;
     }
 }
 
 // Exact inverse of fft512_fwd up to the factor 512 (folded into the key).
-template <int ROOT = 0>
-__device__ __forceinline__ void fft512_inv(double2 (&v)[16], double2* xbuf,
+template <int ROOT = 0, bool HALF = false>
+__device__ __forceinline__ void fft512_inv(double2 (&v)[16], void* xbuf,
                                            const double2* tw2, int lane)
 {
     const bool odd = lane & 1;
 #pragma unroll
     for (int k = 0; k < 8; k++) {
         double2 a = v[k], b = v[k + 8];
-        bf_inv(a, b, tw2[(15 + k) * 32 + lane]);
+        const int br = bitrev_const(k, 3);
+        const double2 t = tw2[tw_entry(8, br & 3) * 32 + lane];
+        if (br >> 2)
+            bf_inv_q<1>(a, b, t);
+        else
+            bf_inv_q<0>(a, b, t);
         const double2 send = odd ? a : b;
         const double2 recv = shfl_xor_d2(send, 1);
         v[k] = odd ? recv : a;
@@ -181,18 +316,16 @@ __device__ __forceinline__ void fft512_inv(double2 (&v)[16], double2* xbuf,
         const int h = 8 >> (d - 4);
 #pragma unroll
         for (int j = 0; j < 16; j++)
-            if ((j & h) == 0)
-                bf_inv(v[j], v[j + h], tw2[((1 << (d - 4)) - 1 + (j >> (8 - d))) * 32 + lane]);
+            if ((j & h) == 0) {
+                const int k = tw_k(d, j >> (8 - d));
+                const double2 w = tw2[tw_entry(d, k & 3) * 32 + lane];
+                if (k >> 2)
+                    bf_inv_q<1>(v[j], v[j + h], w);
+                else
+                    bf_inv_q<0>(v[j], v[j + h], w);
+            }
     }
-    __syncwarp();
-    const int rbase = (lane & 1) + 34 * (lane >> 1);
-#pragma unroll
-    for (int j = 0; j < 16; j++)
-        xbuf[rbase + 2 * j] = v[j];
-    __syncwarp();
-#pragma unroll
-    for (int j = 0; j < 16; j++)
-        v[j] = xbuf[lane + 34 * j];
+    xpose_inv<HALF>(v, xbuf, lane);
     const double2* tw1 = &c_tw1[ROOT][0] + opaque_zero();
 #pragma unroll
     for (int d = 3; d >= 0; d--) {

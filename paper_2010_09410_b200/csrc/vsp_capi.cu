@@ -123,15 +123,32 @@ void twiddles(int root, double2* tw1, double2* tw1t, std::vector<double2>& tw2)
                 tw_form_a(root, d, b) ? make_double2((double)cosl(a), (double)tanl(a))
                                       : make_double2((double)sinl(a), (double)(cosl(a) / sinl(a)));
         }
+    // compressed per-lane table (fft512.cuh, kTw2Entries): store the q = 0 twiddles and
+    // check that every q = 1 twiddle is i times a stored one
     tw2.assign(kTw2Entries * 32, make_double2(0, 0));
+    auto put = [&](int e, int L, double2 z) { tw2[e * 32 + L] = z; };
+    auto check_i = [&](int e, int L, double2 z) {
+        const double2 w = tw2[e * 32 + L];  // z must equal i * w
+        if (fabs(z.x + w.y) > 1e-15 || fabs(z.y - w.x) > 1e-15)
+            throw std::logic_error("twiddle table: i-symmetry violated");
+    };
     for (int L = 0; L < 32; L++) {
         const uint32_t hi = L >> 1, odd = L & 1;
-        int e = 0;
-        for (int d = 4; d < 8; d++)
-            for (uint32_t s = 0; s < (1u << (d - 4)); s++)
-                tw2[(e++) * 32 + L] = zeta_root(t0, d, (hi << (d - 4)) | s);
-        for (uint32_t k = 0; k < 8; k++)
-            tw2[(e++) * 32 + L] = zeta_root(t0, 8, hi * 16 + k + 8 * odd);
+        for (int pass = 0; pass < 2; pass++) {
+            for (int d = 4; d < 8; d++)
+                for (int jt = 0; jt < (1 << (d - 4)); jt++) {
+                    const int k = tw_k(d, jt);
+                    const double2 z = zeta_root(t0, d, (hi << (d - 4)) | (uint32_t)jt);
+                    if ((k >> 2) == pass)
+                        pass == 0 ? put(tw_entry(d, k & 3), L, z) : check_i(tw_entry(d, k & 3), L, z);
+                }
+            for (int k = 0; k < 8; k++) {
+                const int br = bitrev_const(k, 3);
+                const double2 z = zeta_root(t0, 8, hi * 16 + (uint32_t)k + 8 * odd);
+                if ((br >> 2) == pass)
+                    pass == 0 ? put(tw_entry(8, br & 3), L, z) : check_i(tw_entry(8, br & 3), L, z);
+            }
+        }
     }
 }
 
@@ -261,19 +278,42 @@ void launch_br(vsp_ctx* c, const uint32_t* d_tasks, uint32_t* d_trlwe, int T, cu
         return;
     const Params& p = c->p;
     if (p.fft) {
-        const int W = br_warps_for(T, c->sms);
-        timed(c, "br1024", st, [&] {
+        // Every task costs the same and one CTA (W tasks) runs per SM, so a partial last
+        // wave of W = 8 would cost a full wave: run the whole waves at W = 8 and spread
+        // the remainder as one wave of ceil(rem / SMs) tasks per SM (cheaper per wave).
+        const long wave8 = 8L * c->sms;
+        const int full = (br_warps_for(T, c->sms) == 8 && T > wave8) ? (int)(T / wave8 * wave8) : 0;
+        int forced = 0;
+        if (const char* e = getenv("VSP_BR_WARPS"))  // tuning knob (scripts/br_occupancy.py)
+            forced = atoi(e);
+        auto launch_part = [&](const uint32_t* tk, uint32_t* tr, int cnt, int W) {
             switch (W) {
-            case 8: launch_br_w<8>(c, d_tasks, d_trlwe, T, st); break;
-            case 7: launch_br_w<7>(c, d_tasks, d_trlwe, T, st); break;
-            case 6: launch_br_w<6>(c, d_tasks, d_trlwe, T, st); break;
-            case 5: launch_br_w<5>(c, d_tasks, d_trlwe, T, st); break;
-            case 4: launch_br_w<4>(c, d_tasks, d_trlwe, T, st); break;
-            case 3: launch_br_w<3>(c, d_tasks, d_trlwe, T, st); break;
-            case 2: launch_br_w<2>(c, d_tasks, d_trlwe, T, st); break;
-            default: launch_br_w<1>(c, d_tasks, d_trlwe, T, st); break;
+            case 8: launch_br_w<8>(c, tk, tr, cnt, st); break;
+            case 7: launch_br_w<7>(c, tk, tr, cnt, st); break;
+            case 6: launch_br_w<6>(c, tk, tr, cnt, st); break;
+            case 5: launch_br_w<5>(c, tk, tr, cnt, st); break;
+            case 4: launch_br_w<4>(c, tk, tr, cnt, st); break;
+            case 3: launch_br_w<3>(c, tk, tr, cnt, st); break;
+            case 2: launch_br_w<2>(c, tk, tr, cnt, st); break;
+            default: launch_br_w<1>(c, tk, tr, cnt, st); break;
             }
+            VSP_CUDA_CHECK(cudaGetLastError());
+            c->launches++;
+        };
+        timed(c, "br1024", st, [&] {
+            if (forced) {
+                launch_part(d_tasks, d_trlwe, T, forced);
+                return;
+            }
+            if (full)
+                launch_part(d_tasks, d_trlwe, full, 8);
+            const int rem = T - full;
+            if (rem)
+                launch_part(d_tasks + (size_t)full * (p.n + 1), d_trlwe + (size_t)full * 2 * p.N1,
+                            rem, br_warps_for(rem, c->sms));
         });
+        c->counters[1] += (uint64_t)T;
+        return;
     }
     else {
         const int N = (int)p.N1;
