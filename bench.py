@@ -37,6 +37,7 @@ UNIT = "gates/s"
 # Algorithmic work per external product and per level-1 bootstrap:
 # F_EP = (2l+2)*5*M*log2(M) + 2l*2*8*M with M = 512, l = 2.
 F_EP = (2 * 2 + 2) * 5 * 512 * 9 + 2 * 2 * 2 * 8 * 512
+KERNEL_TIMERS = ("br1024", "br_lat", "iks", "gate_prep", "cmux_chain", "br2", "pks")
 
 
 def parse():
@@ -367,6 +368,8 @@ def run_memory(args, world, rank, local):
     raddr = vsp.encrypt(p, keys["lv0"], rng.integers(0, 2, 7), 10)
     times, times_rom = [], []
     for it in range(args.warmup + args.steps):
+        if it == args.warmup:
+            eng.counters_reset()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         ro, ram = eng.ram_cycle(ram, v, w, addr, wflag, wdata)
@@ -401,7 +404,8 @@ def run_memory(args, world, rank, local):
                    "ram_cycle_s": round(float(np.mean(times)), 5),
                    "rom_read_s": round(float(np.mean(times_rom)), 5)},
         "timing": "host wall clock around the C-ABI host calls (includes 32 MiB RAM H2D/D2H)",
-        "counters_per_access": eng.counters(), "cpu_baseline": cpu}), flush=True)
+        "counters_per_access": {k: v // max(args.steps, 1) for k, v in eng.counters().items()},
+        "cpu_baseline": cpu}), flush=True)
 
 
 def run_cycle(args, world, rank, local):
@@ -427,7 +431,12 @@ def run_cycle(args, world, rank, local):
     stats = []
     ev.run(args.warmup)
     eng.counters_reset()
+    eng.profile_reset()
+    eng.profile_enable(True)
     ev.run(args.steps, N.RunOptions(stats=stats))
+    eng.synchronize()
+    eng.profile_enable(False)
+    kernels = {k: round(eng.profile_read(k)[0] / args.steps, 3) for k in KERNEL_TIMERS}
     if rank != 0:
         return
     st = N.netlist_stats(nl)
@@ -442,6 +451,7 @@ def run_cycle(args, world, rank, local):
                    "dffs": st["dff_count"], "depth": st["depth"], "gmax": st["gmax"],
                    "rom": "512 B, 7 addr bits", "ram": "v=8 w=16", "n": p.n},
         "counters_per_cycle": {k: v // max(args.steps, 1) for k, v in eng.counters().items()},
+        "kernel_ms_per_cycle": kernels,
         "timing": "CUDA events around each device-resident cycle"}), flush=True)
 
 

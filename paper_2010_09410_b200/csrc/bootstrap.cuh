@@ -225,6 +225,177 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
 }
 
 // ---------------------------------------------------------------------------
+// Latency-optimised blind rotation for narrow netlist levels (T <= ~2 x SMs), where
+// br1024_kernel runs one dependent chain of n external products per warp and per-level
+// latency is the chain length (630 x ~9 us).  Here FOUR warps share one task: warp r
+// owns gadget row r = 2P + lvl (digit level lvl of accumulator polynomial P), so each
+// external product is one forward transform + one MAC row deep instead of four:
+//   1. warp r: digits of row r of (X^bara - 1) acc   (decomposePoly, poly.hpp:79-97)
+//   2. warp r: forward transform, partial products A_r = z.bkA_r, B_r = z.bkB_r
+//   3. one smem exchange: warp 0 gathers A = sum A_r, warp 1 gathers B = sum B_r
+//   4. warps 0 / 1: inverse transform, round, acc.a / acc.b += (ops.cpp:587-597)
+// The four row products are summed in row order as in br1024_kernel (here as separate
+// products then adds instead of a fused chain); every coefficient is an integer the
+// FP64 error (<< 1/2) rounds back to exactly, so outputs equal the reference's.  All four BK rows of step i are
+// staged together (64 KiB) by the bulk-copy engine, two steps in flight.
+constexpr int kLatBuf = kFftXbufStride;  // double2 per exchange / transpose buffer
+
+struct BrLatSmem {
+    double2 ring[2][4 * 1024];
+    double2 tw2[kTw2Entries * 32];
+    double2 bufA[4][kLatBuf];  // row partials of output A / B; warp r's forward
+    double2 bufB[4][kLatBuf];  // transposes use xbuf[r] (aliases bufA[r], see below)
+    uint32_t acc[2048];
+    uint64_t full[2];
+    __device__ double2* xbuf(int r) { return bufA[r]; }
+};
+
+__device__ __forceinline__ void bar_group(int id, int nthreads)
+{
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// PROBE: per-warp clock64 totals of the step phases -> probe[task][warp][16] (tuning).
+template <int BG, bool PROBE = false>
+__global__ void __launch_bounds__(128, 1)
+    br_lat_kernel(const uint32_t* __restrict__ tasks, const double2* __restrict__ bkfd,
+                  const double2* __restrict__ tw2g, uint32_t* __restrict__ out, int n,
+                  unsigned long long* __restrict__ probe = nullptr)
+{
+    unsigned long long ph[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    long long tprev = PROBE ? clock64() : 0;
+    auto mark = [&](int k) {
+        if constexpr (PROBE) {
+            const long long t = clock64();
+            ph[k] += (unsigned long long)(t - tprev);
+            tprev = t;
+        }
+    };
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    auto& sm = *reinterpret_cast<BrLatSmem*>(smem_raw);
+    const int r = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int task = blockIdx.x;
+    const uint32_t* lwe = tasks + (size_t)task * (n + 1);
+    const int P = r >> 1, lvl = r & 1;
+
+    for (int i = threadIdx.x; i < kTw2Entries * 32; i += blockDim.x)
+        sm.tw2[i] = tw2g[i];
+    if (threadIdx.x == 0) {
+        mbar_init(&sm.full[0], 1);
+        mbar_init(&sm.full[1], 1);
+    }
+    {
+        const uint32_t rot = (2048u - mod_switch_2n(lwe[n], 11)) & 2047u;
+        for (int q = threadIdx.x; q < 1024; q += blockDim.x) {
+            sm.acc[q] = 0;
+            uint32_t val;
+            if (rot < 1024)
+                val = ((uint32_t)q < rot) ? (0u - kMu32) : kMu32;
+            else
+                val = ((uint32_t)q < rot - 1024) ? kMu32 : (0u - kMu32);
+            sm.acc[1024 + q] = val;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < 2 && s < n; s++) {
+            mbar_arrive_expect_tx(&sm.full[s], 65536);
+            bulk_g2s(sm.ring[s], bkfd + (size_t)s * 4096, 65536, &sm.full[s]);
+        }
+    }
+
+    constexpr uint32_t kHalf = 1u << (BG - 1);
+    constexpr uint32_t kMask = (1u << BG) - 1;
+    constexpr uint32_t kOffset = (kHalf << (32 - BG)) + (kHalf << (32 - 2 * BG));
+    const uint32_t* src = sm.acc + P * 1024;
+    const uint32_t sh = (uint32_t)(32 - (lvl + 1) * BG);
+
+#pragma unroll 1
+    for (int i = 0; i < n; i++) {
+        const uint32_t bara = mod_switch_2n(lwe[i], 11);
+        double2 z[16];
+        {
+            const uint32_t lo = (uint32_t)lane + (uint32_t)opaque_zero();
+            const uint32_t lk = lo - bara;
+            const uint32_t* srcl = src + lo;
+#pragma unroll
+            for (int j = 0; j < 16; j++) {
+                const uint32_t v0 = rot_coef1024(src, lk + 32 * j) - srcl[32 * j] + kOffset;
+                const uint32_t v1 = rot_coef1024(src, lk + 32 * j + 512) - srcl[32 * j + 512] + kOffset;
+                // level lvl digit = bits [32 - (lvl+1) BG, 32 - lvl BG) of v, recentred;
+                // one code path for both levels (the mask is a no-op for lvl 0)
+                const uint32_t d0 = ((v0 >> sh) & kMask) - kHalf;
+                const uint32_t d1 = ((v1 >> sh) & kMask) - kHalf;
+                z[j].x = (double)(int32_t)d0;
+                z[j].y = (double)(int32_t)d1;
+            }
+        }
+        mark(0);
+        fft512_fwd(z, sm.xbuf(r), sm.tw2, lane);
+        mark(1);
+        const int s = i & 1;
+        mbar_wait(&sm.full[s], (uint32_t)((i >> 1) & 1));
+        mark(2);
+        const double2* bk = sm.ring[s] + r * 1024;
+        // partial products of row r -> bufA[r], bufB[r] (one code path for all warps)
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 16; j++) {
+            const double2 ba = bk[j * 32 + lane];
+            const double2 bb = bk[512 + j * 32 + lane];
+            sm.bufA[r][j * 32 + lane] = make_double2(fma(z[j].x, ba.x, -z[j].y * ba.y),
+                                                     fma(z[j].x, ba.y, z[j].y * ba.x));
+            sm.bufB[r][j * 32 + lane] = make_double2(fma(z[j].x, bb.x, -z[j].y * bb.y),
+                                                     fma(z[j].x, bb.y, z[j].y * bb.x));
+        }
+        mark(3);
+        bar_group(1, 128);  // all partials written; every warp is done with ring slot s
+        mark(4);
+        // refill from warp 3 (idle until the next step): issuing a bulk copy can hold the
+        // issuing warp, so keep it off the inverse-transform warps' critical path
+        if (threadIdx.x == 96 && i + 2 < n) {
+            fence_proxy_async();
+            mbar_arrive_expect_tx(&sm.full[s], 65536);
+            bulk_g2s(sm.ring[s], bkfd + (size_t)(i + 2) * 4096, 65536, &sm.full[s]);
+        }
+        if (r < 2) {
+            // warp 0 sums output A, warp 1 output B, rows in order 0..3 (as br1024_kernel)
+            const double2(*pr)[kLatBuf] = r == 0 ? sm.bufA : sm.bufB;
+            double2 acc2[16];
+#pragma unroll
+            for (int j = 0; j < 16; j++) {
+                const double2 a0 = pr[0][j * 32 + lane], a1 = pr[1][j * 32 + lane];
+                const double2 a2 = pr[2][j * 32 + lane], a3 = pr[3][j * 32 + lane];
+                acc2[j] = make_double2(((a0.x + a1.x) + a2.x) + a3.x, ((a0.y + a1.y) + a2.y) + a3.y);
+            }
+            mark(5);
+            // transposes in the exchange buffer of a row only this warp reads
+            fft512_inv(acc2, r == 0 ? sm.bufA[3] : sm.bufB[3], sm.tw2, lane);
+            mark(6);
+            uint32_t* dst = sm.acc + r * 1024;
+#pragma unroll
+            for (int j = 0; j < 16; j++) {
+                const int p = lane + 32 * j;
+                dst[p] += (uint32_t)__double2ll_rn(acc2[j].x);
+                dst[p + 512] += (uint32_t)__double2ll_rn(acc2[j].y);
+            }
+            mark(7);
+        }
+        bar_group(2, 128);  // acc updated before the next step's digits
+        mark(8);
+    }
+    if constexpr (PROBE) {
+        if (lane == 0)
+            for (int k = 0; k < 9; k++)
+                probe[((size_t)task * 4 + r) * 16 + k] = ph[k];
+    }
+    uint4* dst = reinterpret_cast<uint4*>(out + (size_t)task * 2048);
+    const uint4* s4 = reinterpret_cast<const uint4*>(sm.acc);
+    for (int q = threadIdx.x; q < 512; q += blockDim.x)
+        dst[q] = s4[q];
+}
+
+// ---------------------------------------------------------------------------
 // Gate linear combinations (linComb + per-kind coefficients, ops.cpp:774-893).
 // Emits the level-0 TLWE input of each blind-rotation task; NOT is finished here
 // (pure negation, ops.cpp:849-855).

@@ -300,6 +300,34 @@ void launch_br(vsp_ctx* c, const uint32_t* d_tasks, uint32_t* d_trlwe, int T, cu
             VSP_CUDA_CHECK(cudaGetLastError());
             c->launches++;
         };
+        if (!forced && T <= 2 * c->sms) {
+            // narrow level: latency kernel, 4 warps per task (bootstrap.cuh br_lat_kernel)
+            static const bool probe = getenv("VSP_LAT_PROBE") != nullptr;  // tuning only
+            if (probe) {
+                unsigned long long* d_pr = nullptr;
+                VSP_CUDA_CHECK(cudaMalloc(&d_pr, (size_t)T * 64 * 8));
+                br_lat_kernel<kBrBg, true><<<T, 128, sizeof(BrLatSmem), st>>>(
+                    d_tasks, c->d_bk1fd, c->d_tw2, d_trlwe, (int)p.n, d_pr);
+                std::vector<unsigned long long> h(64);
+                VSP_CUDA_CHECK(cudaMemcpyAsync(h.data(), d_pr, 64 * 8, cudaMemcpyDeviceToHost, st));
+                VSP_CUDA_CHECK(cudaStreamSynchronize(st));
+                cudaFree(d_pr);
+                for (int w = 0; w < 4; w++) {
+                    fprintf(stderr, "br_lat probe warp %d cycles/step:", w);
+                    for (int k = 0; k < 9; k++)
+                        fprintf(stderr, " %.0f", (double)h[w * 16 + k] / p.n);
+                    fprintf(stderr, "\n");
+                }
+            }
+            timed(c, "br_lat", st, [&] {
+                br_lat_kernel<kBrBg><<<T, 128, sizeof(BrLatSmem), st>>>(d_tasks, c->d_bk1fd,
+                                                                      c->d_tw2, d_trlwe, (int)p.n);
+            });
+            VSP_CUDA_CHECK(cudaGetLastError());
+            c->launches++;
+            c->counters[1] += (uint64_t)T;
+            return;
+        }
         timed(c, "br1024", st, [&] {
             if (forced) {
                 launch_part(d_tasks, d_trlwe, T, forced);
@@ -408,6 +436,12 @@ void launch_iks(vsp_ctx* c, const uint32_t* d_trlwe, const int2* d_gtask, const 
 // every new context; cudaFuncSetAttribute applies to the current device.
 void configure_kernels()
 {
+    VSP_CUDA_CHECK(cudaFuncSetAttribute(br_lat_kernel<kBrBg>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)sizeof(BrLatSmem)));
+    VSP_CUDA_CHECK(cudaFuncSetAttribute(br_lat_kernel<kBrBg, true>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)sizeof(BrLatSmem)));
     set_br_attr<8>();
     set_br_attr<7>();
     set_br_attr<6>();
