@@ -8,9 +8,9 @@ n=630, N=1024, l=2, Bg=2^10).  One "step" = one pass of the hot path over the ba
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--gates G]
 
-Multi-GPU (launched by torchrun): every rank bootstraps its own independent batch
-(weak scaling; gates of one netlist level shard with no data-path exchange), value =
-all gates / max-over-ranks device time.
+Multi-GPU (launched by torchrun): one level of G x N gates; each rank bootstraps its
+contiguous slice of G gates and the engine all-gathers the level's outputs over NCCL
+(weak scaling); value = all gates / max-over-ranks device time.
 
 Prints ONE JSON line (rank 0).  `value` is device-timed with CUDA events with inputs
 resident in HBM and L2 flushed between steps; `e2e` is the same metric through the
@@ -154,6 +154,10 @@ def traffic_from_profiles():
 
 
 def run_ours(args, world, rank, local):
+    """One step = one netlist level of G x world independent gates, sharded across the
+    ranks by the engine (vsp_hom_gate_level_dev: each GPU bootstraps its contiguous slice
+    of G gates, then one NCCL all-gather over NVLink leaves every output on every GPU).
+    N = 1 is the same call with no exchange."""
     import torch
     import paper_2010_09410_b200 as vsp
 
@@ -164,17 +168,22 @@ def run_ours(args, world, rank, local):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     p = vsp.ParameterSet("tfhe-80", n_override=args.n)
     G = args.gates
-    keys, kinds, ins, truth = make_workload(vsp, p, G, 1000 + rank)
+    GA = G * world
+    # identical keys and level on every rank (keys are replicated)
+    keys, kinds, ins, truth = make_workload(vsp, p, GA, 1000)
     eng = vsp.Engine(p, device=local)
     eng.upload_keys(keys)
+    if world > 1:
+        eng.connect()
+    lo, hi, _ = vsp.level_partition(GA, world, rank)
 
     d_in = torch.from_numpy(ins.view(np.int32)).to(f"cuda:{local}")
-    d_out = torch.empty((G, p.n + 1), dtype=torch.int32, device=f"cuda:{local}")
+    d_out = torch.empty((GA, p.n + 1), dtype=torch.int32, device=f"cuda:{local}")
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=f"cuda:{local}")
     stream = torch.cuda.current_stream()
 
     def step():
-        eng.hom_gate_batch_dev(kinds, d_in.data_ptr(), d_out.data_ptr(), G, stream.cuda_stream)
+        eng.hom_gate_level_dev(kinds, d_in.data_ptr(), d_out.data_ptr(), GA, stream.cuda_stream)
 
     for _ in range(max(args.warmup, 1)):
         step()
@@ -214,28 +223,46 @@ def run_ours(args, world, rank, local):
     if dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
-    value = G * world * args.steps / (ms_max / 1e3)
+    value = GA * args.steps / (ms_max / 1e3)
 
-    # ---- end to end through the C ABI with pinned host buffers ----
+    # ---- end to end: host level in, host level out, through the engine API ----
     e2e = None
     if not args.no_e2e:
-        h_in = torch.from_numpy(ins.view(np.int32)).pin_memory()
-        h_out = torch.empty((G, p.n + 1), dtype=torch.int32).pin_memory()
-        h_in_np, h_out_np = h_in.numpy().view(np.uint32), h_out.numpy().view(np.uint32)
-        eng.hom_gate_batch(kinds, h_in_np)  # warm
-        if dist:
+        if world == 1:
+            h_in = torch.from_numpy(ins.view(np.int32)).pin_memory()
+            h_in_np = h_in.numpy().view(np.uint32)
+            res = eng.hom_gate_batch(kinds, h_in_np)  # warm
+            t0 = time.perf_counter()
+            for _ in range(args.steps):
+                res = eng.hom_gate_batch(kinds, h_in_np)
+            dt = time.perf_counter() - t0
+            h2d, d2h, api = int(ins.nbytes), int(res.nbytes), \
+                "vsp_hom_gate_batch (C ABI, pinned host buffers)"
+        else:
+            # each rank uploads its slice, the engine shards + all-gathers, every rank
+            # reads the whole level back (pinned host buffers, copies inside the timing)
+            h_in = torch.from_numpy(ins[lo:hi].view(np.int32)).pin_memory()
+            h_out = torch.empty((GA, p.n + 1), dtype=torch.int32).pin_memory()
+
+            def e2e_step():
+                d_in[lo:hi].copy_(h_in, non_blocking=True)
+                step()
+                h_out.copy_(d_out, non_blocking=True)
+                torch.cuda.synchronize()
+
+            e2e_step()
             dist.barrier()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            res = eng.hom_gate_batch(kinds, h_in_np)
-        dt = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            for _ in range(args.steps):
+                e2e_step()
+            dt = time.perf_counter() - t0
+            h2d, d2h, api = int(ins.nbytes), int(world * h_out.numel() * 4), \
+                "vsp_hom_gate_level_dev (C ABI, NCCL all-gather) + pinned H2D/D2H per rank"
         te = torch.tensor([dt], dtype=torch.float64, device=f"cuda:{local}")
         if dist:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": G * world * args.steps / float(te.item()), "unit": UNIT,
-               "h2d_bytes_per_step": int(ins.nbytes), "d2h_bytes_per_step": int(res.nbytes),
-               "api": "vsp_hom_gate_batch (C ABI, pinned host buffers)"}
-        del h_out_np, h_out
+        e2e = {"value": GA * args.steps / float(te.item()), "unit": UNIT,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "api": api}
 
     if rank != 0:
         if dist:
@@ -272,11 +299,13 @@ def run_ours(args, world, rank, local):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32+f64",
         "data": "synthetic (seeded client keygen + encryption of uniform random bits)",
-        "config": {"workload": f"{G} random NAND/XOR gates per GPU, tfhe-80 with n={p.n} "
-                               "(BASELINE.json configs[0])",
+        "config": {"workload": f"one level of {GA} random NAND/XOR gates ({G} per GPU), "
+                               f"tfhe-80 with n={p.n} (BASELINE.json configs[0])",
                    "gates_per_gpu": G, "n": p.n, "N": p.N1, "l": p.l1, "Bg_bits": p.Bg1Bits,
                    "ks": f"2^{p.ksBaseBits} x {p.ksLen}", "l2": "flushed (512 MiB write) "
-                   "between timed steps", "parallelism": f"dp{world} (independent batches)"},
+                   "between timed steps",
+                   "parallelism": f"level sharded over {world} GPU(s), outputs all-gathered "
+                                  "over NCCL" if world > 1 else "1 GPU"},
         "outputs_decrypt_correct": correct,
         "gpu_launches": int(launches),
         "e2e": e2e,

@@ -153,6 +153,21 @@ int vsp_netlist_run(vsp_netlist* nl, uint64_t cycles, double* stats);
 uint64_t vsp_netlist_cycle(vsp_netlist* nl);
 int vsp_netlist_set_cycle(vsp_netlist* nl, uint64_t cycle);
 
+/* ---- multi-GPU --------------------------------------------------------
+ * One process per GPU.  Rank 0 creates an NCCL unique id, the host distributes it (e.g.
+ * torch.distributed broadcast), every rank attaches its context.  Afterwards the
+ * netlist runner shards each level's gates across the ranks (contiguous slices of
+ * ceil(G/world)) and all-gathers the output TLWEs over NVLink; keys stay replicated.
+ * The reference has no distributed path (parallelFor on host threads only). */
+int vsp_nccl_unique_id(uint8_t out[128]);
+int vsp_attach_comm(vsp_ctx* ctx, const uint8_t id[128], int rank, int world);
+/* The slice [lo, hi) of a G-gate level owned by `rank`; per = ceil(G / world) slots. */
+int vsp_level_partition(size_t G, int world, int rank, size_t* lo, size_t* hi, size_t* per);
+/* homGate over one whole level, sharded across the attached ranks: every rank passes
+ * all G gates' inputs (device) and receives all G outputs (device) on `stream`. */
+int vsp_hom_gate_level_dev(vsp_ctx* ctx, const int32_t* kinds, const uint32_t* d_in,
+                           uint32_t* d_out, size_t G, void* stream);
+
 /* OpCounters (counters.hpp:11-28): cmux, blindRotate, identityKeySwitch,
  * privateKeySwitch, circuitBootstrap — counted per batched operation exactly as
  * the reference increments them per call. */

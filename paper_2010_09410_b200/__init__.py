@@ -74,6 +74,12 @@ def lib() -> ctypes.CDLL:
         L.vsp_client_tlwe_decrypt.argtypes = [vp, u32, vp, sz, vp, vp]
         L.vsp_client_trlwe_encrypt.argtypes = [ctypes.POINTER(VspParams), vp, u64, vp, sz, vp]
         L.vsp_client_trlwe_phase_at.argtypes = [vp, u32, vp, sz, u32, vp]
+        L.vsp_nccl_unique_id.argtypes = [vp]
+        L.vsp_attach_comm.argtypes = [vp, vp, ctypes.c_int, ctypes.c_int]
+        L.vsp_level_partition.argtypes = [sz, ctypes.c_int, ctypes.c_int,
+                                          ctypes.POINTER(sz), ctypes.POINTER(sz),
+                                          ctypes.POINTER(sz)]
+        L.vsp_hom_gate_level_dev.argtypes = [vp, vp, vp, vp, sz, vp]
         _lib = L
     return _lib
 
@@ -427,6 +433,50 @@ class Engine:
 
     def profile_reset(self):
         _check(lib().vsp_profile_reset(self.h))
+
+    # ---- multi-GPU --------------------------------------------------
+    def attach_comm(self, uid: bytes, rank: int, world: int):
+        """Join the NCCL communicator `uid` (from nccl_unique_id on rank 0) as `rank`;
+        afterwards netlist levels are sharded across the ranks and all-gathered."""
+        buf = np.frombuffer(bytes(uid), np.uint8).copy()
+        if buf.size != 128:
+            raise ValueError("attach_comm: NCCL unique id must be 128 bytes")
+        _check(lib().vsp_attach_comm(self.h, _ptr(buf), int(rank), int(world)))
+        self.rank, self.world = int(rank), int(world)
+
+    def connect(self, group=None):
+        """attach_comm over an initialised torch.distributed group (any backend): rank 0
+        creates the NCCL id, a broadcast distributes it."""
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        box = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0, group=group)
+        self.attach_comm(box[0], rank, world)
+
+    def hom_gate_level_dev(self, kinds, d_in_ptr: int, d_out_ptr: int, G: int,
+                           stream: int = 0):
+        """homGate over one netlist level sharded across the attached ranks (device
+        buffers holding ALL G gates on every rank)."""
+        kid = self._kind_ids(kinds)
+        _check(lib().vsp_hom_gate_level_dev(self.h, _ptr(kid), ctypes.c_void_p(d_in_ptr),
+                                            ctypes.c_void_p(d_out_ptr), G,
+                                            ctypes.c_void_p(stream)))
+
+
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId through the engine (NCCL is dlopen'ed by the library)."""
+    buf = np.zeros(128, np.uint8)
+    _check(lib().vsp_nccl_unique_id(_ptr(buf)))
+    return buf.tobytes()
+
+
+def level_partition(G: int, world: int, rank: int) -> tuple[int, int, int]:
+    """The runner's per-rank slice [lo, hi) of a G-gate level and the padded per-rank
+    slot count ceil(G / world) (multi.cuh level_slice)."""
+    lo, hi, per = ctypes.c_size_t(), ctypes.c_size_t(), ctypes.c_size_t()
+    _check(lib().vsp_level_partition(G, world, rank, ctypes.byref(lo), ctypes.byref(hi),
+                                     ctypes.byref(per)))
+    return int(lo.value), int(hi.value), int(per.value)
 
 
 def fp64_peak_tflops(device: int = 0) -> float:

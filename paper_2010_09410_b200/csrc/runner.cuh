@@ -8,6 +8,11 @@
 // values; each level's gates become ONE batched gate-bootstrap launch sequence, and
 // the memory ports of the level run the batched CMUX-memory pipeline.  The value
 // table, DFF state and the RAM image stay resident in HBM across cycles.
+//
+// With a communicator attached (vsp_attach_comm) every rank runs the same runner on its
+// own GPU: each level's gates are sharded across the ranks and all-gathered
+// (hom_gate_level_dev, multi.cuh); memory ports run replicated (identical deterministic
+// results on every rank), so the DFF latch stays rank-local.
 #pragma once
 
 namespace vsp {
@@ -214,7 +219,7 @@ void run_cycle(vsp_netlist* nl, cudaStream_t st)
             gather_tlwe_kernel<<<G * 3, 128, 0, st>>>(nl->nets_buf.as<int>(0), G * 3, vals, gin,
                                                       (int)n);
             c->launches++;
-            hom_gate_dev(c, kinds.data(), gin, gout, (size_t)G, st);
+            hom_gate_level_dev(c, kinds.data(), gin, gout, (size_t)G, st);  // sharded when world > 1
             upload_ints(c, nl->nets_buf, onets, st);
             scatter_tlwe_kernel<<<G, 128, 0, st>>>(nl->nets_buf.as<int>(0), G, gout, vals, (int)n);
             c->launches++;

@@ -177,6 +177,10 @@ struct vsp_ctx {
         pairs;
     uint64_t counters[5] = {0, 0, 0, 0, 0};
     uint64_t launches = 0;
+    // multi-GPU (multi.cuh): NCCL communicator over the ranks, level slices staged here
+    void* comm = nullptr;  // ncclComm_t
+    int rank = 0, world = 1;
+    DevBuf mg_send, mg_recv;
     std::mutex mu;
     // optional per-kernel CUDA-event timing (bench.py's live roofline)
     bool profiling = false;
@@ -839,6 +843,7 @@ void rom_read_dev(vsp_ctx* c, const uint32_t* d_luts, int nluts, uint32_t depth_
 
 }  // namespace
 
+#include "multi.cuh"
 #include "runner.cuh"
 
 // DFMA throughput probe: 16 independent FMA chains per thread.
@@ -938,6 +943,10 @@ void vsp_destroy(vsp_ctx* c)
     for (void* q : {(void*)c->d_bk2fd, (void*)c->d_tv2[0], (void*)c->d_tv2[1]})
         if (q)
             cudaFree(q);
+    c->mg_send.release();
+    c->mg_recv.release();
+    if (c->comm)
+        nccl().commDestroy((ncclComm_t)c->comm);
     cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -1604,6 +1613,64 @@ int vsp_counters_reset(vsp_ctx* c)
 }
 
 uint64_t vsp_kernel_launches(vsp_ctx* c) { return c->launches; }
+
+// ---- multi-GPU ------------------------------------------------------------------
+
+int vsp_nccl_unique_id(uint8_t out[128])
+{
+    return guard([&] {
+        static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+        ncclUniqueId id;
+        nccl_check(nccl().getUniqueId(&id), "ncclGetUniqueId");
+        std::memcpy(out, &id, sizeof id);
+    });
+}
+
+int vsp_attach_comm(vsp_ctx* c, const uint8_t id[128], int rank, int world)
+{
+    return guard([&] {
+        if (world < 1 || rank < 0 || rank >= world)
+            throw std::invalid_argument("attach_comm: bad rank/world");
+        std::lock_guard<std::mutex> lk(c->mu);
+        c->set_device();
+        if (c->comm) {
+            nccl().commDestroy((ncclComm_t)c->comm);
+            c->comm = nullptr;
+        }
+        c->rank = rank;
+        c->world = world;
+        if (world > 1) {
+            ncclUniqueId uid;
+            std::memcpy(&uid, id, sizeof uid);
+            ncclComm_t comm;
+            nccl_check(nccl().commInitRank(&comm, world, uid, rank), "ncclCommInitRank");
+            c->comm = comm;
+        }
+    });
+}
+
+int vsp_level_partition(size_t G, int world, int rank, size_t* lo, size_t* hi, size_t* per)
+{
+    return guard([&] {
+        if (world < 1 || rank < 0 || rank >= world)
+            throw std::invalid_argument("level_partition: bad rank/world");
+        const Slice sl = level_slice(G, world, rank);
+        *lo = sl.lo;
+        *hi = sl.hi;
+        *per = sl.per;
+    });
+}
+
+int vsp_hom_gate_level_dev(vsp_ctx* c, const int32_t* kinds, const uint32_t* d_in,
+                           uint32_t* d_out, size_t G, void* stream)
+{
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(c->mu);
+        c->set_device();
+        hom_gate_level_dev(c, kinds, d_in, d_out, G, (cudaStream_t)stream);
+        VSP_CUDA_CHECK(cudaGetLastError());
+    });
+}
 
 int vsp_profile_enable(vsp_ctx* c, int on)
 {

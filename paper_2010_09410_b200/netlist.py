@@ -467,26 +467,82 @@ class PlainEvaluator:
                 vals[self.nl.cells[i].outputs[0]] = v
             for ci in self.order:
                 c = self.nl.cells[ci]
-                x = [vals[b] for b in c.inputs]
                 if c.kind in GATES:
-                    vals[c.outputs[0]] = plain_gate(c.kind, x)
-                elif c.kind == "CONST0":
-                    vals[c.outputs[0]] = 0
-                elif c.kind == "CONST1":
-                    vals[c.outputs[0]] = 1
-                elif c.kind == "ROM":
-                    blk = sum(b << i for i, b in enumerate(x))
-                    word = int.from_bytes(bytes(self.rom[4 * blk:4 * blk + 4]), "little")
-                    for k, o in enumerate(c.outputs):
-                        vals[o] = (word >> k) & 1
-                elif c.kind == "RAM":
-                    v, w, words = self.ram
-                    a = sum(b << i for i, b in enumerate(x[:v]))
-                    old = words[a]
-                    if x[v + w]:
-                        words[a] = sum(b << i for i, b in enumerate(x[v:v + w]))
-                    for k, o in enumerate(c.outputs):
-                        vals[o] = (old >> k) & 1
+                    vals[c.outputs[0]] = plain_gate(c.kind, [vals[b] for b in c.inputs])
+                else:
+                    self._eval_port(c, vals)
+            for i in self.dff:
+                self.dff[i] = vals[self.nl.cells[i].inputs[0]]
+
+    def _eval_port(self, c, vals):
+        """Constants and memory ports (PlainBackend::romRead / ramCycle, engine.cpp:83-111)."""
+        x = [vals[b] for b in c.inputs]
+        if c.kind == "CONST0":
+            vals[c.outputs[0]] = 0
+        elif c.kind == "CONST1":
+            vals[c.outputs[0]] = 1
+        elif c.kind == "ROM":
+            blk = sum(b << i for i, b in enumerate(x))
+            word = int.from_bytes(bytes(self.rom[4 * blk:4 * blk + 4]), "little")
+            for k, o in enumerate(c.outputs):
+                vals[o] = (word >> k) & 1
+        elif c.kind == "RAM":
+            v, w, words = self.ram
+            a = sum(b << i for i, b in enumerate(x[:v]))
+            old = words[a]
+            if x[v + w]:
+                words[a] = sum(b << i for i, b in enumerate(x[v:v + w]))
+            for k, o in enumerate(c.outputs):
+                vals[o] = (old >> k) & 1
+
+
+class ShardedPlainEvaluator(PlainEvaluator):
+    """The multi-GPU runner's schedule on plaintext bits (CPU, any torch.distributed
+    backend, e.g. gloo): every ASAP level's gates are split with the runner's own
+    partition (level_partition, multi.cuh) and each rank evaluates only its slice; the
+    slices are all-gathered (the runner's ncclAllGather) before the next level; memory
+    ports and constants are evaluated on every rank, DFFs latch locally.  Must equal
+    PlainEvaluator exactly (tests/test_multi_cpu.py)."""
+
+    def __init__(self, nl: Netlist, group=None):
+        super().__init__(nl)
+        import torch.distributed as dist
+        from . import level_partition
+        self._dist, self._part, self.group = dist, level_partition, group
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        lv = self.dag["level"]
+        depth = self.dag["depth"]
+        self.levels = [[] for _ in range(depth)]
+        for node, ci in enumerate(self.dag["dag_cells"]):  # runner order: DAG node order
+            self.levels[lv[node]].append(ci)
+        self.gate_evals = 0  # gates this rank evaluated (the shard)
+
+    def run(self, cycles=1):
+        dist = self._dist
+        for _ in range(cycles):
+            vals = self.values
+            for b, v in self.inputs.items():
+                vals[b] = v
+            for i, v in self.dff.items():
+                vals[self.nl.cells[i].outputs[0]] = v
+            for cells in self.levels:
+                gates = [ci for ci in cells if self.nl.cells[ci].kind in GATES]
+                lo, hi, per = self._part(len(gates), self.world, self.rank)
+                mine = [plain_gate(self.nl.cells[ci].kind,
+                                   [vals[b] for b in self.nl.cells[ci].inputs])
+                        for ci in gates[lo:hi]]
+                self.gate_evals += len(mine)
+                if gates:
+                    box = [None] * self.world
+                    dist.all_gather_object(box, mine + [0] * (per - len(mine)), group=self.group)
+                    flat = [x for part in box for x in part][:len(gates)]
+                    for ci, v in zip(gates, flat):
+                        vals[self.nl.cells[ci].outputs[0]] = v
+                for ci in cells:
+                    c = self.nl.cells[ci]
+                    if c.kind in GATES:
+                        continue
+                    self._eval_port(c, vals)
             for i in self.dff:
                 self.dff[i] = vals[self.nl.cells[i].inputs[0]]
 
