@@ -151,6 +151,22 @@ int vsp_netlist_ram(vsp_netlist* nl, uint32_t v, uint32_t w, uint32_t* get, cons
  * gMax, depth, seconds) or NULL. */
 int vsp_netlist_run(vsp_netlist* nl, uint64_t cycles, double* stats);
 uint64_t vsp_netlist_cycle(vsp_netlist* nl);
+/* Geometry (v, w) of the bound RAM image (Evaluator::ram().enc.geom). */
+int vsp_netlist_ram_geometry(vsp_netlist* nl, uint32_t* v, uint32_t* w);
+/* Netlist::name (netlist.hpp:58), recorded in snapshots. */
+int vsp_netlist_set_name(vsp_netlist* nl, const char* name);
+/* snapshotSave / snapshotLoad / snapshotPeek (snapshot.hpp:17-33, snapshot.cpp:84-176):
+ * the reference's "HVPS" byte format, so snapshots move between this runner and
+ * hvp::netlist::Evaluator<TfheBackend> in both directions.  param_name is the parameter
+ * set's name (ParameterSet::name) written/checked in the header.  save: out == NULL
+ * returns the size in *len.  load errors are VSP_ERUNTIME with the reference's text
+ * (magic, version, backend, parameter set, netlist name/hash, truncated input). */
+int vsp_netlist_snapshot_save(vsp_netlist* nl, const char* param_name, uint8_t* out,
+                              size_t cap, size_t* len);
+int vsp_netlist_snapshot_load(vsp_netlist* nl, const char* param_name, const uint8_t* in,
+                              size_t len);
+int vsp_snapshot_peek(const uint8_t* in, size_t len, char* backend, char* param,
+                      char* netlist, size_t cap);
 int vsp_netlist_set_cycle(vsp_netlist* nl, uint64_t cycle);
 
 /* ---- multi-GPU --------------------------------------------------------

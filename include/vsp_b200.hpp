@@ -518,7 +518,9 @@ public:
         }
         for (const auto& port : nl.inputs)
             inputNets.insert(inputNets.end(), port.bits.begin(), port.bits.end());
-        return Runner(bk, nl.netCount, kinds, ids, inOff, inNets, outOff, outNets, inputNets);
+        Runner r(bk, nl.netCount, kinds, ids, inOff, inNets, outOff, outNets, inputNets);
+        r.setName(nl.name);
+        return r;
     }
 
     Runner(const Runner&) = delete;
@@ -583,6 +585,26 @@ public:
         std::vector<uint32_t> flat(geom_.bits() * bk_->params().trlweWords());
         detail::check(vsp_netlist_ram(h_, geom_.v, geom_.w, flat.data(), nullptr));
         return {geom_, detail::split(flat, bk_->params().trlweWords())};
+    }
+
+    // snapshotSave / snapshotLoad (snapshot.hpp:17-29): the reference's HVPS bytes,
+    // interchangeable with hvp::netlist::Evaluator<TfheBackend> snapshots.
+    void setName(const std::string& name) { detail::check(vsp_netlist_set_name(h_, name.c_str())); }
+    std::vector<uint8_t> snapshotSave() const
+    {
+        size_t n = 0;
+        detail::check(vsp_netlist_snapshot_save(h_, bk_->params().name.c_str(), nullptr, 0, &n));
+        std::vector<uint8_t> b(n);
+        detail::check(vsp_netlist_snapshot_save(h_, bk_->params().name.c_str(), b.data(), n, &n));
+        return b;
+    }
+    void snapshotLoad(const std::vector<uint8_t>& bytes)
+    {
+        detail::check(vsp_netlist_snapshot_load(h_, bk_->params().name.c_str(), bytes.data(),
+                                                bytes.size()));
+        uint32_t v = 0, w = 0;
+        if (vsp_netlist_ram_geometry(h_, &v, &w) == VSP_OK)
+            geom_ = {v, w};
     }
 
     // Evaluator::run (engine.hpp:238-247).

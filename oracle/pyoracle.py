@@ -69,6 +69,9 @@ def _lib(kind: str) -> ctypes.CDLL:
             L.ref_eval_dff_count.restype = sz
             L.ref_eval_dff_count.argtypes = [vp]
             L.ref_hardware_threads.restype = ctypes.c_uint
+            L.ref_eval_snapshot_save.argtypes = [vp, vp, sz, ctypes.POINTER(sz)]
+            L.ref_eval_snapshot_load.restype = vp
+            L.ref_eval_snapshot_load.argtypes = [vp, ctypes.c_char_p, vp, sz, ctypes.c_uint]
         _libs[kind] = L
     return _libs[kind]
 

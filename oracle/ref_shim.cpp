@@ -29,6 +29,7 @@
 #include "hvp/mem/mem.hpp"
 #include "hvp/netlist/engine.hpp"
 #include "hvp/netlist/netlist.hpp"
+#include "hvp/netlist/snapshot.hpp"
 #include "hvp/tfhe/counters.hpp"
 #include "hvp/tfhe/ops.hpp"
 #include "hvp/tfhe/serialize.hpp"
@@ -716,6 +717,39 @@ int ref_eval_run(void* e, uint64_t cycles, unsigned workers, uint64_t shuffle_se
                 stats_out[4 * i + 3] = st[i].wallSeconds * 1e6;
             }
     });
+}
+
+// snapshotSave / snapshotLoad (snapshot.cpp:84-158) of the reference evaluator.
+int ref_eval_snapshot_save(void* e, uint8_t* out, size_t cap, size_t* len)
+{
+    auto* r = static_cast<RefEval*>(e);
+    return guard([&] {
+        const std::vector<uint8_t> b = netlist::snapshotSave(*r->ev);
+        *len = b.size();
+        if (out) {
+            if (cap < b.size())
+                throw std::invalid_argument("buffer too small");
+            std::memcpy(out, b.data(), b.size());
+        }
+    });
+}
+
+void* ref_eval_snapshot_load(void* h, const char* json, const uint8_t* in, size_t len,
+                             unsigned threads)
+{
+    auto* c = static_cast<RefCtx*>(h);
+    RefEval* out = nullptr;
+    int rc = guard([&] {
+        netlist::Netlist nl = netlist::parseNetlist(json);
+        netlist::TfheBackend be;
+        be.bk = &c->bk.value();
+        be.threads = threads;
+        auto e = std::make_unique<RefEval>();
+        e->ev = std::make_unique<netlist::Evaluator<netlist::TfheBackend>>(
+            netlist::snapshotLoad(nl, be, std::vector<uint8_t>(in, in + len)));
+        out = e.release();
+    });
+    return rc == 0 ? out : nullptr;
 }
 
 // DAG analysis (buildDag, netlist.cpp:348-432): levels per DAG node, in

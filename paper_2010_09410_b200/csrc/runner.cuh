@@ -53,6 +53,7 @@ __global__ void scatter_tlwe_kernel(const int* __restrict__ nets, int count,
 
 struct vsp_netlist {
     vsp_ctx* ctx = nullptr;
+    std::string name;  // Netlist::name (snapshots record it with netlistHash)
     int nets = 0;
     std::vector<int> kind, id, in_off, in_nets, out_off, out_nets;
     // DAG (buildDag, netlist.cpp:348-432)

@@ -845,6 +845,7 @@ void rom_read_dev(vsp_ctx* c, const uint32_t* d_luts, int nluts, uint32_t depth_
 
 #include "multi.cuh"
 #include "runner.cuh"
+#include "snapshot.cuh"
 
 // DFMA throughput probe: 16 independent FMA chains per thread.
 __global__ void fp64_probe_kernel(double* out, int iters, double m)
@@ -1593,6 +1594,75 @@ int vsp_netlist_run(vsp_netlist* nl, uint64_t cycles, double* stats)
 }
 
 uint64_t vsp_netlist_cycle(vsp_netlist* nl) { return nl->cycle; }
+
+int vsp_netlist_ram_geometry(vsp_netlist* nl, uint32_t* v, uint32_t* w)
+{
+    return guard([&] {
+        if (!nl->has_ram)
+            throw std::runtime_error("RAM image not bound");
+        *v = nl->ram_v;
+        *w = nl->ram_w;
+    });
+}
+
+int vsp_netlist_set_name(vsp_netlist* nl, const char* name)
+{
+    return guard([&] { nl->name = name ? name : ""; });
+}
+
+int vsp_netlist_snapshot_save(vsp_netlist* nl, const char* param_name, uint8_t* out,
+                              size_t cap, size_t* len)
+{
+    return guard([&] {
+        vsp_ctx* c = nl->ctx;
+        std::lock_guard<std::mutex> lk(c->mu);
+        c->set_device();
+        VSP_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+        const std::vector<uint8_t> b = snapshot_save(nl, param_name ? param_name : "");
+        *len = b.size();
+        if (out) {
+            if (cap < b.size())
+                throw std::invalid_argument("snapshot: output buffer too small");
+            std::memcpy(out, b.data(), b.size());
+        }
+    });
+}
+
+int vsp_netlist_snapshot_load(vsp_netlist* nl, const char* param_name, const uint8_t* in,
+                              size_t len)
+{
+    return guard([&] {
+        vsp_ctx* c = nl->ctx;
+        std::lock_guard<std::mutex> lk(c->mu);
+        c->set_device();
+        VSP_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+        snapshot_load(nl, param_name ? param_name : "", in, len);
+    });
+}
+
+int vsp_snapshot_peek(const uint8_t* in, size_t len, char* backend, char* param, char* netlist,
+                      size_t cap)
+{
+    return guard([&] {
+        SnapReader r{in, in + len};
+        r.need(4);
+        if (std::memcmp(r.p, kSnapMagic, 4) != 0)
+            throw std::runtime_error("bad snapshot magic (expected HVPS)");
+        r.p += 4;
+        const uint16_t version = r.u16();
+        if (version != kSnapVersion)
+            throw std::runtime_error("unsupported snapshot version " + std::to_string(version));
+        const std::string b = r.u8() == 0 ? "plain" : "tfhe";
+        const std::string pn = r.str(), nn = r.str();
+        for (auto [dst, src] : {std::pair<char*, const std::string*>{backend, &b},
+                                {param, &pn}, {netlist, &nn}})
+            if (dst) {
+                if (src->size() + 1 > cap)
+                    throw std::invalid_argument("snapshot_peek: buffer too small");
+                std::memcpy(dst, src->c_str(), src->size() + 1);
+            }
+    });
+}
 
 int vsp_netlist_set_cycle(vsp_netlist* nl, uint64_t cycle)
 {

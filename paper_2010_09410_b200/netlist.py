@@ -286,6 +286,12 @@ def _bind():
     L.vsp_netlist_cycle.argtypes = [vp]
     L.vsp_netlist_cycle.restype = u64
     L.vsp_netlist_set_cycle.argtypes = [vp, u64]
+    L.vsp_netlist_set_name.argtypes = [vp, ctypes.c_char_p]
+    L.vsp_netlist_ram_geometry.argtypes = [vp, ctypes.POINTER(u32), ctypes.POINTER(u32)]
+    L.vsp_netlist_snapshot_save.argtypes = [vp, ctypes.c_char_p, vp, ctypes.c_size_t,
+                                            ctypes.POINTER(ctypes.c_size_t)]
+    L.vsp_netlist_snapshot_load.argtypes = [vp, ctypes.c_char_p, vp, ctypes.c_size_t]
+    L.vsp_snapshot_peek.argtypes = [vp, ctypes.c_size_t, vp, vp, vp, ctypes.c_size_t]
     L._nl_bound = True
     return L
 
@@ -321,6 +327,7 @@ class Evaluator:
             from . import _raise
             _raise(3, L.vsp_last_error())
         self.h = ctypes.c_void_p(h)
+        _check(L.vsp_netlist_set_name(self.h, nl.name.encode()))
         info = np.zeros(6, np.int32)
         _check(L.vsp_netlist_info(self.h, _ptr(info), None))
         self.dag_nodes, self.n_dffs, self.gmax, self.depth, self.rom_cell, self.ram_cell = \
@@ -420,6 +427,26 @@ class Evaluator:
         _check(lib().vsp_netlist_ram(self.h, v, w, _ptr(out), None))
         return out
 
+    def snapshot_save(self, param_name: str | None = None) -> bytes:
+        """snapshotSave (snapshot.cpp:84-101): the reference's HVPS bytes."""
+        L = lib()
+        name = (param_name or self.engine.params.name).encode()
+        n = ctypes.c_size_t()
+        _check(L.vsp_netlist_snapshot_save(self.h, name, None, 0, ctypes.byref(n)))
+        buf = np.zeros(n.value, np.uint8)
+        _check(L.vsp_netlist_snapshot_save(self.h, name, _ptr(buf), buf.size, ctypes.byref(n)))
+        return buf.tobytes()
+
+    def snapshot_load(self, data: bytes, param_name: str | None = None):
+        """snapshotLoad (snapshot.cpp:124-158) into this runner: cycle, DFFs, RAM, ROM."""
+        buf = np.frombuffer(bytes(data), np.uint8).copy()
+        name = (param_name or self.engine.params.name).encode()
+        _check(lib().vsp_netlist_snapshot_load(self.h, name, _ptr(buf), buf.size))
+        if self.ram_cell >= 0:
+            v, w = ctypes.c_uint32(), ctypes.c_uint32()
+            if lib().vsp_netlist_ram_geometry(self.h, ctypes.byref(v), ctypes.byref(w)) == 0:
+                self._ram_geom = (int(v.value), int(w.value))
+
     def run(self, cycles: int, opt: RunOptions | None = None):
         """Evaluator::run (engine.hpp:238-247)."""
         opt = opt or RunOptions()
@@ -429,6 +456,16 @@ class Evaluator:
             for i in range(cycles):
                 opt.stats.append(CycleStats(int(st[4 * i]), int(st[4 * i + 1]),
                                             int(st[4 * i + 2]), float(st[4 * i + 3])))
+
+
+def snapshot_peek(data: bytes) -> dict:
+    """snapshotPeek (snapshot.cpp:165-176): backend tag, parameter set, netlist name."""
+    L = _bind()
+    buf = np.frombuffer(bytes(data), np.uint8).copy()
+    outs = [ctypes.create_string_buffer(256) for _ in range(3)]
+    _check(L.vsp_snapshot_peek(_ptr(buf), buf.size, *[ctypes.addressof(o) for o in outs], 256))
+    return {"backend": outs[0].value.decode(), "param": outs[1].value.decode(),
+            "netlist": outs[2].value.decode()}
 
 
 class PlainEvaluator:

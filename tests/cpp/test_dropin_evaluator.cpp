@@ -17,6 +17,7 @@
 #include "hvp/mem/mem.hpp"
 #include "hvp/netlist/engine.hpp"
 #include "hvp/netlist/netlist.hpp"
+#include "hvp/netlist/snapshot.hpp"
 #include "hvp/tfhe/ops.hpp"
 #include "vsp_b200.hpp"
 
@@ -169,6 +170,12 @@ int main()
                 CHECK(flat(rs[i]) == us[i]);
             }
         }
+        // HVPS snapshots are interchangeable: the runner's bytes == the reference's
+        const std::vector<uint8_t> refSnap = netlist::snapshotSave(ref);
+        CHECK(runner.snapshotSave() == refSnap);
+        auto resumed = vsp::netlist::Runner::fromNetlist(gpuBk, nl);
+        resumed.snapshotLoad(refSnap);
+        CHECK(resumed.cycle() == 4 && resumed.dffState() == runner.dffState());
         const auto& rc = ref.ram().enc.cells;
         const auto& gc = gpu.ram().enc.cells;
         const auto uc = runner.ram().cells;
