@@ -67,6 +67,17 @@ int vsp_upload_keys(vsp_ctx* ctx, const uint32_t* bk1, const uint32_t* ksk,
                     const uint64_t* bk2, const uint32_t* pks_negs, const uint32_t* pks_id,
                     int has_cb);
 
+/* deserializeBootstrappingKey (serialize.cpp:209-230) + upload: the reference's "HVP1"
+ * key file (tag 2) as produced by serializeBootstrappingKey, checked against the
+ * context's parameters (VSP_ERUNTIME with the reference's messages on mismatch). */
+int vsp_upload_keys_hvp1(vsp_ctx* ctx, const uint8_t* bytes, size_t len);
+
+/* HVP1 ciphertext containers (serialize.cpp:240-245, mem.cpp:340-403): TLWE (tag 3),
+ * TRLWE (4), RAM (6), ROM (7) flattened to the layouts above.  out == NULL returns the
+ * size in *words; meta = {tag, count, v, w, depthBytes}. */
+int vsp_read_hvp1(vsp_ctx* ctx, const uint8_t* bytes, size_t len, uint32_t* out, size_t cap,
+                  size_t* words, uint32_t meta[5]);
+
 /* homGate (ops.cpp:839-896) over a batch of independent gates, host buffers.
  * kinds[G]; in[G x 3 x (n+1)] (unused operand slots ignored; MUX = {sel, a, b});
  * out[G x (n+1)].  Equivalent to G calls of homGate. */

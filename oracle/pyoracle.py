@@ -70,6 +70,10 @@ def _lib(kind: str) -> ctypes.CDLL:
             L.ref_eval_dff_count.argtypes = [vp]
             L.ref_hardware_threads.restype = ctypes.c_uint
             L.ref_eval_snapshot_save.argtypes = [vp, vp, sz, ctypes.POINTER(sz)]
+            L.ref_serialize_bk.argtypes = [vp, vp, sz, ctypes.POINTER(sz)]
+            L.ref_serialize_tlwe.argtypes = [vp, vp, vp, sz, ctypes.POINTER(sz)]
+            L.ref_serialize_ram.argtypes = [vp, u32, u32, vp, vp, sz, ctypes.POINTER(sz)]
+            L.ref_serialize_rom.argtypes = [vp, u32, vp, u32, vp, sz, ctypes.POINTER(sz)]
             L.ref_eval_snapshot_load.restype = vp
             L.ref_eval_snapshot_load.argtypes = [vp, ctypes.c_char_p, vp, sz, ctypes.c_uint]
         _libs[kind] = L
@@ -330,3 +334,18 @@ class CpuTfhe:
 
     def counters_reset(self):
         self._f("counters_reset")()
+
+
+def ref_bytes(fn, *args) -> bytes:
+    """Call a two-pass ref_serialize_* / snapshot function of the reference shim."""
+    L = _lib("ref")
+    n = ctypes.c_size_t()
+    rc = getattr(L, fn)(*args, None, 0, ctypes.byref(n))
+    if rc:
+        raise RuntimeError(L.ref_last_error().decode())
+    buf = np.zeros(n.value, np.uint8)
+    rc = getattr(L, fn)(*args, buf.ctypes.data_as(ctypes.c_void_p), buf.size, ctypes.byref(n))
+    if rc:
+        raise RuntimeError(L.ref_last_error().decode())
+    return buf.tobytes()
+

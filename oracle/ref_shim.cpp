@@ -719,6 +719,58 @@ int ref_eval_run(void* e, uint64_t cycles, unsigned workers, uint64_t shuffle_se
     });
 }
 
+// HVP1 containers written by the reference (serialize.cpp:190-245, mem.cpp:354-396).
+static int put_bytes(const std::vector<uint8_t>& b, uint8_t* out, size_t cap, size_t* len)
+{
+    *len = b.size();
+    if (out) {
+        if (cap < b.size())
+            throw std::invalid_argument("buffer too small");
+        std::memcpy(out, b.data(), b.size());
+    }
+    return 0;
+}
+
+int ref_serialize_bk(void* h, uint8_t* out, size_t cap, size_t* len)
+{
+    auto* c = static_cast<RefCtx*>(h);
+    return guard([&] { put_bytes(serializeBootstrappingKey(c->bk.value()), out, cap, len); });
+}
+
+int ref_serialize_tlwe(void* h, const uint32_t* ct, uint8_t* out, size_t cap, size_t* len)
+{
+    auto* c = static_cast<RefCtx*>(h);
+    return guard([&] {
+        put_bytes(serializeTlwe(toTlwe(ct, c->params.n, 0), c->params), out, cap, len);
+    });
+}
+
+int ref_serialize_ram(void* h, uint32_t v, uint32_t w, const uint32_t* ram, uint8_t* out,
+                      size_t cap, size_t* len)
+{
+    auto* c = static_cast<RefCtx*>(h);
+    return guard([&] {
+        mem::EncryptedRam r;
+        r.geom = {v, w};
+        for (size_t i = 0; i < r.geom.bits(); i++)
+            r.cells.push_back(toTrlwe(ram + i * 2 * c->params.N1, c->params.N1));
+        put_bytes(mem::serializeRam(r, c->params), out, cap, len);
+    });
+}
+
+int ref_serialize_rom(void* h, uint32_t depth, const uint32_t* luts, uint32_t nluts, uint8_t* out,
+                      size_t cap, size_t* len)
+{
+    auto* c = static_cast<RefCtx*>(h);
+    return guard([&] {
+        mem::EncryptedRom r;
+        r.depthBytes = depth;
+        for (uint32_t t = 0; t < nluts; t++)
+            r.luts.push_back(toTrlwe(luts + size_t{t} * 2 * c->params.N1, c->params.N1));
+        put_bytes(mem::serializeRom(r, c->params), out, cap, len);
+    });
+}
+
 // snapshotSave / snapshotLoad (snapshot.cpp:84-158) of the reference evaluator.
 int ref_eval_snapshot_save(void* e, uint8_t* out, size_t cap, size_t* len)
 {

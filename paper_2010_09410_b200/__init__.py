@@ -80,6 +80,8 @@ def lib() -> ctypes.CDLL:
                                           ctypes.POINTER(sz), ctypes.POINTER(sz),
                                           ctypes.POINTER(sz)]
         L.vsp_hom_gate_level_dev.argtypes = [vp, vp, vp, vp, sz, vp]
+        L.vsp_upload_keys_hvp1.argtypes = [vp, vp, sz]
+        L.vsp_read_hvp1.argtypes = [vp, vp, sz, vp, sz, ctypes.POINTER(sz), vp]
         _lib = L
     return _lib
 
@@ -283,6 +285,27 @@ class Engine:
                                      _ptr(kk.get("bk2")), _ptr(kk.get("pks_negs")),
                                      _ptr(kk.get("pks_id")), int(has_cb)))
         self._keys = None
+
+    def upload_keys_hvp1(self, data: bytes):
+        """deserializeBootstrappingKey (serialize.cpp:209-230): load the reference's HVP1
+        key file straight into the device."""
+        buf = np.frombuffer(bytes(data), np.uint8).copy()
+        _check(lib().vsp_upload_keys_hvp1(self.h, _ptr(buf), buf.size))
+
+    def read_hvp1(self, data: bytes):
+        """HVP1 TLWE / TRLWE / RAM / ROM container -> (meta, flat array) in engine layout:
+        TLWE (n+1,), TRLWE (2N,), RAM (w*2^v, 2N) with meta v, w, ROM (luts, 2N)."""
+        buf = np.frombuffer(bytes(data), np.uint8).copy()
+        meta = np.zeros(5, np.uint32)
+        words = ctypes.c_size_t()
+        _check(lib().vsp_read_hvp1(self.h, _ptr(buf), buf.size, None, 0, ctypes.byref(words),
+                                   _ptr(meta)))
+        out = np.zeros(words.value, np.uint32)
+        _check(lib().vsp_read_hvp1(self.h, _ptr(buf), buf.size, _ptr(out), out.size,
+                                   ctypes.byref(words), _ptr(meta)))
+        tag, count, v, w, depth = (int(x) for x in meta)
+        m = {"tag": tag, "count": count, "v": v, "w": w, "depth_bytes": depth}
+        return m, (out.reshape(count, -1) if tag in (6, 7) else out)
 
     @staticmethod
     def _kind_ids(kinds) -> np.ndarray:

@@ -846,6 +846,7 @@ void rom_read_dev(vsp_ctx* c, const uint32_t* d_luts, int nluts, uint32_t depth_
 #include "multi.cuh"
 #include "runner.cuh"
 #include "snapshot.cuh"
+#include "hvp1.cuh"
 
 // DFMA throughput probe: 16 independent FMA chains per thread.
 __global__ void fp64_probe_kernel(double* out, int iters, double m)
@@ -1594,6 +1595,31 @@ int vsp_netlist_run(vsp_netlist* nl, uint64_t cycles, double* stats)
 }
 
 uint64_t vsp_netlist_cycle(vsp_netlist* nl) { return nl->cycle; }
+
+int vsp_upload_keys_hvp1(vsp_ctx* c, const uint8_t* bytes, size_t len)
+{
+    Hvp1Keys k;
+    const int rc = guard([&] { k = hvp1_keys(c->p, bytes, len); });
+    if (rc != VSP_OK)
+        return rc;
+    return vsp_upload_keys(c, k.bk1.data(), k.ksk.data(), k.bk2.empty() ? nullptr : k.bk2.data(),
+                           k.pks_negs.empty() ? nullptr : k.pks_negs.data(),
+                           k.pks_id.empty() ? nullptr : k.pks_id.data(), k.has_cb);
+}
+
+int vsp_read_hvp1(vsp_ctx* c, const uint8_t* bytes, size_t len, uint32_t* out, size_t cap,
+                  size_t* words, uint32_t meta[5])
+{
+    return guard([&] {
+        const std::vector<uint32_t> v = hvp1_ciphertexts(c->p, bytes, len, meta);
+        *words = v.size();
+        if (out) {
+            if (cap < v.size())
+                throw std::invalid_argument("read_hvp1: output buffer too small");
+            std::memcpy(out, v.data(), v.size() * 4);
+        }
+    });
+}
 
 int vsp_netlist_ram_geometry(vsp_netlist* nl, uint32_t* v, uint32_t* w)
 {
