@@ -437,6 +437,36 @@ def run_memory(args, world, rank, local):
         "cpu_baseline": cpu}), flush=True)
 
 
+def _cycle_cpu_baseline(p, keys, nl, ram, v, w, luts, dff0, ins):
+    """One cycle of the reference's own Evaluator<TfheBackend> (oracle/_ref, patched
+    engine.hpp) on the same netlist, keys and state, on all host cores."""
+    import ctypes
+    from oracle.pyoracle import CpuTfhe, available
+    from paper_2010_09410_b200 import netlist as N
+    if not available("ref"):
+        return None
+    th = os.cpu_count() or 1
+    r = CpuTfhe("ref", "tfhe-80", n_override=p.n, seed=1)
+    r.import_keys(keys)
+    L = r.L
+    h = ctypes.c_void_p(L.ref_eval_new(r.h, N.netlist_to_json(nl).encode(), th))
+    vp = ctypes.c_void_p
+    L.ref_eval_set_ram(h, v, w, ram.ctypes.data_as(vp), p.N1)
+    L.ref_eval_set_rom(h, 512, luts.ctypes.data_as(vp), luts.shape[0], p.N1)
+    L.ref_eval_set_dff(h, np.ascontiguousarray(dff0).ctypes.data_as(vp), ctypes.c_uint32(p.n))
+    for i, ct in enumerate(ins):
+        L.ref_eval_set_input(h, b"in", i, np.ascontiguousarray(ct).ctypes.data, p.n)
+    t0 = time.perf_counter()
+    rc = L.ref_eval_run(h, 1, th, 0, None)
+    dt = time.perf_counter() - t0
+    L.ref_eval_free(h)
+    if rc:
+        return None
+    return {"value": round(dt, 3), "unit": "s/cycle", "cores": th, "kind": "reference",
+            "sample": f"one cycle of hvp::netlist::Evaluator<TfheBackend> (reference, "
+                      f"{th} workers) on the same netlist, keys and state"}
+
+
 def run_cycle(args, world, rank, local):
     """BASELINE configs[2]: seconds per clock cycle of a seeded synthetic Ruby-shaped
     pipelined-processor netlist (gate mix of PAPER.md:1376-1385, one ROM + one RAM port)."""
@@ -457,12 +487,16 @@ def run_cycle(args, world, rank, local):
     nl = N.synthetic_netlist(seed=1, levels=args.levels)
     ev = N.Evaluator(nl, eng)
     v, w = 8, 16
-    ev.set_ram(vsp.encrypt_ram(p, keys, rng.integers(0, 256, (w << v) // 8).astype(np.uint8), v,
-                               w, 3), v, w)
-    ev.set_rom(vsp.encrypt_rom(p, keys, rng.integers(0, 256, 512).astype(np.uint8), 4), 512)
-    ev.set_dff_state_raw(vsp.encrypt(p, keys["lv0"], rng.integers(0, 2, ev.n_dffs), 5))
-    for i in range(len(nl.inputs[0].bits)):
-        ev.set_input("in", i, vsp.encrypt(p, keys["lv0"], [int(rng.integers(0, 2))], 6 + i)[0])
+    ram = vsp.encrypt_ram(p, keys, rng.integers(0, 256, (w << v) // 8).astype(np.uint8), v, w, 3)
+    luts = vsp.encrypt_rom(p, keys, rng.integers(0, 256, 512).astype(np.uint8), 4)
+    dff0 = vsp.encrypt(p, keys["lv0"], rng.integers(0, 2, ev.n_dffs), 5)
+    ins = [vsp.encrypt(p, keys["lv0"], [int(rng.integers(0, 2))], 6 + i)[0]
+           for i in range(len(nl.inputs[0].bits))]
+    ev.set_ram(ram, v, w)
+    ev.set_rom(luts, 512)
+    ev.set_dff_state_raw(dff0)
+    for i, ct in enumerate(ins):
+        ev.set_input("in", i, ct)
     stats = []
     ev.run(args.warmup)
     eng.counters_reset()
@@ -482,6 +516,9 @@ def run_cycle(args, world, rank, local):
             dist.destroy_process_group()
         return
     st = N.netlist_stats(nl)
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        cpu = _cycle_cpu_baseline(p, keys, nl, ram, v, w, luts, dff0, ins)
     print(json.dumps({
         "metric": "seconds_per_clock_cycle", "value": round(float(np.mean(secs)), 5),
         "unit": "s/cycle", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -492,7 +529,7 @@ def run_cycle(args, world, rank, local):
                    "dffs": st["dff_count"], "depth": st["depth"], "gmax": st["gmax"],
                    "rom": "512 B, 7 addr bits", "ram": "v=8 w=16", "n": p.n},
         "counters_per_cycle": {k: v // max(args.steps, 1) for k, v in eng.counters().items()},
-        "kernel_ms_per_cycle": kernels,
+        "kernel_ms_per_cycle": kernels, "cpu_baseline": cpu,
         "timing": "CUDA events around each device-resident cycle (max over ranks)"}), flush=True)
     if dist:
         dist.destroy_process_group()
