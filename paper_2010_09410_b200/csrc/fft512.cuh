@@ -58,7 +58,12 @@ constexpr int kFftXbufStride = 544;  // 512 + 32 swizzle pad (double2 units)
 // k = br(jt) << (7-d) = 4q + m: only the q = 0 values are stored (1, 1, 2, 4 for
 // stages 4-7 and 4 for stage 8); multiplying by i is a swap/negate folded into the
 // butterfly.  12 loads per transform instead of 23 (the kernels are shared-memory bound).
-constexpr int kTw2Entries = 12;
+// Entries [0, kTw2Plain) hold zeta (inverse butterflies); entries [kTw2Plain, 2 kTw2Plain)
+// hold the same twiddles in tangent form (kappa, tau), zeta = kappa (1 + i tau), for the
+// forward butterflies (6 FMAs).  tau may be large where zeta is near +-i; the products
+// kappa * tau v stay within the same rounding bound, and zeta is never exactly +-i here.
+constexpr int kTw2Plain = 12;
+constexpr int kTw2Entries = 2 * kTw2Plain;
 
 __host__ __device__ constexpr int tw_k(int d, int jt) { return bitrev_const(jt, d - 4) << (7 - d); }
 __host__ __device__ constexpr int tw_entry(int d, int m)
@@ -94,6 +99,27 @@ __device__ __forceinline__ void bf_fwd_q(double2& u, double2& v, const double2 w
         bf_fwd_i(u, v, w);
     else
         bf_fwd(u, v, w);
+}
+
+// Forward butterfly with a per-lane tangent-form twiddle kt = (kappa, tau) of zeta, times
+// i^Q: t = (1 + i tau) v (Q = 0) or (i - tau) v (Q = 1); v' = u - kappa t, u' = u + kappa t.
+template <int Q>
+__device__ __forceinline__ void bf_fwd_tq(double2& u, double2& v, const double2 kt)
+{
+    const double k = kt.x, t = kt.y;
+    double tx, ty;
+    if (Q) {
+        tx = fma(-t, v.x, -v.y);
+        ty = fma(-t, v.y, v.x);
+    }
+    else {
+        tx = fma(-t, v.y, v.x);
+        ty = fma(t, v.x, v.y);
+    }
+    v.x = fma(-k, tx, u.x);
+    v.y = fma(-k, ty, u.y);
+    u.x = fma(k, tx, u.x);
+    u.y = fma(k, ty, u.y);
 }
 
 // Forward butterfly with a tangent-form twiddle: 6 FMAs instead of 2 MUL + 2 FMA + 4 ADD.
@@ -238,12 +264,13 @@ __device__ __forceinline__ void xpose_inv(double2 (&v)[16], void* buf, int lane)
 }
 
 // Forward transform in place.  xbuf: per-warp smem, kFftXbufStride double2 (HALF:
-// kFftXbufStride doubles).  tw2: smem table [kTw2Entries][32] double2.
+// kFftXbufStride doubles).  tw2: smem table [kTw2Entries][32] double2 (plain, then tangent).
 template <int ROOT = 0, bool HALF = false>
 __device__ __forceinline__ void fft512_fwd(double2 (&v)[16], void* xbuf,
                                            const double2* tw2, int lane)
 {
     const double2* tw1t = &c_tw1t[ROOT][0] + opaque_zero();
+    const double2* tw2t = tw2 + kTw2Plain * 32;
 #pragma unroll
     for (int d = 0; d < 4; d++) {
         const int h = 8 >> d;
@@ -266,11 +293,11 @@ __device__ __forceinline__ void fft512_fwd(double2 (&v)[16], void* xbuf,
         for (int j = 0; j < 16; j++)
             if ((j & h) == 0) {
                 const int k = tw_k(d, j >> (8 - d));
-                const double2 w = tw2[tw_entry(d, k & 3) * 32 + lane];
+                const double2 w = tw2t[tw_entry(d, k & 3) * 32 + lane];
                 if (k >> 2)
-                    bf_fwd_q<1>(v[j], v[j + h], w);
+                    bf_fwd_tq<1>(v[j], v[j + h], w);
                 else
-                    bf_fwd_q<0>(v[j], v[j + h], w);
+                    bf_fwd_tq<0>(v[j], v[j + h], w);
             }
     }
     const bool odd = lane & 1;
@@ -281,11 +308,11 @@ __device__ __forceinline__ void fft512_fwd(double2 (&v)[16], void* xbuf,
         double2 u = odd ? recv : v[k];
         double2 w = odd ? v[k + 8] : recv;
         const int br = bitrev_const(k, 3);
-        const double2 t = tw2[tw_entry(8, br & 3) * 32 + lane];
+        const double2 t = tw2t[tw_entry(8, br & 3) * 32 + lane];
         if (br >> 2)
-            bf_fwd_q<1>(u, w, t);
+            bf_fwd_tq<1>(u, w, t);
         else
-            bf_fwd_q<0>(u, w, t);
+            bf_fwd_tq<0>(u, w, t);
         v[k] = u;
         v[k + 8] = w;
     }

@@ -126,7 +126,12 @@ void twiddles(int root, double2* tw1, double2* tw1t, std::vector<double2>& tw2)
     // compressed per-lane table (fft512.cuh, kTw2Entries): store the q = 0 twiddles and
     // check that every q = 1 twiddle is i times a stored one
     tw2.assign(kTw2Entries * 32, make_double2(0, 0));
-    auto put = [&](int e, int L, double2 z) { tw2[e * 32 + L] = z; };
+    auto put = [&](int e, int L, double2 z) {
+        tw2[e * 32 + L] = z;
+        // tangent form (kappa, tau) = (cos, tan) of the same angle (fft512.cuh bf_fwd_tq)
+        const long double a = atan2l((long double)z.y, (long double)z.x);
+        tw2[(kTw2Plain + e) * 32 + L] = make_double2((double)cosl(a), (double)tanl(a));
+    };
     auto check_i = [&](int e, int L, double2 z) {
         const double2 w = tw2[e * 32 + L];  // z must equal i * w
         if (fabs(z.x + w.y) > 1e-15 || fabs(z.y - w.x) > 1e-15)
