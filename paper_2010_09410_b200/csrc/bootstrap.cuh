@@ -8,6 +8,13 @@
 
 #include "fft512.cuh"
 
+#ifndef VSP_BR_INV2
+#define VSP_BR_INV2 1
+#endif
+#ifndef VSP_BR_FWD2
+#define VSP_BR_FWD2 0  // measured slower (spills at 255 regs): 32.8 vs 30.2 ms
+#endif
+
 namespace vsp {
 
 // Gate kinds in hvp::tfhe::GateKind order (ops.hpp:183-194).
@@ -131,47 +138,103 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
 
     double2 accA[16], accB[16];
 
+    // Slot release: the last warp to finish with chunk c refills its slot with c + S.
+    auto release = [&](int c) {
+        __syncwarp();
+        if (lane == 0) {
+            const int s = c % S;
+            const uint32_t old = atomicAdd(&sm.cnt[s], 1u);
+            if (old == WARPS - 1) {
+                sm.cnt[s] = 0;
+                const int cn = c + S;
+                if (cn < nchunks) {
+                    fence_proxy_async();
+                    mbar_arrive_expect_tx(&sm.full[s], 16384);
+                    bulk_g2s(sm.ring[s], bkfd + (size_t)cn * 1024, 16384, &sm.full[s]);
+                }
+            }
+        }
+    };
+    // diff = (X^bara - 1) * acc_P (polyMulByXkMinusOne, poly.hpp:51-57) computed once;
+    // both digit levels (decomposePoly, poly.hpp:79-97) are parked in smem as packed
+    // int16 pairs (coefficients p, p+512) so no transform registers are live.
+    // lane + 32 j is recomputed from an opaque base every step so the compiler does not
+    // hoist 32 loop-invariant indices into (spilled) registers.
+    auto digits = [&](int P, uint32_t bara) {
+        const uint32_t* src = acc + P * 1024;
+        const uint32_t lo = (uint32_t)lane + (uint32_t)opaque_zero();
+        const uint32_t lk = lo - bara;
+        const uint32_t* srcl = src + lo;
+#pragma unroll
+        for (int j = 0; j < 16; j++) {
+            const uint32_t v0 = rot_coef1024(src, lk + 32 * j) - srcl[32 * j] + kOffset;
+            const uint32_t v1 = rot_coef1024(src, lk + 32 * j + 512) - srcl[32 * j + 512] + kOffset;
+            const uint32_t d0 = (v0 >> (32 - BG)) - kHalf;
+            const uint32_t d1 = (v1 >> (32 - BG)) - kHalf;
+            const uint32_t e0 = ((v0 >> (32 - 2 * BG)) & kMask) - kHalf;
+            const uint32_t e1 = ((v1 >> (32 - 2 * BG)) & kMask) - kHalf;
+            sm.dig[warp][0][j * 32 + lane] = (d0 & 0xffffu) | (d1 << 16);
+            sm.dig[warp][1][j * 32 + lane] = (e0 & 0xffffu) | (e1 << 16);
+        }
+    };
+    auto load_digits = [&](double2 (&z)[16], int lvl) {
+#pragma unroll
+        for (int j = 0; j < 16; j++) {
+            const uint32_t w = sm.dig[warp][lvl][j * 32 + lane];
+            z[j].x = (double)(int16_t)(w & 0xffffu);
+            z[j].y = (double)(int16_t)(w >> 16);
+        }
+    };
+
 #pragma unroll 1
     for (int i = 0; i < n; i++) {
         const uint32_t bara = mod_switch_2n(lwe[i], 11);
+        const int c0 = i * 4;
+#if VSP_BR_FWD2
+        // rows 0, 1 (polynomial a, both digit levels): two transforms at once, while the
+        // MAC accumulators are not yet live; their products initialise accA / accB.
+        digits(0, bara);
+        {
+            double2 z0[16], z1[16];
+            load_digits(z0, 0);
+            load_digits(z1, 1);
+            fft512_fwd2(z0, z1, xbuf, sm.tw2, lane);
+            mbar_wait(&sm.full[c0 % S], (uint32_t)((c0 / S) & 1));
+            mbar_wait(&sm.full[(c0 + 1) % S], (uint32_t)(((c0 + 1) / S) & 1));
+            const double2* bk0 = sm.ring[c0 % S];
+            const double2* bk1 = sm.ring[(c0 + 1) % S];
+#pragma unroll
+            for (int j = 0; j < 16; j++) {
+                const double2 ba = bk0[j * 32 + lane];
+                const double2 bb = bk0[512 + j * 32 + lane];
+                const double2 ca = bk1[j * 32 + lane];
+                const double2 cb = bk1[512 + j * 32 + lane];
+                accA[j].x = fma(z1[j].x, ca.x, fma(-z1[j].y, ca.y, fma(z0[j].x, ba.x, -z0[j].y * ba.y)));
+                accA[j].y = fma(z1[j].x, ca.y, fma(z1[j].y, ca.x, fma(z0[j].x, ba.y, z0[j].y * ba.x)));
+                accB[j].x = fma(z1[j].x, cb.x, fma(-z1[j].y, cb.y, fma(z0[j].x, bb.x, -z0[j].y * bb.y)));
+                accB[j].y = fma(z1[j].x, cb.y, fma(z1[j].y, cb.x, fma(z0[j].x, bb.y, z0[j].y * bb.x)));
+            }
+        }
+        release(c0);
+        release(c0 + 1);
+        constexpr int P0 = 1;
+#else
 #pragma unroll
         for (int j = 0; j < 16; j++) {
             accA[j] = make_double2(0.0, 0.0);
             accB[j] = make_double2(0.0, 0.0);
         }
+        constexpr int P0 = 0;
+#endif
 #pragma unroll 1
-        for (int P = 0; P < 2; P++) {
-            const uint32_t* src = acc + P * 1024;
-            // diff = (X^bara - 1) * acc (polyMulByXkMinusOne, poly.hpp:51-57) computed once;
-            // both digit levels (decomposePoly, poly.hpp:79-97) are parked in smem as
-            // packed int16 pairs (coefficients p, p+512) so no transform registers are live.
-            // lane + 32 j is recomputed from an opaque base every step so the compiler does
-            // not hoist 32 loop-invariant indices into (spilled) registers.
-            const uint32_t lo = (uint32_t)lane + (uint32_t)opaque_zero();
-            const uint32_t lk = lo - bara;
-            const uint32_t* srcl = src + lo;
-#pragma unroll
-            for (int j = 0; j < 16; j++) {
-                const uint32_t v0 = rot_coef1024(src, lk + 32 * j) - srcl[32 * j] + kOffset;
-                const uint32_t v1 = rot_coef1024(src, lk + 32 * j + 512) - srcl[32 * j + 512] + kOffset;
-                const uint32_t d0 = (v0 >> (32 - BG)) - kHalf;
-                const uint32_t d1 = (v1 >> (32 - BG)) - kHalf;
-                const uint32_t e0 = ((v0 >> (32 - 2 * BG)) & kMask) - kHalf;
-                const uint32_t e1 = ((v1 >> (32 - 2 * BG)) & kMask) - kHalf;
-                sm.dig[warp][0][j * 32 + lane] = (d0 & 0xffffu) | (d1 << 16);
-                sm.dig[warp][1][j * 32 + lane] = (e0 & 0xffffu) | (e1 << 16);
-            }
+        for (int P = P0; P < 2; P++) {
+            digits(P, bara);
 #pragma unroll 1
             for (int lvl = 0; lvl < 2; lvl++) {
                 double2 z[16];
-#pragma unroll
-                for (int j = 0; j < 16; j++) {
-                    const uint32_t w = sm.dig[warp][lvl][j * 32 + lane];
-                    z[j].x = (double)(int16_t)(w & 0xffffu);
-                    z[j].y = (double)(int16_t)(w >> 16);
-                }
+                load_digits(z, lvl);
                 fft512_fwd(z, xbuf, sm.tw2, lane);
-                const int c = i * 4 + P * 2 + lvl;
+                const int c = c0 + P * 2 + lvl;
                 const int s = c % S;
                 mbar_wait(&sm.full[s], (uint32_t)((c / S) & 1));
                 const double2* bk = sm.ring[s];
@@ -184,30 +247,24 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
                     accB[j].x = fma(z[j].x, bb.x, fma(-z[j].y, bb.y, accB[j].x));
                     accB[j].y = fma(z[j].x, bb.y, fma(z[j].y, bb.x, accB[j].y));
                 }
-                __syncwarp();
-                if (lane == 0) {
-                    const uint32_t old = atomicAdd(&sm.cnt[s], 1u);
-                    if (old == WARPS - 1) {
-                        sm.cnt[s] = 0;
-                        const int cn = c + S;
-                        if (cn < nchunks) {
-                            fence_proxy_async();
-                            mbar_arrive_expect_tx(&sm.full[s], 16384);
-                            bulk_g2s(sm.ring[s], bkfd + (size_t)cn * 1024, 16384, &sm.full[s]);
-                        }
-                    }
-                }
+                release(c);
             }
         }
         // inverse transforms, round (llrint, fft.hpp:47-50) and accumulate
+#if VSP_BR_INV2
+        fft512_inv2(accA, accB, xbuf, sm.tw2, lane);
+#else
         fft512_inv(accA, xbuf, sm.tw2, lane);
+#endif
 #pragma unroll
         for (int j = 0; j < 16; j++) {
             const int p = lane + 32 * j;
             acc[p] += (uint32_t)__double2ll_rn(accA[j].x);
             acc[p + 512] += (uint32_t)__double2ll_rn(accA[j].y);
         }
+#if !VSP_BR_INV2
         fft512_inv(accB, xbuf, sm.tw2, lane);
+#endif
 #pragma unroll
         for (int j = 0; j < 16; j++) {
             const int p = lane + 32 * j;

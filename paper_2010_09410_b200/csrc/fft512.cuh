@@ -364,4 +364,136 @@ __device__ __forceinline__ void fft512_inv(double2 (&v)[16], void* xbuf,
     }
 }
 
+// Two inverse transforms at once (the accumulator pair of an external product): every
+// per-lane twiddle is loaded once for both, and the two independent butterfly streams
+// give the scheduler FP64 work to overlap with the other's shuffles and transposes.
+template <int ROOT = 0>
+__device__ __forceinline__ void fft512_inv2(double2 (&va)[16], double2 (&vb)[16], void* xbuf,
+                                            const double2* tw2, int lane)
+{
+    const bool odd = lane & 1;
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        const int br = bitrev_const(k, 3);
+        const double2 t = tw2[tw_entry(8, br & 3) * 32 + lane];
+        double2 a = va[k], b = va[k + 8];
+        double2 c = vb[k], d = vb[k + 8];
+        if (br >> 2) {
+            bf_inv_q<1>(a, b, t);
+            bf_inv_q<1>(c, d, t);
+        }
+        else {
+            bf_inv_q<0>(a, b, t);
+            bf_inv_q<0>(c, d, t);
+        }
+        const double2 ra = shfl_xor_d2(odd ? a : b, 1);
+        const double2 rb = shfl_xor_d2(odd ? c : d, 1);
+        va[k] = odd ? ra : a;
+        va[k + 8] = odd ? b : ra;
+        vb[k] = odd ? rb : c;
+        vb[k + 8] = odd ? d : rb;
+    }
+#pragma unroll
+    for (int d = 7; d >= 4; d--) {
+        const int h = 8 >> (d - 4);
+#pragma unroll
+        for (int j = 0; j < 16; j++)
+            if ((j & h) == 0) {
+                const int k = tw_k(d, j >> (8 - d));
+                const double2 w = tw2[tw_entry(d, k & 3) * 32 + lane];
+                if (k >> 2) {
+                    bf_inv_q<1>(va[j], va[j + h], w);
+                    bf_inv_q<1>(vb[j], vb[j + h], w);
+                }
+                else {
+                    bf_inv_q<0>(va[j], va[j + h], w);
+                    bf_inv_q<0>(vb[j], vb[j + h], w);
+                }
+            }
+    }
+    xpose_inv<false>(va, xbuf, lane);
+    xpose_inv<false>(vb, xbuf, lane);
+    const double2* tw1 = &c_tw1[ROOT][0] + opaque_zero();
+#pragma unroll
+    for (int d = 3; d >= 0; d--) {
+        const int h = 8 >> d;
+#pragma unroll
+        for (int j = 0; j < 16; j++)
+            if ((j & h) == 0) {
+                const double2 w = tw1[(1 << d) - 1 + (j >> (4 - d))];
+                bf_inv(va[j], va[j + h], w);
+                bf_inv(vb[j], vb[j + h], w);
+            }
+    }
+}
+
+// Two forward transforms at once (shared per-lane twiddle loads, two independent streams).
+template <int ROOT = 0>
+__device__ __forceinline__ void fft512_fwd2(double2 (&va)[16], double2 (&vb)[16], void* xbuf,
+                                            const double2* tw2, int lane)
+{
+    const double2* tw1t = &c_tw1t[ROOT][0] + opaque_zero();
+    const double2* tw2t = tw2 + kTw2Plain * 32;
+#pragma unroll
+    for (int d = 0; d < 4; d++) {
+        const int h = 8 >> d;
+#pragma unroll
+        for (int j = 0; j < 16; j++)
+            if ((j & h) == 0) {
+                const int b = j >> (4 - d);
+                const double2 kt = tw1t[(1 << d) - 1 + b];
+                if (tw_form_a(ROOT, d, b)) {
+                    bf_fwd_tan<true>(va[j], va[j + h], kt);
+                    bf_fwd_tan<true>(vb[j], vb[j + h], kt);
+                }
+                else {
+                    bf_fwd_tan<false>(va[j], va[j + h], kt);
+                    bf_fwd_tan<false>(vb[j], vb[j + h], kt);
+                }
+            }
+    }
+    xpose_fwd<false>(va, xbuf, lane);
+    xpose_fwd<false>(vb, xbuf, lane);
+#pragma unroll
+    for (int d = 4; d < 8; d++) {
+        const int h = 8 >> (d - 4);
+#pragma unroll
+        for (int j = 0; j < 16; j++)
+            if ((j & h) == 0) {
+                const int k = tw_k(d, j >> (8 - d));
+                const double2 w = tw2t[tw_entry(d, k & 3) * 32 + lane];
+                if (k >> 2) {
+                    bf_fwd_tq<1>(va[j], va[j + h], w);
+                    bf_fwd_tq<1>(vb[j], vb[j + h], w);
+                }
+                else {
+                    bf_fwd_tq<0>(va[j], va[j + h], w);
+                    bf_fwd_tq<0>(vb[j], vb[j + h], w);
+                }
+            }
+    }
+    const bool odd = lane & 1;
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        const double2 ra = shfl_xor_d2(odd ? va[k] : va[k + 8], 1);
+        const double2 rb = shfl_xor_d2(odd ? vb[k] : vb[k + 8], 1);
+        double2 ua = odd ? ra : va[k], wa = odd ? va[k + 8] : ra;
+        double2 ub = odd ? rb : vb[k], wb = odd ? vb[k + 8] : rb;
+        const int br = bitrev_const(k, 3);
+        const double2 t = tw2t[tw_entry(8, br & 3) * 32 + lane];
+        if (br >> 2) {
+            bf_fwd_tq<1>(ua, wa, t);
+            bf_fwd_tq<1>(ub, wb, t);
+        }
+        else {
+            bf_fwd_tq<0>(ua, wa, t);
+            bf_fwd_tq<0>(ub, wb, t);
+        }
+        va[k] = ua;
+        va[k + 8] = wa;
+        vb[k] = ub;
+        vb[k + 8] = wb;
+    }
+}
+
 }  // namespace vsp
