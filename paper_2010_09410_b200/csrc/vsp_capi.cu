@@ -196,6 +196,22 @@ struct vsp_ctx {
     };
     std::map<std::string, KTimer> timers;
 
+    // host-pipeline copy stream + per-chunk events (vsp_hom_gate_batch)
+    cudaStream_t cstream = nullptr;
+    std::vector<cudaEvent_t> ev_in, ev_done;
+    void ensure_copy_stream(size_t chunks)
+    {
+        if (!cstream)
+            VSP_CUDA_CHECK(cudaStreamCreateWithFlags(&cstream, cudaStreamNonBlocking));
+        while (ev_in.size() < chunks) {
+            cudaEvent_t a, b;
+            VSP_CUDA_CHECK(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+            VSP_CUDA_CHECK(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+            ev_in.push_back(a);
+            ev_done.push_back(b);
+        }
+    }
+
     void set_device() const { VSP_CUDA_CHECK(cudaSetDevice(device)); }
     size_t ksk_words() const
     {
@@ -954,6 +970,12 @@ void vsp_destroy(vsp_ctx* c)
     c->mg_recv.release();
     if (c->comm)
         nccl().commDestroy((ncclComm_t)c->comm);
+    for (size_t k = 0; k < c->ev_in.size(); k++) {
+        cudaEventDestroy(c->ev_in[k]);
+        cudaEventDestroy(c->ev_done[k]);
+    }
+    if (c->cstream)
+        cudaStreamDestroy(c->cstream);
     cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -1073,9 +1095,48 @@ int vsp_hom_gate_batch(vsp_ctx* c, const int32_t* kinds, const uint32_t* in, uin
         const size_t w = c->p.n + 1;
         uint32_t* d_in = c->in.as<uint32_t>(G * 3 * w);
         uint32_t* d_out = c->out.as<uint32_t>(G * w);
-        VSP_CUDA_CHECK(cudaMemcpyAsync(d_in, in, G * 3 * w * 4, cudaMemcpyHostToDevice, c->stream));
-        hom_gate_dev(c, kinds, d_in, d_out, G, c->stream);
-        VSP_CUDA_CHECK(cudaMemcpyAsync(out, d_out, G * w * 4, cudaMemcpyDeviceToHost, c->stream));
+        // Host pipeline: the batch is cut into chunks of one full blind-rotation wave
+        // (8 tasks per SM); chunk k+1's upload and chunk k-1's download run on the copy
+        // stream while chunk k computes, so only the first upload and the last download
+        // are exposed.  Small batches take a single chunk.
+        std::vector<size_t> cuts{0};
+        {
+            const size_t target = (size_t)8 * c->sms;
+            size_t tasks = 0;
+            for (size_t g = 0; g < G; g++) {
+                tasks += kinds[g] == kMux ? 2 : kinds[g] == kNot ? 0 : 1;
+                if (tasks >= target && G - (g + 1) > 0) {
+                    cuts.push_back(g + 1);
+                    tasks = 0;
+                }
+            }
+            cuts.push_back(G);
+        }
+        const size_t nch = cuts.size() - 1;
+        if (nch == 1) {
+            VSP_CUDA_CHECK(cudaMemcpyAsync(d_in, in, G * 3 * w * 4, cudaMemcpyHostToDevice, c->stream));
+            hom_gate_dev(c, kinds, d_in, d_out, G, c->stream);
+            VSP_CUDA_CHECK(cudaMemcpyAsync(out, d_out, G * w * 4, cudaMemcpyDeviceToHost, c->stream));
+            VSP_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+            return;
+        }
+        c->ensure_copy_stream(nch);
+        for (size_t k = 0; k < nch; k++) {
+            const size_t lo = cuts[k], cnt = cuts[k + 1] - lo;
+            VSP_CUDA_CHECK(cudaMemcpyAsync(d_in + lo * 3 * w, in + lo * 3 * w, cnt * 3 * w * 4,
+                                           cudaMemcpyHostToDevice, c->cstream));
+            VSP_CUDA_CHECK(cudaEventRecord(c->ev_in[k], c->cstream));
+            VSP_CUDA_CHECK(cudaStreamWaitEvent(c->stream, c->ev_in[k], 0));
+            hom_gate_dev(c, kinds + lo, d_in + lo * 3 * w, d_out + lo * w, cnt, c->stream);
+            VSP_CUDA_CHECK(cudaEventRecord(c->ev_done[k], c->stream));
+        }
+        for (size_t k = 0; k < nch; k++) {
+            const size_t lo = cuts[k], cnt = cuts[k + 1] - lo;
+            VSP_CUDA_CHECK(cudaStreamWaitEvent(c->cstream, c->ev_done[k], 0));
+            VSP_CUDA_CHECK(cudaMemcpyAsync(out + lo * w, d_out + lo * w, cnt * w * 4,
+                                           cudaMemcpyDeviceToHost, c->cstream));
+        }
+        VSP_CUDA_CHECK(cudaStreamSynchronize(c->cstream));
         VSP_CUDA_CHECK(cudaStreamSynchronize(c->stream));
     });
 }
