@@ -286,24 +286,27 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
 // br1024_kernel runs one dependent chain of n external products per warp and per-level
 // latency is the chain length (630 x ~9 us).  Here FOUR warps share one task: warp r
 // owns gadget row r = 2P + lvl (digit level lvl of accumulator polynomial P), so each
-// external product is one forward transform + one MAC row deep instead of four:
+// external product is one forward transform deep instead of four:
 //   1. warp r: digits of row r of (X^bara - 1) acc   (decomposePoly, poly.hpp:79-97)
-//   2. warp r: forward transform, partial products A_r = z.bkA_r, B_r = z.bkB_r
-//   3. one smem exchange: warp 0 gathers A = sum A_r, warp 1 gathers B = sum B_r
+//   2. warp r: forward transform, published to smem
+//   3. warp 0 forms A = sum_r z_r bkA_r, warp 1 B = sum_r z_r bkB_r (own row from
+//      registers), in row order as in br1024_kernel
 //   4. warps 0 / 1: inverse transform, round, acc.a / acc.b += (ops.cpp:587-597)
-// The four row products are summed in row order as in br1024_kernel (here as separate
-// products then adds instead of a fused chain); every coefficient is an integer the
-// FP64 error (<< 1/2) rounds back to exactly, so outputs equal the reference's.  All four BK rows of step i are
-// staged together (64 KiB) by the bulk-copy engine, two steps in flight.
+// Every coefficient is an integer the FP64 error (<< 1/2) rounds back to exactly, so the
+// outputs equal the reference's.  All four BK rows of step i are staged together (64 KiB)
+// by the bulk-copy engine, two steps in flight; warp 3 refills a slot once warps 0 and 1
+// have released it (mbarrier `empty`).
 constexpr int kLatBuf = kFftXbufStride;  // double2 per exchange / transpose buffer
+constexpr int kLatThreads = 160;          // 4 transform warps + 1 producer warp
 
 struct BrLatSmem {
     double2 ring[2][4 * 1024];
     double2 tw2[kTw2Entries * 32];
-    double2 bufA[4][kLatBuf];  // row partials of output A / B; warp r's forward
-    double2 bufB[4][kLatBuf];  // transposes use xbuf[r] (aliases bufA[r], see below)
+    double2 bufA[4][kLatBuf];  // transformed row z_r (also warp r's forward transposes)
+    double2 bufB[2][kLatBuf];  // inverse-transform transposes of warps 0 / 1
     uint32_t acc[2048];
     uint64_t full[2];
+    uint64_t empty[2];  // slot consumed by the four transform warps (count 4)
     __device__ double2* xbuf(int r) { return bufA[r]; }
 };
 
@@ -314,12 +317,12 @@ __device__ __forceinline__ void bar_group(int id, int nthreads)
 
 // PROBE: per-warp clock64 totals of the step phases -> probe[task][warp][16] (tuning).
 template <int BG, bool PROBE = false>
-__global__ void __launch_bounds__(128, 1)
+__global__ void __launch_bounds__(kLatThreads, 1)
     br_lat_kernel(const uint32_t* __restrict__ tasks, const double2* __restrict__ bkfd,
                   const double2* __restrict__ tw2g, uint32_t* __restrict__ out, int n,
                   unsigned long long* __restrict__ probe = nullptr)
 {
-    unsigned long long ph[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long ph[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     long long tprev = PROBE ? clock64() : 0;
     auto mark = [&](int k) {
         if constexpr (PROBE) {
@@ -333,13 +336,14 @@ __global__ void __launch_bounds__(128, 1)
     const int r = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int task = blockIdx.x;
     const uint32_t* lwe = tasks + (size_t)task * (n + 1);
-    const int P = r >> 1, lvl = r & 1;
 
     for (int i = threadIdx.x; i < kTw2Entries * 32; i += blockDim.x)
         sm.tw2[i] = tw2g[i];
     if (threadIdx.x == 0) {
-        mbar_init(&sm.full[0], 1);
-        mbar_init(&sm.full[1], 1);
+        for (int q = 0; q < 2; q++) {
+            mbar_init(&sm.full[q], 1);
+            mbar_init(&sm.empty[q], 4);
+        }
     }
     {
         const uint32_t rot = (2048u - mod_switch_2n(lwe[n], 11)) & 2047u;
@@ -354,98 +358,115 @@ __global__ void __launch_bounds__(128, 1)
         }
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < 2 && s < n; s++) {
-            mbar_arrive_expect_tx(&sm.full[s], 65536);
-            bulk_g2s(sm.ring[s], bkfd + (size_t)s * 4096, 65536, &sm.full[s]);
+
+    if (r == 4) {
+        // producer warp: keeps the two-slot ring of bk rows full.  A warp issuing bulk
+        // copies is slowed while they are in flight, so no transform warp issues them.
+        if (lane == 0) {
+            for (int i = 0; i < n; i++) {
+                const int s = i & 1;
+                if (i >= 2)
+                    mbar_wait(&sm.empty[s], (uint32_t)(((i - 2) >> 1) & 1));
+                mbar_arrive_expect_tx(&sm.full[s], 65536);
+                bulk_g2s(sm.ring[s], bkfd + (size_t)i * 4096, 65536, &sm.full[s]);
+            }
         }
     }
+    else {
+        constexpr uint32_t kHalf = 1u << (BG - 1);
+        constexpr uint32_t kMask = (1u << BG) - 1;
+        constexpr uint32_t kOffset = (kHalf << (32 - BG)) + (kHalf << (32 - 2 * BG));
+        const int P = r >> 1, lvl = r & 1;
+        const uint32_t* src = sm.acc + P * 1024;
+        const uint32_t sh = (uint32_t)(32 - (lvl + 1) * BG);
+        // MAC / inverse role: output o (0: a, 1: b) on the warp pair (o, o + 2), half h
+        const int o = r & 1, h = r >> 1;
+        const int L = 16 * h + (lane & 15), e = lane >> 4;
 
-    constexpr uint32_t kHalf = 1u << (BG - 1);
-    constexpr uint32_t kMask = (1u << BG) - 1;
-    constexpr uint32_t kOffset = (kHalf << (32 - BG)) + (kHalf << (32 - 2 * BG));
-    const uint32_t* src = sm.acc + P * 1024;
-    const uint32_t sh = (uint32_t)(32 - (lvl + 1) * BG);
-
+        // a_i is fetched one step ahead (lwe[i + 1] <= lwe[n] is in bounds) so the global
+        // load latency hides behind the current external product
+        uint32_t a_next = lwe[0];
 #pragma unroll 1
-    for (int i = 0; i < n; i++) {
-        const uint32_t bara = mod_switch_2n(lwe[i], 11);
-        double2 z[16];
-        {
-            const uint32_t lo = (uint32_t)lane + (uint32_t)opaque_zero();
-            const uint32_t lk = lo - bara;
-            const uint32_t* srcl = src + lo;
+        for (int i = 0; i < n; i++) {
+            const uint32_t bara = mod_switch_2n(a_next, 11);
+            a_next = lwe[i + 1];
+            mark(9);
+            double2 z[16];
+            {
+                const uint32_t lo = (uint32_t)lane + (uint32_t)opaque_zero();
+                const uint32_t lk = lo - bara;
+                const uint32_t* srcl = src + lo;
 #pragma unroll
-            for (int j = 0; j < 16; j++) {
-                const uint32_t v0 = rot_coef1024(src, lk + 32 * j) - srcl[32 * j] + kOffset;
-                const uint32_t v1 = rot_coef1024(src, lk + 32 * j + 512) - srcl[32 * j + 512] + kOffset;
-                // level lvl digit = bits [32 - (lvl+1) BG, 32 - lvl BG) of v, recentred;
-                // one code path for both levels (the mask is a no-op for lvl 0)
-                const uint32_t d0 = ((v0 >> sh) & kMask) - kHalf;
-                const uint32_t d1 = ((v1 >> sh) & kMask) - kHalf;
-                z[j].x = (double)(int32_t)d0;
-                z[j].y = (double)(int32_t)d1;
+                for (int j = 0; j < 16; j++) {
+                    const uint32_t v0 = rot_coef1024(src, lk + 32 * j) - srcl[32 * j] + kOffset;
+                    const uint32_t v1 = rot_coef1024(src, lk + 32 * j + 512) - srcl[32 * j + 512] + kOffset;
+                    // level lvl digit = bits [32 - (lvl+1) BG, 32 - lvl BG) of v, recentred;
+                    // one code path for both levels (the mask is a no-op for lvl 0)
+                    const uint32_t d0 = ((v0 >> sh) & kMask) - kHalf;
+                    const uint32_t d1 = ((v1 >> sh) & kMask) - kHalf;
+                    z[j].x = (double)(int32_t)d0;
+                    z[j].y = (double)(int32_t)d1;
+                }
             }
-        }
-        mark(0);
-        fft512_fwd(z, sm.xbuf(r), sm.tw2, lane);
-        mark(1);
-        const int s = i & 1;
-        mbar_wait(&sm.full[s], (uint32_t)((i >> 1) & 1));
-        mark(2);
-        const double2* bk = sm.ring[s] + r * 1024;
-        // partial products of row r -> bufA[r], bufB[r] (one code path for all warps)
-        __syncwarp();
+            mark(0);
+            fft512_fwd(z, sm.xbuf(r), sm.tw2, lane);
+            mark(1);
+            // publish the transformed row: z_r -> bufA[r] (warp r's own transpose buffer,
+            // free again after the transform's last __syncwarp)
+            __syncwarp();
 #pragma unroll
-        for (int j = 0; j < 16; j++) {
-            const double2 ba = bk[j * 32 + lane];
-            const double2 bb = bk[512 + j * 32 + lane];
-            sm.bufA[r][j * 32 + lane] = make_double2(fma(z[j].x, ba.x, -z[j].y * ba.y),
-                                                     fma(z[j].x, ba.y, z[j].y * ba.x));
-            sm.bufB[r][j * 32 + lane] = make_double2(fma(z[j].x, bb.x, -z[j].y * bb.y),
-                                                     fma(z[j].x, bb.y, z[j].y * bb.x));
-        }
-        mark(3);
-        bar_group(1, 128);  // all partials written; every warp is done with ring slot s
-        mark(4);
-        // refill from warp 3 (idle until the next step): issuing a bulk copy can hold the
-        // issuing warp, so keep it off the inverse-transform warps' critical path
-        if (threadIdx.x == 96 && i + 2 < n) {
-            fence_proxy_async();
-            mbar_arrive_expect_tx(&sm.full[s], 65536);
-            bulk_g2s(sm.ring[s], bkfd + (size_t)(i + 2) * 4096, 65536, &sm.full[s]);
-        }
-        if (r < 2) {
-            // warp 0 sums output A, warp 1 output B, rows in order 0..3 (as br1024_kernel)
-            const double2(*pr)[kLatBuf] = r == 0 ? sm.bufA : sm.bufB;
-            double2 acc2[16];
+            for (int j = 0; j < 16; j++)
+                sm.bufA[r][j * 32 + lane] = z[j];
+            const int s = i & 1;
+            bar_group(1, 128);  // all four rows transformed
+            mark(2);
+            // output o at this lane's 8 slots: acc_o = sum_q z_q . bk[q][o], rows in order
+            // 0..3 as in br1024_kernel
+            mbar_wait(&sm.full[s], (uint32_t)((i >> 1) & 1));
+            mark(3);
+            const double2* bk = sm.ring[s] + o * 512;
+            double2 u[8];
 #pragma unroll
-            for (int j = 0; j < 16; j++) {
-                const double2 a0 = pr[0][j * 32 + lane], a1 = pr[1][j * 32 + lane];
-                const double2 a2 = pr[2][j * 32 + lane], a3 = pr[3][j * 32 + lane];
-                acc2[j] = make_double2(((a0.x + a1.x) + a2.x) + a3.x, ((a0.y + a1.y) + a2.y) + a3.y);
+            for (int t = 0; t < 8; t++) {
+                const int q = (2 * t + e) * 32 + L;
+                const double2 z0 = sm.bufA[0][q], z1 = sm.bufA[1][q];
+                const double2 z2 = sm.bufA[2][q], z3 = sm.bufA[3][q];
+                const double2 b0 = bk[q], b1 = bk[1024 + q], b2 = bk[2048 + q], b3 = bk[3072 + q];
+                double ax = fma(z0.x, b0.x, -z0.y * b0.y);
+                double ay = fma(z0.x, b0.y, z0.y * b0.x);
+                ax = fma(z1.x, b1.x, fma(-z1.y, b1.y, ax));
+                ay = fma(z1.x, b1.y, fma(z1.y, b1.x, ay));
+                ax = fma(z2.x, b2.x, fma(-z2.y, b2.y, ax));
+                ay = fma(z2.x, b2.y, fma(z2.y, b2.x, ay));
+                ax = fma(z3.x, b3.x, fma(-z3.y, b3.y, ax));
+                ay = fma(z3.x, b3.y, fma(z3.y, b3.x, ay));
+                u[t] = make_double2(ax, ay);
             }
+            __syncwarp();
+            if (lane == 0)
+                mbar_arrive(&sm.empty[s]);  // this warp is done with slot s
             mark(5);
-            // transposes in the exchange buffer of a row only this warp reads
-            fft512_inv(acc2, r == 0 ? sm.bufA[3] : sm.bufB[3], sm.tw2, lane);
+            fft512_inv_pair(u, sm.bufB[o], sm.tw2, lane, h, 3 + o);
             mark(6);
-            uint32_t* dst = sm.acc + r * 1024;
+            // (every warp read acc for its digits before barrier 1)
+            uint32_t* dst = sm.acc + o * 1024;
 #pragma unroll
-            for (int j = 0; j < 16; j++) {
-                const int p = lane + 32 * j;
-                dst[p] += (uint32_t)__double2ll_rn(acc2[j].x);
-                dst[p + 512] += (uint32_t)__double2ll_rn(acc2[j].y);
+            for (int t = 0; t < 8; t++) {
+                const int p = L + 32 * (t + 8 * e);
+                dst[p] += (uint32_t)__double2ll_rn(u[t].x);
+                dst[p + 512] += (uint32_t)__double2ll_rn(u[t].y);
             }
             mark(7);
+            bar_group(2, 128);  // acc updated before the next step's digits
+            mark(8);
         }
-        bar_group(2, 128);  // acc updated before the next step's digits
-        mark(8);
     }
     if constexpr (PROBE) {
-        if (lane == 0)
-            for (int k = 0; k < 9; k++)
+        if (lane == 0 && r < 4)
+            for (int k = 0; k < 10; k++)
                 probe[((size_t)task * 4 + r) * 16 + k] = ph[k];
     }
+    __syncthreads();
     uint4* dst = reinterpret_cast<uint4*>(out + (size_t)task * 2048);
     const uint4* s4 = reinterpret_cast<const uint4*>(sm.acc);
     for (int q = threadIdx.x; q < 512; q += blockDim.x)

@@ -496,4 +496,100 @@ __device__ __forceinline__ void fft512_fwd2(double2 (&va)[16], double2 (&vb)[16]
     }
 }
 
+// Inverse transform of one block split over a warp pair (64 lanes x 8 values), for the
+// latency kernel.  Lane l of pair half h stands for virtual lane L = 16h + (l & 15) of
+// fft512_inv's layout and half e = l >> 4 of that lane's 16 values:
+//   input  u[t] = v_L[2t + e]                    (frequency slot (2t + e) * 32 + L)
+//   output u[t] = z at time position L + 32 (t + 8e)   (z_p = x_p + i x_{p+512})
+// The butterflies are fft512_inv's, in the same order with the same twiddles; the two
+// stages that pair the halves (7, and 0 after the transpose) go through __shfl_xor 16,
+// stage 8's lane pairs (L, L^1) through __shfl_xor 1.  xbuf: kFftXbufStride double2
+// shared by the pair, synchronised by named barrier bar_id over its 64 threads.
+__device__ __forceinline__ double2 cmul(const double2 a, const double2 b)
+{
+    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+
+template <int ROOT = 0>
+__device__ __forceinline__ void fft512_inv_pair(double2 (&u)[8], double2* xbuf,
+                                                const double2* tw2, int lane, int h, int bar_id)
+{
+    const int L = 16 * h + (lane & 15);
+    const int e = lane >> 4;
+    const bool oddL = L & 1;
+    const double sg = e ? -1.0 : 1.0;
+    // stage 8: butterflies (k, k + 8), k = 2 tp + e; bitrev3(k) = (e << 2) | bitrev2(tp)
+#pragma unroll
+    for (int tp = 0; tp < 4; tp++) {
+        double2 w = tw2[tw_entry(8, bitrev_const(tp, 2)) * 32 + L];
+        if (e)
+            w = make_double2(-w.y, w.x);  // i^Q with Q = e
+        double2 a = u[tp], b = u[tp + 4];
+        bf_inv(a, b, w);
+        const double2 recv = shfl_xor_d2(oddL ? a : b, 1);
+        u[tp] = oddL ? recv : a;
+        u[tp + 4] = oddL ? b : recv;
+    }
+    // stage 7: pairs (2t, 2t + 1) = the two halves; half 0 keeps a + b, half 1 (a - b) conj(w)
+#pragma unroll
+    for (int t = 0; t < 8; t++) {
+        const int k = tw_k(7, t);
+        double2 w = tw2[tw_entry(7, k & 3) * 32 + L];
+        if (k >> 2)
+            w = make_double2(-w.y, w.x);
+        const double2 c = e ? make_double2(w.x, -w.y) : make_double2(1.0, 0.0);
+        const double2 o = shfl_xor_d2(u[t], 16);
+        const double2 d = make_double2(fma(sg, u[t].x, o.x), fma(sg, u[t].y, o.y));
+        u[t] = cmul(d, c);
+    }
+    // stages 6, 5, 4: local pairs (t, t + hh)
+#pragma unroll
+    for (int d = 6; d >= 4; d--) {
+        const int hh = 1 << (6 - d);
+#pragma unroll
+        for (int t = 0; t < 8; t++)
+            if ((t & hh) == 0) {
+                const int k = tw_k(d, t >> (7 - d));
+                const double2 w = tw2[tw_entry(d, k & 3) * 32 + L];
+                if (k >> 2)
+                    bf_inv_q<1>(u[t], u[t + hh], w);
+                else
+                    bf_inv_q<0>(u[t], u[t + hh], w);
+            }
+    }
+    // transpose through the pair's buffer (fft512_inv's xpose_inv element mapping)
+    const int wbase = (L & 1) + 34 * (L >> 1) + 2 * e;
+#pragma unroll
+    for (int t = 0; t < 8; t++)
+        xbuf[wbase + 4 * t] = u[t];
+    asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+#pragma unroll
+    for (int t = 0; t < 8; t++)
+        u[t] = xbuf[L + 34 * (t + 8 * e)];
+    // stages 3, 2, 1 local (j = t + 8e: twiddle index depends on the half), stage 0 pairs
+    // the halves
+    const double2* tw1 = &c_tw1[ROOT][0] + opaque_zero();
+#pragma unroll
+    for (int d = 3; d >= 1; d--) {
+        const int hh = 8 >> d;
+#pragma unroll
+        for (int t = 0; t < 8; t++)
+            if ((t & hh) == 0) {
+                const int base = (1 << d) - 1 + (t >> (4 - d));
+                const double2 w0 = tw1[base], w1 = tw1[base + (8 >> (4 - d))];
+                bf_inv(u[t], u[t + hh], e ? w1 : w0);
+            }
+    }
+    {
+        const double2 w = tw1[0];
+        const double2 c = e ? make_double2(w.x, -w.y) : make_double2(1.0, 0.0);
+#pragma unroll
+        for (int t = 0; t < 8; t++) {
+            const double2 o = shfl_xor_d2(u[t], 16);
+            const double2 d = make_double2(fma(sg, u[t].x, o.x), fma(sg, u[t].y, o.y));
+            u[t] = cmul(d, c);
+        }
+    }
+}
+
 }  // namespace vsp

@@ -118,9 +118,13 @@ __global__ void __launch_bounds__(256, 1)
     for (int i = 1; i <= 4; i++)
         offset += half << (64 - i * bgbits);
 
+    // a_i is fetched one step ahead (lwe[i + 1] <= lwe[n] is in bounds) so the global
+    // load latency hides behind the current external product
+    uint32_t a_next = lwe[0];
 #pragma unroll 1
     for (int i = 0; i < n; i++) {
-        const uint32_t bara = mod_switch_2n(lwe[i], 12);
+        const uint32_t bara = mod_switch_2n(a_next, 12);
+        a_next = lwe[i + 1];
         // ---- phase A: row r = warp (poly r/4, digit level r%4), forward transforms
         {
             const int P = warp >> 2, L = warp & 3;

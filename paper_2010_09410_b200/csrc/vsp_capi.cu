@@ -331,7 +331,7 @@ void launch_br(vsp_ctx* c, const uint32_t* d_tasks, uint32_t* d_trlwe, int T, cu
             if (probe) {
                 unsigned long long* d_pr = nullptr;
                 VSP_CUDA_CHECK(cudaMalloc(&d_pr, (size_t)T * 64 * 8));
-                br_lat_kernel<kBrBg, true><<<T, 128, sizeof(BrLatSmem), st>>>(
+                br_lat_kernel<kBrBg, true><<<T, kLatThreads, sizeof(BrLatSmem), st>>>(
                     d_tasks, c->d_bk1fd, c->d_tw2, d_trlwe, (int)p.n, d_pr);
                 std::vector<unsigned long long> h(64);
                 VSP_CUDA_CHECK(cudaMemcpyAsync(h.data(), d_pr, 64 * 8, cudaMemcpyDeviceToHost, st));
@@ -339,13 +339,13 @@ void launch_br(vsp_ctx* c, const uint32_t* d_tasks, uint32_t* d_trlwe, int T, cu
                 cudaFree(d_pr);
                 for (int w = 0; w < 4; w++) {
                     fprintf(stderr, "br_lat probe warp %d cycles/step:", w);
-                    for (int k = 0; k < 9; k++)
+                    for (int k = 0; k < 10; k++)
                         fprintf(stderr, " %.0f", (double)h[w * 16 + k] / p.n);
                     fprintf(stderr, "\n");
                 }
             }
             timed(c, "br_lat", st, [&] {
-                br_lat_kernel<kBrBg><<<T, 128, sizeof(BrLatSmem), st>>>(d_tasks, c->d_bk1fd,
+                br_lat_kernel<kBrBg><<<T, kLatThreads, sizeof(BrLatSmem), st>>>(d_tasks, c->d_bk1fd,
                                                                       c->d_tw2, d_trlwe, (int)p.n);
             });
             VSP_CUDA_CHECK(cudaGetLastError());
