@@ -11,6 +11,9 @@
 #ifndef VSP_BR_INV2
 #define VSP_BR_INV2 1
 #endif
+#ifndef VSP_IKS_PAIR
+#define VSP_IKS_PAIR 0  // 16-way switch compiles to a divergent compare tree: 6.5 vs 3.4 ms
+#endif
 #ifndef VSP_BR_FWD2
 #define VSP_BR_FWD2 0  // measured slower (spills at 255 regs): 32.8 vs 30.2 ms
 #endif
@@ -169,20 +172,21 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
         for (int j = 0; j < 16; j++) {
             const uint32_t v0 = rot_coef1024(src, lk + 32 * j) - srcl[32 * j] + kOffset;
             const uint32_t v1 = rot_coef1024(src, lk + 32 * j + 512) - srcl[32 * j + 512] + kOffset;
-            const uint32_t d0 = (v0 >> (32 - BG)) - kHalf;
-            const uint32_t d1 = (v1 >> (32 - BG)) - kHalf;
-            const uint32_t e0 = ((v0 >> (32 - 2 * BG)) & kMask) - kHalf;
-            const uint32_t e1 = ((v1 >> (32 - 2 * BG)) & kMask) - kHalf;
-            sm.dig[warp][0][j * 32 + lane] = (d0 & 0xffffu) | (d1 << 16);
-            sm.dig[warp][1][j * 32 + lane] = (e0 & 0xffffu) | (e1 << 16);
+            // digits parked in 16-bit offset binary (digit + 2^15) for ob_to_double
+            const uint32_t d0 = (v0 >> (32 - BG)) + (32768u - kHalf);
+            const uint32_t d1 = (v1 >> (32 - BG)) + (32768u - kHalf);
+            const uint32_t e0 = ((v0 >> (32 - 2 * BG)) & kMask) + (32768u - kHalf);
+            const uint32_t e1 = ((v1 >> (32 - 2 * BG)) & kMask) + (32768u - kHalf);
+            sm.dig[warp][0][j * 32 + lane] = d0 | (d1 << 16);
+            sm.dig[warp][1][j * 32 + lane] = e0 | (e1 << 16);
         }
     };
     auto load_digits = [&](double2 (&z)[16], int lvl) {
 #pragma unroll
         for (int j = 0; j < 16; j++) {
             const uint32_t w = sm.dig[warp][lvl][j * 32 + lane];
-            z[j].x = (double)(int16_t)(w & 0xffffu);
-            z[j].y = (double)(int16_t)(w >> 16);
+            z[j].x = ob_to_double<15>(w & 0xffffu);
+            z[j].y = ob_to_double<15>(w >> 16);
         }
     };
 
@@ -400,12 +404,10 @@ __global__ void __launch_bounds__(kLatThreads, 1)
                 for (int j = 0; j < 16; j++) {
                     const uint32_t v0 = rot_coef1024(src, lk + 32 * j) - srcl[32 * j] + kOffset;
                     const uint32_t v1 = rot_coef1024(src, lk + 32 * j + 512) - srcl[32 * j + 512] + kOffset;
-                    // level lvl digit = bits [32 - (lvl+1) BG, 32 - lvl BG) of v, recentred;
-                    // one code path for both levels (the mask is a no-op for lvl 0)
-                    const uint32_t d0 = ((v0 >> sh) & kMask) - kHalf;
-                    const uint32_t d1 = ((v1 >> sh) & kMask) - kHalf;
-                    z[j].x = (double)(int32_t)d0;
-                    z[j].y = (double)(int32_t)d1;
+                    // level-lvl digit = bits [32 - (lvl+1) BG, 32 - lvl BG) of v, recentred
+                    // (the mask is a no-op for level 0); offset binary for ob_to_double
+                    z[j].x = ob_to_double<31>(((v0 >> sh) & kMask) + (0x80000000u - kHalf));
+                    z[j].y = ob_to_double<31>(((v1 >> sh) & kMask) + (0x80000000u - kHalf));
                 }
             }
             mark(0);
@@ -764,7 +766,58 @@ __global__ void __launch_bounds__(128) iks_b2_kernel(
         }
     };
 
-    const int steps = islice * T;  // even (T = 8)
+    const int steps = islice * T;  // multiple of 8 (T = 8)
+#if VSP_IKS_PAIR
+    // Two digit steps (i, j), (i, j + 1) per gate at once: their 4 digit bits are
+    // contiguous, so one 16-way uniform branch picks both rows and IADD3 adds them
+    // together -- half the branches and adds of the one-step loop.
+    uint32_t rc[3][KPT], rd[3][KPT];
+    auto consume2 = [&](const uint32_t (&ca)[3][KPT], const uint32_t (&cb)[3][KPT], int s) {
+        const int ii = s >> 3, j = s & 7;  // j even
+        const uint4* dp = reinterpret_cast<const uint4*>(dig16 + ii * GT);
+        uint32_t dw[GT / 2];
+#pragma unroll
+        for (int q = 0; q < GT / 8; q++) {
+            const uint4 v = dp[q];
+            dw[4 * q] = v.x;
+            dw[4 * q + 1] = v.y;
+            dw[4 * q + 2] = v.z;
+            dw[4 * q + 3] = v.w;
+        }
+        const int sh = 12 - 2 * j;
+#pragma unroll
+        for (int g = 0; g < GT; g++) {
+            const uint32_t q = (dw[g >> 1] >> ((g & 1) * 16 + sh)) & 15u;  // d_j * 4 + d_j+1
+#define VSP_IKS_C(A, B)                                                   \
+    case (A) * 4 + (B):                                                   \
+        _Pragma("unroll") for (int kk = 0; kk < KPT; kk++)                \
+            acc[g][kk] += ((A) ? ca[(A) ? (A) - 1 : 0][kk] : 0u) +        \
+                          ((B) ? cb[(B) ? (B) - 1 : 0][kk] : 0u);         \
+        break;
+            switch (q) {
+                VSP_IKS_C(0, 1) VSP_IKS_C(0, 2) VSP_IKS_C(0, 3)
+                VSP_IKS_C(1, 0) VSP_IKS_C(1, 1) VSP_IKS_C(1, 2) VSP_IKS_C(1, 3)
+                VSP_IKS_C(2, 0) VSP_IKS_C(2, 1) VSP_IKS_C(2, 2) VSP_IKS_C(2, 3)
+                VSP_IKS_C(3, 0) VSP_IKS_C(3, 1) VSP_IKS_C(3, 2) VSP_IKS_C(3, 3)
+            default: break;
+            }
+#undef VSP_IKS_C
+        }
+    };
+    load(ra);
+    load(rb);
+#pragma unroll 1
+    for (int s = 0; s < steps; s += 4) {
+        load(rc);
+        load(rd);
+        consume2(ra, rb, s);
+        if (s + 4 < steps) {
+            load(ra);
+            load(rb);
+        }
+        consume2(rc, rd, s + 2);
+    }
+#else
     load(ra);
 #pragma unroll 1
     for (int s = 0; s < steps; s += 2) {
@@ -774,6 +827,7 @@ __global__ void __launch_bounds__(128) iks_b2_kernel(
             load(ra);
         consume(rb, s + 1);
     }
+#endif
 #pragma unroll
     for (int g = 0; g < GT; g++) {
         if (g >= ng)

@@ -171,6 +171,14 @@ __device__ __forceinline__ void bf_inv_q(double2& a, double2& b, const double2 w
         bf_inv(a, b, w);
 }
 
+// Exact small-integer -> double without I2F: for an offset-binary word u = d + 2^k (k < 52),
+// (2^52 + u) - (2^52 + 2^k) = d exactly (one DADD; the I2F.F64 conversion is quarter rate).
+template <int K>
+__device__ __forceinline__ double ob_to_double(uint32_t u)
+{
+    return __hiloint2double(0x43300000, (int)u) - (4503599627370496.0 + (double)(1ull << K));
+}
+
 // An opaque zero: keeps the compiler from hoisting the per-stage twiddle loads out of
 // the blind-rotation loop (which would pin ~60 registers for the whole kernel).
 __device__ __forceinline__ int opaque_zero()
