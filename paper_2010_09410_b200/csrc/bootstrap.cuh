@@ -743,9 +743,14 @@ __global__ void __launch_bounds__(128) iks_b2_kernel(
             dw[4 * q + 3] = v.w;
         }
         const int sh = 14 - 2 * j;
+        // all GT digits first (independent shifts, full ILP), then one uniform branch per gate
+        uint32_t dg[GT];
+#pragma unroll
+        for (int g = 0; g < GT; g++)
+            dg[g] = (dw[g >> 1] >> ((g & 1) * 16 + sh)) & 3u;
 #pragma unroll
         for (int g = 0; g < GT; g++) {
-            const uint32_t d = (dw[g >> 1] >> ((g & 1) * 16 + sh)) & 3u;
+            const uint32_t d = dg[g];
             if (d == 0)
                 continue;
             if (d == 1) {

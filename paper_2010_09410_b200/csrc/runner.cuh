@@ -64,7 +64,7 @@ struct vsp_netlist {
     std::vector<std::vector<int>> level_gates, level_mem;
     std::vector<int> const_cells;
     // device state
-    DevBuf values, dff, gin, gout, nets_buf, inputs_store;
+    DevBuf values, dff, gin, gout, nets_buf, inputs_store, cbraw;
     std::vector<int> input_nets;     // nets driven by module inputs (setInput targets)
     std::vector<uint8_t> is_input;   // net -> is module input
     std::vector<int> dff_q, dff_d;   // per DFF: output net (Q), input net (D)
@@ -180,6 +180,48 @@ void upload_ints(vsp_ctx* c, DevBuf& buf, const std::vector<int>& v, cudaStream_
     (void)c;
 }
 
+// A ROM port and a RAM port in the same level: their address circuit bootstraps (v_rom + v
+// TLWEs -> TRGSWs) run as ONE batched launch sequence -- the level-2 blind rotations of
+// both ports side by side on the SMs -- then the two ports proceed as in the per-cell
+// path.  The ports are independent, so the results equal the per-port order.
+void run_mem_pair(vsp_netlist* nl, const std::vector<int>& cells, uint32_t* vals, cudaStream_t st)
+{
+    vsp_ctx* c = nl->ctx;
+    const size_t n1 = c->p.n + 1;
+    const int rom = nl->kind[cells[0]] == cRom ? cells[0] : cells[1];
+    const int ram = rom == cells[0] ? cells[1] : cells[0];
+    std::vector<int> ins(nl->in_nets.begin() + nl->in_off[rom], nl->in_nets.begin() + nl->in_off[rom + 1]);
+    const int vrom = (int)ins.size();
+    ins.insert(ins.end(), nl->in_nets.begin() + nl->in_off[ram], nl->in_nets.begin() + nl->in_off[ram + 1]);
+    std::vector<int> outs(nl->out_nets.begin() + nl->out_off[rom], nl->out_nets.begin() + nl->out_off[rom + 1]);
+    const int nrom_out = (int)outs.size();
+    outs.insert(outs.end(), nl->out_nets.begin() + nl->out_off[ram], nl->out_nets.begin() + nl->out_off[ram + 1]);
+    const int w = (int)outs.size() - nrom_out;
+    const int v = (int)ins.size() - vrom - w - 1;
+    if (v != (int)nl->ram_v || w != (int)nl->ram_w)
+        throw std::invalid_argument("ramCycle: address width mismatch");
+    upload_ints(c, nl->nets_buf, ins, st);
+    uint32_t* gin = nl->gin.as<uint32_t>(ins.size() * n1);
+    uint32_t* gout = nl->gout.as<uint32_t>(outs.size() * n1);
+    gather_tlwe_kernel<<<(unsigned)ins.size(), 128, 0, st>>>(nl->nets_buf.as<int>(0), (int)ins.size(),
+                                                              vals, gin, (int)c->p.n);
+    c->launches++;
+    // ROM address (vrom) and RAM address (v) are contiguous in gin
+    const size_t tw = trgsw_words(c->p);
+    uint32_t* raw = nl->cbraw.as<uint32_t>((size_t)(vrom + v) * tw);
+    cb_batch(c, gin, vrom + v, raw, st);
+    rom_read_dev(c, nl->rom.as<uint32_t>(0), (int)nl->rom_nluts, nl->rom_depth, gin, vrom, gout, st,
+                 raw);
+    const uint32_t* g = gin + (size_t)vrom * n1;  // addr[v], wdata[w], wflag
+    ram_cycle_dev(c, nl->ram.as<uint32_t>(0), v, w, g, g + (size_t)(v + w) * n1, g + (size_t)v * n1,
+                  gout + (size_t)nrom_out * n1, st, raw + (size_t)vrom * tw);
+    upload_ints(c, nl->nets_buf, outs, st);
+    scatter_tlwe_kernel<<<(unsigned)outs.size(), 128, 0, st>>>(nl->nets_buf.as<int>(0), (int)outs.size(),
+                                                                gout, vals, (int)c->p.n);
+    c->launches++;
+    VSP_CUDA_CHECK(cudaGetLastError());
+}
+
 void run_cycle(vsp_netlist* nl, cudaStream_t st)
 {
     vsp_ctx* c = nl->ctx;
@@ -225,6 +267,10 @@ void run_cycle(vsp_netlist* nl, cudaStream_t st)
             scatter_tlwe_kernel<<<G, 128, 0, st>>>(nl->nets_buf.as<int>(0), G, gout, vals, (int)n);
             c->launches++;
             VSP_CUDA_CHECK(cudaGetLastError());
+        }
+        if (nl->level_mem[L].size() == 2 && nl->has_rom && nl->has_ram) {
+            run_mem_pair(nl, nl->level_mem[L], vals, st);
+            continue;
         }
         for (int cell : nl->level_mem[L]) {
             std::vector<int> ins(nl->in_nets.begin() + nl->in_off[cell],

@@ -714,9 +714,11 @@ void iks_of_trlwes(vsp_ctx* c, const uint32_t* d_trlwe, int count, const int* se
 }
 
 // ramCycle (mem.cpp:122-135) on a device-resident RAM image (updated in place).
+// pre_raw: the address TRGSWs when the caller has already circuit-bootstrapped them
+// (the netlist runner batches the CBs of every memory port of a level into one launch).
 void ram_cycle_dev(vsp_ctx* c, uint32_t* d_ram, int v, int w, const uint32_t* d_addr,
                    const uint32_t* d_wflag, const uint32_t* d_wdata, uint32_t* d_readout,
-                   cudaStream_t st)
+                   cudaStream_t st, const uint32_t* pre_raw = nullptr)
 {
     require_cb(c);
     const Params& p = c->p;
@@ -724,8 +726,12 @@ void ram_cycle_dev(vsp_ctx* c, uint32_t* d_ram, int v, int w, const uint32_t* d_
         throw std::invalid_argument("ramCycle: geometry out of range");
     const size_t cw = 2 * (size_t)p.N1, words = (size_t)1 << v, n1 = p.n + 1;
     // 1. addressToTrgsw + prepareAddress
-    uint32_t* raw = c->cbraw.as<uint32_t>(v * trgsw_words(p));
-    cb_batch(c, d_addr, v, raw, st);
+    const uint32_t* raw = pre_raw;
+    if (!raw) {
+        uint32_t* r = c->cbraw.as<uint32_t>(v * trgsw_words(p));
+        cb_batch(c, d_addr, v, r, st);
+        raw = r;
+    }
     prepare_selectors(c, raw, v, st);
     // 2. ramReadUnit (mem.cpp:49-72): layer d halves every tree with sel[d]
     uint32_t* A = c->layerA.as<uint32_t>((size_t)w * (words / 2) * cw);
@@ -798,7 +804,8 @@ int ctz32(uint32_t x)
 
 // addressToTrgsw + prepareAddress + romRead (engine.cpp:133-143, mem.cpp:137-177).
 void rom_read_dev(vsp_ctx* c, const uint32_t* d_luts, int nluts, uint32_t depth_bytes,
-                  const uint32_t* d_addr, int vrom, uint32_t* d_out, cudaStream_t st)
+                  const uint32_t* d_addr, int vrom, uint32_t* d_out, cudaStream_t st,
+                  const uint32_t* pre_raw = nullptr)
 {
     require_cb(c);
     const Params& p = c->p;
@@ -812,8 +819,12 @@ void rom_read_dev(vsp_ctx* c, const uint32_t* d_luts, int nluts, uint32_t depth_
     if (nluts != (1 << highBits))
         throw std::invalid_argument("romRead: LUT count mismatch");
     const size_t cw = 2 * (size_t)p.N1;
-    uint32_t* raw = c->cbraw.as<uint32_t>(std::max(vrom, 1) * trgsw_words(p));
-    cb_batch(c, d_addr, vrom, raw, st);
+    const uint32_t* raw = pre_raw;
+    if (!raw) {
+        uint32_t* r = c->cbraw.as<uint32_t>(std::max(vrom, 1) * trgsw_words(p));
+        cb_batch(c, d_addr, vrom, r, st);
+        raw = r;
+    }
     prepare_selectors(c, raw, vrom, st);
     uint32_t* A = c->layerA.as<uint32_t>(std::max(nluts / 2, 1) * cw);
     uint32_t* B = c->layerB.as<uint32_t>(std::max(nluts / 2, 1) * cw);
@@ -1505,7 +1516,7 @@ void vsp_netlist_destroy(vsp_netlist* nl)
     cudaSetDevice(nl->ctx->device);
     cudaStreamSynchronize(nl->ctx->stream);
     for (DevBuf* b : {&nl->values, &nl->dff, &nl->gin, &nl->gout, &nl->nets_buf, &nl->inputs_store,
-                      &nl->ram, &nl->rom})
+                      &nl->ram, &nl->rom, &nl->cbraw})
         b->release();
     delete nl;
 }
