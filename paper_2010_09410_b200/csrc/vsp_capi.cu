@@ -9,6 +9,7 @@
 #include <cstring>
 #include <memory>
 #include <type_traits>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <stdexcept>
@@ -212,6 +213,22 @@ struct vsp_ctx {
         }
     }
 
+    // second compute stream: key switch of finished whole waves under the remainder wave
+    // (astream, default priority) and the remainder wave itself (hstream, top priority)
+    cudaStream_t astream = nullptr, hstream = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_full = nullptr, ev_rem = nullptr;
+    void ensure_aux_stream()
+    {
+        if (astream)
+            return;
+        int least = 0, greatest = 0;
+        VSP_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        VSP_CUDA_CHECK(cudaStreamCreateWithPriority(&astream, cudaStreamNonBlocking, least));
+        VSP_CUDA_CHECK(cudaStreamCreateWithPriority(&hstream, cudaStreamNonBlocking, greatest));
+        for (cudaEvent_t* e : {&ev_fork, &ev_join, &ev_full, &ev_rem})
+            VSP_CUDA_CHECK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    }
+
     void set_device() const { VSP_CUDA_CHECK(cudaSetDevice(device)); }
     size_t ksk_words() const
     {
@@ -297,7 +314,12 @@ void set_br_attr()
 
 constexpr int kChainWarps = 8;
 
-void launch_br(vsp_ctx* c, const uint32_t* d_tasks, uint32_t* d_trlwe, int T, cudaStream_t st)
+// after_full(full): called (host side) right after the whole-wave launch of a split
+// batch, before the remainder wave is launched -- the gate path uses it to start the key
+// switch of the finished tasks on a second stream, where it co-runs with the remainder
+// wave (which holds only half of each SM's warps and registers).
+void launch_br(vsp_ctx* c, const uint32_t* d_tasks, uint32_t* d_trlwe, int T, cudaStream_t st,
+               const std::function<void(int)>& after_full = {})
 {
     if (T == 0)
         return;
@@ -311,19 +333,22 @@ void launch_br(vsp_ctx* c, const uint32_t* d_tasks, uint32_t* d_trlwe, int T, cu
         int forced = 0;
         if (const char* e = getenv("VSP_BR_WARPS"))  // tuning knob (scripts/br_occupancy.py)
             forced = atoi(e);
-        auto launch_part = [&](const uint32_t* tk, uint32_t* tr, int cnt, int W) {
+        auto launch_part_on = [&](const uint32_t* tk, uint32_t* tr, int cnt, int W, cudaStream_t s) {
             switch (W) {
-            case 8: launch_br_w<8>(c, tk, tr, cnt, st); break;
-            case 7: launch_br_w<7>(c, tk, tr, cnt, st); break;
-            case 6: launch_br_w<6>(c, tk, tr, cnt, st); break;
-            case 5: launch_br_w<5>(c, tk, tr, cnt, st); break;
-            case 4: launch_br_w<4>(c, tk, tr, cnt, st); break;
-            case 3: launch_br_w<3>(c, tk, tr, cnt, st); break;
-            case 2: launch_br_w<2>(c, tk, tr, cnt, st); break;
-            default: launch_br_w<1>(c, tk, tr, cnt, st); break;
+            case 8: launch_br_w<8>(c, tk, tr, cnt, s); break;
+            case 7: launch_br_w<7>(c, tk, tr, cnt, s); break;
+            case 6: launch_br_w<6>(c, tk, tr, cnt, s); break;
+            case 5: launch_br_w<5>(c, tk, tr, cnt, s); break;
+            case 4: launch_br_w<4>(c, tk, tr, cnt, s); break;
+            case 3: launch_br_w<3>(c, tk, tr, cnt, s); break;
+            case 2: launch_br_w<2>(c, tk, tr, cnt, s); break;
+            default: launch_br_w<1>(c, tk, tr, cnt, s); break;
             }
             VSP_CUDA_CHECK(cudaGetLastError());
             c->launches++;
+        };
+        auto launch_part = [&](const uint32_t* tk, uint32_t* tr, int cnt, int W) {
+            launch_part_on(tk, tr, cnt, W, st);
         };
         if (!forced && T <= 2 * c->sms) {
             // narrow level: latency kernel, 4 warps per task (bootstrap.cuh br_lat_kernel)
@@ -361,6 +386,19 @@ void launch_br(vsp_ctx* c, const uint32_t* d_tasks, uint32_t* d_trlwe, int T, cu
             if (full)
                 launch_part(d_tasks, d_trlwe, full, 8);
             const int rem = T - full;
+            if (full && rem && after_full) {
+                // remainder wave on a high-priority stream so its CTAs are placed before
+                // the (default-priority) key-switch CTAs that after_full starts
+                c->ensure_aux_stream();
+                VSP_CUDA_CHECK(cudaEventRecord(c->ev_full, st));
+                VSP_CUDA_CHECK(cudaStreamWaitEvent(c->hstream, c->ev_full, 0));
+                launch_part_on(d_tasks + (size_t)full * (p.n + 1), d_trlwe + (size_t)full * 2 * p.N1,
+                               rem, br_warps_for(rem, c->sms), c->hstream);
+                VSP_CUDA_CHECK(cudaEventRecord(c->ev_rem, c->hstream));
+                after_full(full);
+                VSP_CUDA_CHECK(cudaStreamWaitEvent(st, c->ev_rem, 0));
+                return;
+            }
             if (rem)
                 launch_part(d_tasks + (size_t)full * (p.n + 1), d_trlwe + (size_t)full * 2 * p.N1,
                             rem, br_warps_for(rem, c->sms));
@@ -554,8 +592,29 @@ void hom_gate_dev(vsp_ctx* c, const int32_t* kinds, const uint32_t* d_in, uint32
     });
     VSP_CUDA_CHECK(cudaGetLastError());
     c->launches++;
-    launch_br(c, d_tasks, d_trlwe, pl.T, st);
-    launch_iks(c, d_trlwe, d_gtask, d_glist, (int)pl.glist.size(), d_out, st);
+    const int Gl = (int)pl.glist.size();
+    int k1 = 0;  // gates [0, k1) of glist have all their tasks in the whole waves
+    bool forked = false;
+    auto fork_iks = [&](int full) {
+        while (k1 < Gl) {
+            const int2 t = pl.gtask[pl.glist[k1]];
+            if (std::max(t.x, t.y) >= full)
+                break;
+            k1++;
+        }
+        if (k1 == 0)
+            return;
+        c->ensure_aux_stream();
+        VSP_CUDA_CHECK(cudaEventRecord(c->ev_fork, st));
+        VSP_CUDA_CHECK(cudaStreamWaitEvent(c->astream, c->ev_fork, 0));
+        launch_iks(c, d_trlwe, d_gtask, d_glist, k1, d_out, c->astream);
+        VSP_CUDA_CHECK(cudaEventRecord(c->ev_join, c->astream));
+        forked = true;
+    };
+    launch_br(c, d_tasks, d_trlwe, pl.T, st, fork_iks);
+    launch_iks(c, d_trlwe, d_gtask, d_glist + k1, Gl - k1, d_out, st);
+    if (forked)
+        VSP_CUDA_CHECK(cudaStreamWaitEvent(st, c->ev_join, 0));
 }
 
 
@@ -987,6 +1046,12 @@ void vsp_destroy(vsp_ctx* c)
     }
     if (c->cstream)
         cudaStreamDestroy(c->cstream);
+    if (c->astream) {
+        cudaStreamDestroy(c->astream);
+        cudaStreamDestroy(c->hstream);
+        for (cudaEvent_t e : {c->ev_fork, c->ev_join, c->ev_full, c->ev_rem})
+            cudaEventDestroy(e);
+    }
     cudaStreamDestroy(c->stream);
     delete c;
 }
