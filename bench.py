@@ -182,8 +182,10 @@ def run_ours(args, world, rank, local):
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=f"cuda:{local}")
     stream = torch.cuda.current_stream()
 
+    kid = np.array([vsp.GATE_KINDS.index(k) for k in kinds], np.int32)  # GateKind ids
+
     def step():
-        eng.hom_gate_level_dev(kinds, d_in.data_ptr(), d_out.data_ptr(), GA, stream.cuda_stream)
+        eng.hom_gate_level_dev(kid, d_in.data_ptr(), d_out.data_ptr(), GA, stream.cuda_stream)
 
     for _ in range(max(args.warmup, 1)):
         step()
@@ -231,11 +233,14 @@ def run_ours(args, world, rank, local):
         if world == 1:
             h_in = torch.from_numpy(ins.view(np.int32)).pin_memory()
             h_in_np = h_in.numpy().view(np.uint32)
-            res = eng.hom_gate_batch(kinds, h_in_np)  # warm
+            h_out = torch.empty((GA, p.n + 1), dtype=torch.int32).pin_memory()
+            h_out_np = h_out.numpy().view(np.uint32)
+            res = eng.hom_gate_batch(kid, h_in_np, out=h_out_np)  # warm
             t0 = time.perf_counter()
             for _ in range(args.steps):
-                res = eng.hom_gate_batch(kinds, h_in_np)
+                res = eng.hom_gate_batch(kid, h_in_np, out=h_out_np)
             dt = time.perf_counter() - t0
+            e2e_ok = bool(np.array_equal(vsp.decrypt(keys["lv0"], res), truth))
             h2d, d2h, api = int(ins.nbytes), int(res.nbytes), \
                 "vsp_hom_gate_batch (C ABI, pinned host buffers)"
         else:
@@ -263,6 +268,8 @@ def run_ours(args, world, rank, local):
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": GA * args.steps / float(te.item()), "unit": UNIT,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "api": api}
+        if world == 1:
+            e2e["outputs_decrypt_correct"] = e2e_ok
 
     if rank != 0:
         if dist:

@@ -22,6 +22,7 @@ LIB_PATH = os.path.join(HERE, "libvsp_b200.so")
 # hvp::tfhe::GateKind order (ops.hpp:183-194)
 GATE_KINDS = ["AND", "ANDNOT", "MUX", "NAND", "NOR", "NOT", "OR", "ORNOT", "XNOR", "XOR"]
 GATE_ARITY = {k: (1 if k == "NOT" else 3 if k == "MUX" else 2) for k in GATE_KINDS}
+_KIND_ID = {k: i for i, k in enumerate(GATE_KINDS)}
 MU32 = 1 << 29
 
 _lib = None
@@ -309,12 +310,16 @@ class Engine:
 
     @staticmethod
     def _kind_ids(kinds) -> np.ndarray:
+        """Gate kinds as GateKind ids (ops.hpp:183-194): names, ints, or an int array (fast
+        path, no per-element Python work).  Out-of-range ids are rejected by the C ABI."""
+        if isinstance(kinds, np.ndarray) and kinds.dtype.kind in "iu":
+            return np.ascontiguousarray(kinds, np.int32)
         out = []
         for k in kinds:
             if isinstance(k, str):
-                if k not in GATE_KINDS:
+                if k not in _KIND_ID:
                     raise ValueError(f"homGate: unknown kind {k}")
-                out.append(GATE_KINDS.index(k))
+                out.append(_KIND_ID[k])
             else:
                 out.append(int(k))
         return np.ascontiguousarray(np.asarray(out, np.int32))
@@ -329,14 +334,19 @@ class Engine:
             x[0, i] = t
         return self.hom_gate_batch([name], x)[0]
 
-    def hom_gate_batch(self, kinds, ins: np.ndarray) -> np.ndarray:
-        """Batched homGate: kinds[G], ins (G, 3, n+1) -> (G, n+1)."""
+    def hom_gate_batch(self, kinds, ins: np.ndarray, out: np.ndarray | None = None) -> np.ndarray:
+        """Batched homGate: kinds[G], ins (G, 3, n+1) -> (G, n+1).  `out` may be a
+        caller-owned (e.g. pinned) (G, n+1) uint32 array to write into."""
         kid = self._kind_ids(kinds)
         ins = np.ascontiguousarray(ins, np.uint32)
         G = kid.size
         if ins.shape != (G, 3, self.params.n + 1):
             raise ValueError(f"expected inputs of shape {(G, 3, self.params.n + 1)}")
-        out = np.zeros((G, self.params.n + 1), np.uint32)
+        if out is None:
+            out = np.empty((G, self.params.n + 1), np.uint32)
+        elif out.shape != (G, self.params.n + 1) or out.dtype != np.uint32 or \
+                not out.flags["C_CONTIGUOUS"]:
+            raise ValueError(f"out must be a C-contiguous uint32 array of shape {(G, self.params.n + 1)}")
         _check(lib().vsp_hom_gate_batch(self.h, _ptr(kid), _ptr(ins), _ptr(out), G))
         return out
 

@@ -318,17 +318,25 @@ constexpr int kChainWarps = 8;
 // batch, before the remainder wave is launched -- the gate path uses it to start the key
 // switch of the finished tasks on a second stream, where it co-runs with the remainder
 // wave (which holds only half of each SM's warps and registers).
+// before_part(lo, hi): called (host side) before the launch that consumes tasks [lo, hi);
+// when set, whole waves are launched one wave per launch so the host pipeline can upload
+// the inputs of wave k + 1 while wave k runs.
 void launch_br(vsp_ctx* c, const uint32_t* d_tasks, uint32_t* d_trlwe, int T, cudaStream_t st,
-               const std::function<void(int)>& after_full = {})
+               const std::function<void(int)>& after_full = {},
+               const std::function<void(int, int)>& before_part = {})
 {
     if (T == 0)
         return;
     const Params& p = c->p;
+    const long wave8 = 8L * c->sms;
+    const bool split = p.fft && !getenv("VSP_BR_WARPS") && br_warps_for(T, c->sms) == 8 &&
+                       T > wave8 && T > 2 * c->sms;
+    if (before_part && !split)
+        before_part(0, T);
     if (p.fft) {
         // Every task costs the same and one CTA (W tasks) runs per SM, so a partial last
         // wave of W = 8 would cost a full wave: run the whole waves at W = 8 and spread
         // the remainder as one wave of ceil(rem / SMs) tasks per SM (cheaper per wave).
-        const long wave8 = 8L * c->sms;
         const int full = (br_warps_for(T, c->sms) == 8 && T > wave8) ? (int)(T / wave8 * wave8) : 0;
         int forced = 0;
         if (const char* e = getenv("VSP_BR_WARPS"))  // tuning knob (scripts/br_occupancy.py)
@@ -383,7 +391,16 @@ void launch_br(vsp_ctx* c, const uint32_t* d_tasks, uint32_t* d_trlwe, int T, cu
                 launch_part(d_tasks, d_trlwe, T, forced);
                 return;
             }
-            if (full)
+            if (full && before_part) {
+                for (int lo = 0; lo < full; lo += (int)wave8) {
+                    before_part(lo, lo + (int)wave8);
+                    launch_part(d_tasks + (size_t)lo * (p.n + 1), d_trlwe + (size_t)lo * 2 * p.N1,
+                                (int)wave8, 8);
+                }
+                if (T > full)
+                    before_part(full, T);
+            }
+            else if (full)
                 launch_part(d_tasks, d_trlwe, full, 8);
             const int rem = T - full;
             if (full && rem && after_full) {
@@ -567,8 +584,17 @@ GatePlan plan_gates(const int32_t* kinds, size_t G)
     return pl;
 }
 
+// Host buffers of a pipelined call (vsp_hom_gate_batch): inputs are uploaded wave by wave
+// on the copy stream ahead of the blind rotations that need them, and outputs of gates
+// finished early (the whole waves, key-switched under the remainder wave) are downloaded
+// while the rest still computes.
+struct HostIO {
+    const uint32_t* in;
+    uint32_t* out;
+};
+
 void hom_gate_dev(vsp_ctx* c, const int32_t* kinds, const uint32_t* d_in, uint32_t* d_out,
-                  size_t G, cudaStream_t st)
+                  size_t G, cudaStream_t st, const HostIO* io = nullptr)
 {
     require_keys(c);
     if (G == 0)
@@ -586,15 +612,57 @@ void hom_gate_dev(vsp_ctx* c, const int32_t* kinds, const uint32_t* d_in, uint32
                                        cudaMemcpyHostToDevice, st));
     uint32_t* d_tasks = c->tasks.as<uint32_t>((size_t)std::max(pl.T, 1) * (p.n + 1));
     uint32_t* d_trlwe = c->trlwe.as<uint32_t>((size_t)std::max(pl.T, 1) * 2 * p.N1);
-    timed(c, "gate_prep", st, [&] {
-        gate_prep_kernel<<<(unsigned)G, 128, 0, st>>>(d_kinds, d_in, d_gtask, d_tasks, d_out,
-                                                      (int)G, (int)p.n);
-    });
-    VSP_CUDA_CHECK(cudaGetLastError());
-    c->launches++;
+    const size_t w = p.n + 1;
+    // gates [g0, g1): upload (host pipeline) and linear combinations
+    auto prep = [&](size_t g0, size_t g1) {
+        if (g1 <= g0)
+            return;
+        if (io) {
+            c->ensure_copy_stream(1);
+            VSP_CUDA_CHECK(cudaMemcpyAsync(const_cast<uint32_t*>(d_in) + g0 * 3 * w, io->in + g0 * 3 * w,
+                                           (g1 - g0) * 3 * w * 4, cudaMemcpyHostToDevice, c->cstream));
+            VSP_CUDA_CHECK(cudaEventRecord(c->ev_in[0], c->cstream));
+            VSP_CUDA_CHECK(cudaStreamWaitEvent(st, c->ev_in[0], 0));
+        }
+        timed(c, "gate_prep", st, [&] {
+            gate_prep_kernel<<<(unsigned)(g1 - g0), 128, 0, st>>>(
+                d_kinds + g0, d_in + g0 * 3 * w, d_gtask + g0, d_tasks, d_out + g0 * w,
+                (int)(g1 - g0), (int)p.n);
+        });
+        VSP_CUDA_CHECK(cudaGetLastError());
+        c->launches++;
+    };
+    // first gate with a task >= t (NOT gates belong to the preceding task range)
+    auto gate_of_task = [&](int t) -> size_t {
+        size_t g = 0;
+        while (g < G) {
+            const int2 tt = pl.gtask[g];
+            if (tt.x >= 0 && std::max(tt.x, tt.y) >= t)
+                break;
+            g++;
+        }
+        return g;
+    };
+    size_t prepped = 0;
+    std::function<void(int, int)> before_part;
+    if (io) {
+        before_part = [&](int lo, int hi) {
+            const size_t g1 = hi >= pl.T ? G : gate_of_task(hi);
+            prep(prepped, g1);
+            prepped = g1;
+            (void)lo;
+        };
+    }
+    else {
+        prep(0, G);
+        prepped = G;
+    }
+    if (pl.T == 0 && prepped < G)
+        prep(prepped, G);
     const int Gl = (int)pl.glist.size();
     int k1 = 0;  // gates [0, k1) of glist have all their tasks in the whole waves
     bool forked = false;
+    size_t gdone = 0;  // host pipeline: gates [0, gdone) downloaded early
     auto fork_iks = [&](int full) {
         while (k1 < Gl) {
             const int2 t = pl.gtask[pl.glist[k1]];
@@ -610,11 +678,26 @@ void hom_gate_dev(vsp_ctx* c, const int32_t* kinds, const uint32_t* d_in, uint32
         launch_iks(c, d_trlwe, d_gtask, d_glist, k1, d_out, c->astream);
         VSP_CUDA_CHECK(cudaEventRecord(c->ev_join, c->astream));
         forked = true;
+        if (io)  // gates below the first remainder task are final once this key switch is
+            gdone = gate_of_task(full);
     };
-    launch_br(c, d_tasks, d_trlwe, pl.T, st, fork_iks);
+    launch_br(c, d_tasks, d_trlwe, pl.T, st, fork_iks, before_part);
     launch_iks(c, d_trlwe, d_gtask, d_glist + k1, Gl - k1, d_out, st);
     if (forked)
         VSP_CUDA_CHECK(cudaStreamWaitEvent(st, c->ev_join, 0));
+    if (io) {
+        // issued only now: a download into pageable memory blocks the host thread until it
+        // completes, which must not hold back the launches above
+        if (gdone) {
+            VSP_CUDA_CHECK(cudaStreamWaitEvent(c->cstream, c->ev_join, 0));
+            VSP_CUDA_CHECK(cudaMemcpyAsync(io->out, d_out, gdone * w * 4, cudaMemcpyDeviceToHost,
+                                           c->cstream));
+        }
+        VSP_CUDA_CHECK(cudaMemcpyAsync(io->out + gdone * w, d_out + gdone * w, (G - gdone) * w * 4,
+                                       cudaMemcpyDeviceToHost, st));
+        VSP_CUDA_CHECK(cudaStreamSynchronize(c->cstream));
+        VSP_CUDA_CHECK(cudaStreamSynchronize(st));
+    }
 }
 
 
@@ -1171,49 +1254,18 @@ int vsp_hom_gate_batch(vsp_ctx* c, const int32_t* kinds, const uint32_t* in, uin
         const size_t w = c->p.n + 1;
         uint32_t* d_in = c->in.as<uint32_t>(G * 3 * w);
         uint32_t* d_out = c->out.as<uint32_t>(G * w);
-        // Host pipeline: the batch is cut into chunks of one full blind-rotation wave
-        // (8 tasks per SM); chunk k+1's upload and chunk k-1's download run on the copy
-        // stream while chunk k computes, so only the first upload and the last download
-        // are exposed.  Small batches take a single chunk.
-        std::vector<size_t> cuts{0};
-        {
-            const size_t target = (size_t)8 * c->sms;
-            size_t tasks = 0;
-            for (size_t g = 0; g < G; g++) {
-                tasks += kinds[g] == kMux ? 2 : kinds[g] == kNot ? 0 : 1;
-                if (tasks >= target && G - (g + 1) > 0) {
-                    cuts.push_back(g + 1);
-                    tasks = 0;
-                }
-            }
-            cuts.push_back(G);
-        }
-        const size_t nch = cuts.size() - 1;
-        if (nch == 1) {
+        // Host pipeline (HostIO): wave-by-wave uploads ahead of the blind rotations and an
+        // early download of the gates finished under the remainder wave; only the first
+        // wave's upload and the remainder's download are exposed.
+        if (getenv("VSP_HOST_PIPELINE") && atoi(getenv("VSP_HOST_PIPELINE")) == 0) {
             VSP_CUDA_CHECK(cudaMemcpyAsync(d_in, in, G * 3 * w * 4, cudaMemcpyHostToDevice, c->stream));
             hom_gate_dev(c, kinds, d_in, d_out, G, c->stream);
             VSP_CUDA_CHECK(cudaMemcpyAsync(out, d_out, G * w * 4, cudaMemcpyDeviceToHost, c->stream));
             VSP_CUDA_CHECK(cudaStreamSynchronize(c->stream));
             return;
         }
-        c->ensure_copy_stream(nch);
-        for (size_t k = 0; k < nch; k++) {
-            const size_t lo = cuts[k], cnt = cuts[k + 1] - lo;
-            VSP_CUDA_CHECK(cudaMemcpyAsync(d_in + lo * 3 * w, in + lo * 3 * w, cnt * 3 * w * 4,
-                                           cudaMemcpyHostToDevice, c->cstream));
-            VSP_CUDA_CHECK(cudaEventRecord(c->ev_in[k], c->cstream));
-            VSP_CUDA_CHECK(cudaStreamWaitEvent(c->stream, c->ev_in[k], 0));
-            hom_gate_dev(c, kinds + lo, d_in + lo * 3 * w, d_out + lo * w, cnt, c->stream);
-            VSP_CUDA_CHECK(cudaEventRecord(c->ev_done[k], c->stream));
-        }
-        for (size_t k = 0; k < nch; k++) {
-            const size_t lo = cuts[k], cnt = cuts[k + 1] - lo;
-            VSP_CUDA_CHECK(cudaStreamWaitEvent(c->cstream, c->ev_done[k], 0));
-            VSP_CUDA_CHECK(cudaMemcpyAsync(out + lo * w, d_out + lo * w, cnt * w * 4,
-                                           cudaMemcpyDeviceToHost, c->cstream));
-        }
-        VSP_CUDA_CHECK(cudaStreamSynchronize(c->cstream));
-        VSP_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+        const HostIO io{in, out};
+        hom_gate_dev(c, kinds, d_in, d_out, G, c->stream, &io);
     });
 }
 
