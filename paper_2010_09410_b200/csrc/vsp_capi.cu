@@ -461,7 +461,7 @@ void launch_iks(vsp_ctx* c, const uint32_t* d_trlwe, const int2* d_gtask, const 
             constexpr int GT = 16;
             const int tiles = (Gl + GT - 1) / GT;
             int split = 1;
-            while (split < 64 && split * 2 <= (int)p.N1 && tiles * split < 6 * c->sms)
+            while (split < 256 && split * 2 <= (int)p.N1 && tiles * split < 6 * c->sms)
                 split *= 2;
             const dim3 grid(tiles, split);
             const size_t smem = (size_t)(p.N1 / split) * GT * sizeof(uint16_t);
