@@ -310,6 +310,10 @@ void set_br_attr()
     VSP_CUDA_CHECK(cudaFuncSetAttribute(br1024_kernel<W, kBrSlots, kBrBg>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)sizeof(Br1024Smem<W, kBrSlots>)));
+    // full shared-memory carveout: an SM running a partial-width CTA keeps room for the
+    // key-switch CTAs that co-run with the remainder wave
+    VSP_CUDA_CHECK(cudaFuncSetAttribute(br1024_kernel<W, kBrSlots, kBrBg>,
+                                        cudaFuncAttributePreferredSharedMemoryCarveout, 100));
 }
 
 constexpr int kChainWarps = 8;
@@ -446,8 +450,11 @@ int iks_split(int tiles, int N)
     return s;
 }
 
+// gt8: 8 gates per CTA instead of 16 (fewer registers, so more CTAs fit beside a running
+// blind-rotation wave; the key is streamed twice as often).
 void launch_iks(vsp_ctx* c, const uint32_t* d_trlwe, const int2* d_gtask, const int* d_glist,
-                int Gl, uint32_t* d_out, cudaStream_t st, const int* d_seidx = nullptr)
+                int Gl, uint32_t* d_out, cudaStream_t st, const int* d_seidx = nullptr,
+                bool gt8 = false)
 {
     if (Gl == 0)
         return;
@@ -458,24 +465,30 @@ void launch_iks(vsp_ctx* c, const uint32_t* d_trlwe, const int2* d_gtask, const 
                                             p.N1);
         const int kpt4 = (int)((p.n + 1 + 127) / 128);
         if (p.ksBaseBits == 2 && p.ksLen == 8 && kpt4 >= 1 && kpt4 <= 5) {
-            constexpr int GT = 16;
-            const int tiles = (Gl + GT - 1) / GT;
-            int split = 1;
-            while (split < 256 && split * 2 <= (int)p.N1 && tiles * split < 6 * c->sms)
-                split *= 2;
-            const dim3 grid(tiles, split);
-            const size_t smem = (size_t)(p.N1 / split) * GT * sizeof(uint16_t);
+            auto run = [&](auto gtc) {
+                constexpr int GT = decltype(gtc)::value;
+                const int tiles = (Gl + GT - 1) / GT;
+                int split = 1;
+                while (split < 256 && split * 2 <= (int)p.N1 && tiles * split < 6 * c->sms)
+                    split *= 2;
+                const dim3 grid(tiles, split);
+                const size_t smem = (size_t)(p.N1 / split) * GT * sizeof(uint16_t);
 #define VSP_IKS_B2(K)                                                                       \
     iks_b2_kernel<K, GT><<<grid, 128, smem, st>>>(d_trlwe, d_gtask, d_glist, d_seidx, Gl, \
                                                   c->d_ksk, d_out, p.n, p.N1)
-            switch (kpt4) {
-            case 1: VSP_IKS_B2(1); break;
-            case 2: VSP_IKS_B2(2); break;
-            case 3: VSP_IKS_B2(3); break;
-            case 4: VSP_IKS_B2(4); break;
-            default: VSP_IKS_B2(5); break;
-            }
+                switch (kpt4) {
+                case 1: VSP_IKS_B2(1); break;
+                case 2: VSP_IKS_B2(2); break;
+                case 3: VSP_IKS_B2(3); break;
+                case 4: VSP_IKS_B2(4); break;
+                default: VSP_IKS_B2(5); break;
+                }
 #undef VSP_IKS_B2
+            };
+            if (gt8)
+                run(std::integral_constant<int, 8>{});
+            else
+                run(std::integral_constant<int, 16>{});
         }
         else if (p.ksBaseBits == 2 && p.ksLen <= 8) {
             constexpr int GT = 32;
@@ -675,7 +688,8 @@ void hom_gate_dev(vsp_ctx* c, const int32_t* kinds, const uint32_t* d_in, uint32
         c->ensure_aux_stream();
         VSP_CUDA_CHECK(cudaEventRecord(c->ev_fork, st));
         VSP_CUDA_CHECK(cudaStreamWaitEvent(c->astream, c->ev_fork, 0));
-        launch_iks(c, d_trlwe, d_gtask, d_glist, k1, d_out, c->astream);
+        static const bool gt8 = !getenv("VSP_IKS_FORK_GT") || atoi(getenv("VSP_IKS_FORK_GT")) == 8;
+        launch_iks(c, d_trlwe, d_gtask, d_glist, k1, d_out, c->astream, nullptr, gt8);
         VSP_CUDA_CHECK(cudaEventRecord(c->ev_join, c->astream));
         forked = true;
         if (io)  // gates below the first remainder task are final once this key switch is
