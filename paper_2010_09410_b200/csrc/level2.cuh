@@ -298,16 +298,18 @@ __global__ void __launch_bounds__(256) pks_kernel(const uint64_t* __restrict__ a
             acc[g][0] = acc[g][1] = 0;
         for (int i = i0; i < i1; i++) {
             for (int j = 0; j < t; j++) {
-                const uint32_t* base = tab + ((size_t)i * t + j) * perBase * 2 * N1 + k;
+                const uint32_t* base = tab + ((size_t)i * t + j) * perBase * 2 * N1 + (kvalid ? k : 0);
+                // every gate's row load is issued unconditionally (digit 0 and padding
+                // gates read row 0 and are masked) so all GT gathers are in flight at once:
+                // the kernel is bound by the latency of these 8-byte-per-lane row gathers
 #pragma unroll
                 for (int g = 0; g < GT; g++) {
                     const uint32_t d = (pk[(i - i0) * GT + g] >> (nb - (j + 1) * basebits)) & dmask;
-                    if (d && kvalid) {
-                        const uint2 r = __ldg(reinterpret_cast<const uint2*>(
-                            base + (size_t)(d - 1) * 2 * N1));
-                        acc[g][0] += r.x;
-                        acc[g][1] += r.y;
-                    }
+                    const uint32_t m = d ? 0xffffffffu : 0u;
+                    const uint2 r = __ldg(reinterpret_cast<const uint2*>(
+                        base + (size_t)(d ? d - 1 : 0) * 2 * N1));
+                    acc[g][0] += r.x & m;
+                    acc[g][1] += r.y & m;
                 }
             }
         }
