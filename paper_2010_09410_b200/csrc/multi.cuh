@@ -76,7 +76,7 @@ Slice level_slice(size_t G, int world, int rank)
 void hom_gate_level_dev(vsp_ctx* c, const int32_t* kinds, const uint32_t* d_in_all,
                         uint32_t* d_out_all, size_t G, cudaStream_t st)
 {
-    if (c->world <= 1 || G == 0) {
+    if (!c->comm || G == 0) {
         hom_gate_dev(c, kinds, d_in_all, d_out_all, G, st);
         return;
     }

@@ -1943,7 +1943,11 @@ int vsp_attach_comm(vsp_ctx* c, const uint8_t id[128], int rank, int world)
         }
         c->rank = rank;
         c->world = world;
-        if (world > 1) {
+        // world == 1 normally runs without a communicator; VSP_NCCL_SINGLE=1 attaches a
+        // one-rank NCCL communicator anyway so the sharded path (slice, ncclAllGather on the
+        // engine stream, copy-out) can be exercised on a single GPU (tests)
+        const char* single = getenv("VSP_NCCL_SINGLE");
+        if (world > 1 || (single && atoi(single) == 1)) {
             ncclUniqueId uid;
             std::memcpy(&uid, id, sizeof uid);
             ncclComm_t comm;
