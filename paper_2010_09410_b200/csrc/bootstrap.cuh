@@ -11,6 +11,9 @@
 #ifndef VSP_BR_INV2
 #define VSP_BR_INV2 1
 #endif
+#ifndef VSP_BR_Z0
+#define VSP_BR_Z0 1
+#endif
 #ifndef VSP_IKS_PAIR
 #define VSP_IKS_PAIR 0  // 16-way switch compiles to a divergent compare tree: 6.5 vs 3.4 ms
 #endif
@@ -163,7 +166,12 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     // int16 pairs (coefficients p, p+512) so no transform registers are live.
     // lane + 32 j is recomputed from an opaque base every step so the compiler does not
     // hoist 32 loop-invariant indices into (spilled) registers.
+#if VSP_BR_Z0
+    // level-0 digits go straight into the transform registers z; level 1 is parked
+    auto digits = [&](int P, uint32_t bara, double2 (&z)[16]) {
+#else
     auto digits = [&](int P, uint32_t bara) {
+#endif
         const uint32_t* src = acc + P * 1024;
         const uint32_t lo = (uint32_t)lane + (uint32_t)opaque_zero();
         const uint32_t lk = lo - bara;
@@ -177,7 +185,12 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
             const uint32_t d1 = (v1 >> (32 - BG)) + (32768u - kHalf);
             const uint32_t e0 = ((v0 >> (32 - 2 * BG)) & kMask) + (32768u - kHalf);
             const uint32_t e1 = ((v1 >> (32 - 2 * BG)) & kMask) + (32768u - kHalf);
+#if VSP_BR_Z0
+            z[j].x = ob_to_double<15>(d0);
+            z[j].y = ob_to_double<15>(d1);
+#else
             sm.dig[warp][0][j * 32 + lane] = d0 | (d1 << 16);
+#endif
             sm.dig[warp][1][j * 32 + lane] = e0 | (e1 << 16);
         }
     };
@@ -232,11 +245,21 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
 #endif
 #pragma unroll 1
         for (int P = P0; P < 2; P++) {
+#if VSP_BR_Z0
+            double2 z[16];
+            digits(P, bara, z);
+#else
             digits(P, bara);
+#endif
 #pragma unroll 1
             for (int lvl = 0; lvl < 2; lvl++) {
+#if VSP_BR_Z0
+                if (lvl)
+                    load_digits(z, 1);
+#else
                 double2 z[16];
                 load_digits(z, lvl);
+#endif
                 fft512_fwd(z, xbuf, sm.tw2, lane);
                 const int c = c0 + P * 2 + lvl;
                 const int s = c % S;
