@@ -124,6 +124,25 @@ int vsp_ram_cycle(vsp_ctx* ctx, uint32_t v, uint32_t w, uint32_t* ram, const uin
 int vsp_rom_read(vsp_ctx* ctx, uint32_t depth_bytes, const uint32_t* luts, uint32_t nluts,
                  const uint32_t* addr, uint32_t vrom, uint32_t* out);
 
+/* Device-resident ramCycle / romRead (same arguments as device pointers, asynchronous on
+ * `stream`, a cudaStream_t): the RAM image stays in HBM across cycles, as in the netlist
+ * runner.  Replace the same reference calls (mem.cpp:122-135, :137-177). */
+int vsp_ram_cycle_dev(vsp_ctx* ctx, uint32_t v, uint32_t w, uint32_t* d_ram,
+                      const uint32_t* d_addr, const uint32_t* d_wflag, const uint32_t* d_wdata,
+                      uint32_t* d_readout, void* stream);
+int vsp_rom_read_dev(vsp_ctx* ctx, uint32_t depth_bytes, const uint32_t* d_luts, uint32_t nluts,
+                     const uint32_t* d_addr, uint32_t vrom, uint32_t* d_out, void* stream);
+
+/* One access of a ROM port and a RAM port together, as the processor issues them each
+ * cycle (the netlist runner's path for two ports in one level, Evaluator::evaluateCycle
+ * engine.hpp:263-351 with engine.cpp:133-148): both ports' address circuit bootstraps run
+ * as one batch, then romRead and ramCycle proceed; results equal the separate calls. */
+int vsp_mem_ports_dev(vsp_ctx* ctx, uint32_t depth_bytes, const uint32_t* d_luts, uint32_t nluts,
+                      const uint32_t* d_rom_addr, uint32_t vrom, uint32_t* d_rom_out,
+                      uint32_t v, uint32_t w, uint32_t* d_ram, const uint32_t* d_ram_addr,
+                      const uint32_t* d_wflag, const uint32_t* d_wdata, uint32_t* d_readout,
+                      void* stream);
+
 /* blindRotate<uint64_t> (ops.cpp:713-742) with test vector (0, h[t]/2 ...): T level-0
  * TLWEs -> T level-2 TRLWE accumulators (2 x N2 u64).  Exposed for parity tests of the
  * circuit-bootstrapping inner loop. */

@@ -51,6 +51,10 @@ def lib() -> ctypes.CDLL:
         L.vsp_upload_keys.argtypes = [vp, vp, vp, vp, vp, vp, ctypes.c_int]
         L.vsp_hom_gate_batch.argtypes = [vp, vp, vp, vp, sz]
         L.vsp_hom_gate_batch_dev.argtypes = [vp, vp, vp, vp, sz, vp]
+        L.vsp_ram_cycle_dev.argtypes = [vp, u32, u32, vp, vp, vp, vp, vp, vp]
+        L.vsp_rom_read_dev.argtypes = [vp, u32, vp, u32, vp, u32, vp, vp]
+        L.vsp_mem_ports_dev.argtypes = [vp, u32, vp, u32, vp, u32, vp, u32, u32, vp, vp, vp, vp,
+                                        vp, vp]
         L.vsp_bootstrap_to_trlwe_batch.argtypes = [vp, vp, vp, sz]
         L.vsp_gate_bootstrap_batch.argtypes = [vp, vp, vp, sz]
         L.vsp_identity_key_switch_batch.argtypes = [vp, vp, vp, sz]
@@ -430,6 +434,30 @@ class Engine:
         _check(lib().vsp_rom_read(self.h, depth_bytes, _ptr(luts), luts.shape[0], _ptr(a),
                                   a.shape[0], _ptr(out)))
         return out
+
+    def ram_cycle_dev(self, d_ram: int, v: int, w: int, d_addr: int, d_wflag: int,
+                      d_wdata: int, d_readout: int, stream: int = 0):
+        """Device-resident ramCycle: d_ram (w<<v, 2*N1) u32 updated in place in HBM,
+        d_readout (w, n+1); asynchronous on `stream`."""
+        _check(lib().vsp_ram_cycle_dev(self.h, v, w, ctypes.c_void_p(d_ram), ctypes.c_void_p(d_addr),
+                                       ctypes.c_void_p(d_wflag), ctypes.c_void_p(d_wdata),
+                                       ctypes.c_void_p(d_readout), ctypes.c_void_p(stream)))
+
+    def rom_read_dev(self, d_luts: int, nluts: int, depth_bytes: int, d_addr: int, vrom: int,
+                     d_out: int, stream: int = 0):
+        """Device-resident addressToTrgsw + romRead: 32 TLWEs into d_out."""
+        _check(lib().vsp_rom_read_dev(self.h, depth_bytes, ctypes.c_void_p(d_luts), nluts,
+                                      ctypes.c_void_p(d_addr), vrom, ctypes.c_void_p(d_out),
+                                      ctypes.c_void_p(stream)))
+
+    def mem_ports_dev(self, d_luts: int, nluts: int, depth_bytes: int, d_rom_addr: int,
+                      vrom: int, d_rom_out: int, d_ram: int, v: int, w: int, d_ram_addr: int,
+                      d_wflag: int, d_wdata: int, d_readout: int, stream: int = 0):
+        """One ROM read + one RAM cycle with batched address bootstraps (device buffers)."""
+        c = ctypes.c_void_p
+        _check(lib().vsp_mem_ports_dev(self.h, depth_bytes, c(d_luts), nluts, c(d_rom_addr), vrom,
+                                       c(d_rom_out), v, w, c(d_ram), c(d_ram_addr), c(d_wflag),
+                                       c(d_wdata), c(d_readout), c(stream)))
 
     def blind_rotate_lvl2(self, cts: np.ndarray, h) -> np.ndarray:
         p = self.params

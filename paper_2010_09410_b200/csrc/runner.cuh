@@ -64,7 +64,7 @@ struct vsp_netlist {
     std::vector<std::vector<int>> level_gates, level_mem;
     std::vector<int> const_cells;
     // device state
-    DevBuf values, dff, gin, gout, nets_buf, inputs_store, cbraw;
+    DevBuf values, dff, gin, gout, nets_buf, inputs_store;
     std::vector<int> input_nets;     // nets driven by module inputs (setInput targets)
     std::vector<uint8_t> is_input;   // net -> is module input
     std::vector<int> dff_q, dff_d;   // per DFF: output net (Q), input net (D)
@@ -206,15 +206,10 @@ void run_mem_pair(vsp_netlist* nl, const std::vector<int>& cells, uint32_t* vals
     gather_tlwe_kernel<<<(unsigned)ins.size(), 128, 0, st>>>(nl->nets_buf.as<int>(0), (int)ins.size(),
                                                               vals, gin, (int)c->p.n);
     c->launches++;
-    // ROM address (vrom) and RAM address (v) are contiguous in gin
-    const size_t tw = trgsw_words(c->p);
-    uint32_t* raw = nl->cbraw.as<uint32_t>((size_t)(vrom + v) * tw);
-    cb_batch(c, gin, vrom + v, raw, st);
-    rom_read_dev(c, nl->rom.as<uint32_t>(0), (int)nl->rom_nluts, nl->rom_depth, gin, vrom, gout, st,
-                 raw);
-    const uint32_t* g = gin + (size_t)vrom * n1;  // addr[v], wdata[w], wflag
-    ram_cycle_dev(c, nl->ram.as<uint32_t>(0), v, w, g, g + (size_t)(v + w) * n1, g + (size_t)v * n1,
-                  gout + (size_t)nrom_out * n1, st, raw + (size_t)vrom * tw);
+    const uint32_t* g = gin + (size_t)vrom * n1;  // RAM: addr[v], wdata[w], wflag
+    mem_pair_dev(c, nl->rom.as<uint32_t>(0), (int)nl->rom_nluts, nl->rom_depth, gin, vrom, gout,
+                 nl->ram.as<uint32_t>(0), v, w, g, g + (size_t)(v + w) * n1, g + (size_t)v * n1,
+                 gout + (size_t)nrom_out * n1, st);
     upload_ints(c, nl->nets_buf, outs, st);
     scatter_tlwe_kernel<<<(unsigned)outs.size(), 128, 0, st>>>(nl->nets_buf.as<int>(0), (int)outs.size(),
                                                                 gout, vals, (int)c->p.n);

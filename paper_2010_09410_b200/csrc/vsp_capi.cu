@@ -180,7 +180,7 @@ struct vsp_ctx {
     DevBuf tasks, trlwe, in, out, kinds, gtask, glist;
     // memory-path scratch
     DevBuf acc2, hv, rows, cbraw, selraw, selfd, chains, layerA, layerB, ram, aux, aux2, seidx,
-        pairs;
+        pairs, ramio, romio, cbraw2, cbaddr;
     uint64_t counters[5] = {0, 0, 0, 0, 0};
     uint64_t launches = 0;
     // multi-GPU (multi.cuh): NCCL communicator over the ranks, level slices staged here
@@ -1029,6 +1029,28 @@ void rom_read_dev(vsp_ctx* c, const uint32_t* d_luts, int nluts, uint32_t depth_
     launch_iks(c, acc, d_gt, d_gl, 32, d_out, st, d_se);
 }
 
+// One access of a ROM port and a RAM port together (the processor drives both every cycle):
+// the address circuit bootstraps of both ports (vrom + v TLWEs) run as ONE batched launch
+// sequence, then each port continues on its own.  The ports are independent, so the results
+// equal separate romRead + ramCycle calls.  d_rom_addr and d_ram_addr may be anywhere;
+// they are gathered into one contiguous address batch.
+void mem_pair_dev(vsp_ctx* c, const uint32_t* d_luts, int nluts, uint32_t depth_bytes,
+                  const uint32_t* d_rom_addr, int vrom, uint32_t* d_rom_out, uint32_t* d_ram,
+                  int v, int w, const uint32_t* d_ram_addr, const uint32_t* d_wflag,
+                  const uint32_t* d_wdata, uint32_t* d_readout, cudaStream_t st)
+{
+    require_cb(c);
+    const size_t n1 = c->p.n + 1, tw = trgsw_words(c->p);
+    uint32_t* addr = c->cbaddr.as<uint32_t>((size_t)(vrom + v) * n1);
+    VSP_CUDA_CHECK(cudaMemcpyAsync(addr, d_rom_addr, (size_t)vrom * n1 * 4, cudaMemcpyDeviceToDevice, st));
+    VSP_CUDA_CHECK(cudaMemcpyAsync(addr + (size_t)vrom * n1, d_ram_addr, (size_t)v * n1 * 4,
+                                   cudaMemcpyDeviceToDevice, st));
+    uint32_t* raw = c->cbraw2.as<uint32_t>((size_t)(vrom + v) * tw);
+    cb_batch(c, addr, vrom + v, raw, st);
+    rom_read_dev(c, d_luts, nluts, depth_bytes, d_rom_addr, vrom, d_rom_out, st, raw);
+    ram_cycle_dev(c, d_ram, v, w, d_ram_addr, d_wflag, d_wdata, d_readout, st, raw + (size_t)vrom * tw);
+}
+
 }  // namespace
 
 #include "multi.cuh"
@@ -1128,7 +1150,8 @@ void vsp_destroy(vsp_ctx* c)
             cudaFree(q);
     for (DevBuf* b : {&c->tasks, &c->trlwe, &c->in, &c->out, &c->kinds, &c->gtask, &c->glist,
                       &c->acc2, &c->hv, &c->rows, &c->cbraw, &c->selraw, &c->selfd, &c->chains,
-                      &c->layerA, &c->layerB, &c->ram, &c->aux, &c->aux2, &c->seidx, &c->pairs})
+                      &c->layerA, &c->layerB, &c->ram, &c->aux, &c->aux2, &c->seidx, &c->pairs,
+                      &c->ramio, &c->romio, &c->cbraw2, &c->cbaddr})
         b->release();
     for (void* q : {(void*)c->d_bk2fd, (void*)c->d_tv2[0], (void*)c->d_tv2[1]})
         if (q)
@@ -1487,8 +1510,7 @@ int vsp_ram_cycle(vsp_ctx* c, uint32_t v, uint32_t w, uint32_t* ram, const uint3
         const size_t n1 = p.n + 1, cw = 2 * (size_t)p.N1, cells = (size_t)w << v;
         if (v == 0 || w == 0)
             throw std::invalid_argument("ramCycle: address width mismatch");
-        DevBuf ramb;
-        uint32_t* d_ram = ramb.as<uint32_t>(cells * cw);
+        uint32_t* d_ram = c->ramio.as<uint32_t>(cells * cw);
         uint32_t* d_io = c->in.as<uint32_t>((v + 1 + 2 * (size_t)w) * n1);
         uint32_t* d_addr = d_io;
         uint32_t* d_wflag = d_io + v * n1;
@@ -1502,7 +1524,50 @@ int vsp_ram_cycle(vsp_ctx* c, uint32_t v, uint32_t w, uint32_t* ram, const uint3
         VSP_CUDA_CHECK(cudaMemcpyAsync(readout, d_ro, w * n1 * 4, cudaMemcpyDeviceToHost, c->stream));
         VSP_CUDA_CHECK(cudaMemcpyAsync(ram, d_ram, cells * cw * 4, cudaMemcpyDeviceToHost, c->stream));
         VSP_CUDA_CHECK(cudaStreamSynchronize(c->stream));
-        ramb.release();
+    });
+}
+
+// Device-resident variants (RAM image / ROM LUTs and ciphertexts in HBM, asynchronous on
+// `stream`): the netlist runner's memory-port path, exposed for device pipelines.
+int vsp_ram_cycle_dev(vsp_ctx* c, uint32_t v, uint32_t w, uint32_t* d_ram, const uint32_t* d_addr,
+                      const uint32_t* d_wflag, const uint32_t* d_wdata, uint32_t* d_readout,
+                      void* stream)
+{
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(c->mu);
+        c->set_device();
+        if (v == 0 || w == 0)
+            throw std::invalid_argument("ramCycle: address width mismatch");
+        ram_cycle_dev(c, d_ram, (int)v, (int)w, d_addr, d_wflag, d_wdata, d_readout,
+                      static_cast<cudaStream_t>(stream));
+    });
+}
+
+int vsp_mem_ports_dev(vsp_ctx* c, uint32_t depth_bytes, const uint32_t* d_luts, uint32_t nluts,
+                      const uint32_t* d_rom_addr, uint32_t vrom, uint32_t* d_rom_out,
+                      uint32_t v, uint32_t w, uint32_t* d_ram, const uint32_t* d_ram_addr,
+                      const uint32_t* d_wflag, const uint32_t* d_wdata, uint32_t* d_readout,
+                      void* stream)
+{
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(c->mu);
+        c->set_device();
+        if (v == 0 || w == 0)
+            throw std::invalid_argument("ramCycle: address width mismatch");
+        mem_pair_dev(c, d_luts, (int)nluts, depth_bytes, d_rom_addr, (int)vrom, d_rom_out, d_ram,
+                     (int)v, (int)w, d_ram_addr, d_wflag, d_wdata, d_readout,
+                     static_cast<cudaStream_t>(stream));
+    });
+}
+
+int vsp_rom_read_dev(vsp_ctx* c, uint32_t depth_bytes, const uint32_t* d_luts, uint32_t nluts,
+                     const uint32_t* d_addr, uint32_t vrom, uint32_t* d_out, void* stream)
+{
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(c->mu);
+        c->set_device();
+        rom_read_dev(c, d_luts, (int)nluts, depth_bytes, d_addr, (int)vrom, d_out,
+                     static_cast<cudaStream_t>(stream));
     });
 }
 
@@ -1514,8 +1579,7 @@ int vsp_rom_read(vsp_ctx* c, uint32_t depth_bytes, const uint32_t* luts, uint32_
         c->set_device();
         const Params& p = c->p;
         const size_t n1 = p.n + 1, cw = 2 * (size_t)p.N1;
-        DevBuf lb;
-        uint32_t* d_luts = lb.as<uint32_t>(std::max<size_t>(nluts, 1) * cw);
+        uint32_t* d_luts = c->romio.as<uint32_t>(std::max<size_t>(nluts, 1) * cw);
         uint32_t* d_io = c->in.as<uint32_t>((vrom + 32) * n1);
         VSP_CUDA_CHECK(cudaMemcpyAsync(d_luts, luts, nluts * cw * 4, cudaMemcpyHostToDevice, c->stream));
         VSP_CUDA_CHECK(cudaMemcpyAsync(d_io, addr, vrom * n1 * 4, cudaMemcpyHostToDevice, c->stream));
@@ -1524,7 +1588,6 @@ int vsp_rom_read(vsp_ctx* c, uint32_t depth_bytes, const uint32_t* luts, uint32_
         VSP_CUDA_CHECK(cudaMemcpyAsync(out, d_io + vrom * n1, 32 * n1 * 4, cudaMemcpyDeviceToHost,
                                        c->stream));
         VSP_CUDA_CHECK(cudaStreamSynchronize(c->stream));
-        lb.release();
     });
 }
 
@@ -1647,7 +1710,7 @@ void vsp_netlist_destroy(vsp_netlist* nl)
     cudaSetDevice(nl->ctx->device);
     cudaStreamSynchronize(nl->ctx->stream);
     for (DevBuf* b : {&nl->values, &nl->dff, &nl->gin, &nl->gout, &nl->nets_buf, &nl->inputs_store,
-                      &nl->ram, &nl->rom, &nl->cbraw})
+                      &nl->ram, &nl->rom})
         b->release();
     delete nl;
 }

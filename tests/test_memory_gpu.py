@@ -199,3 +199,38 @@ def test_tfhe80_ram_and_rom_functional(prod_cb):
     for blk in (0, 45, 127):
         got = e.rom_read(luts, 512, enc_word(o, blk, 7))
         assert dec_word(o, got) == int.from_bytes(bytes(img[4 * blk:4 * blk + 4]), "little")
+
+
+def test_mem_ports_dev_equals_separate_calls_and_oracle(det):
+    """vsp_mem_ports_dev (ROM read + RAM cycle with one batched address bootstrap, RAM in
+    HBM) == the oracle's romRead and ramCycle, bit for bit, and the device-resident RAM
+    evolves like the host-API RAM over consecutive accesses."""
+    import torch
+    e, o = det
+    rng = np.random.default_rng(8)
+    v, w = 3, 4
+    words = [int(x) for x in rng.integers(0, 1 << w, 1 << v)]
+    ram = o.encrypt_ram(words_to_image(words, v, w), v, w)
+    img = rng.integers(0, 256, 512).astype(np.uint8)
+    luts = o.encrypt_rom(img)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.uint32).view(np.int32)).cuda()
+    d_ram, d_luts = t(ram), t(luts)
+    n1 = o.n + 1
+    ram_o = ram
+    for A, wf, X, blk in [(5, 1, 9, 77), (2, 0, 3, 0), (5, 1, 1, 127)]:
+        addr, f, d, raddr = enc_word(o, A, v), o.encrypt(wf), enc_word(o, X, w), enc_word(o, blk, 7)
+        d_ro = torch.empty((w, n1), dtype=torch.int32, device="cuda")
+        d_rout = torch.empty((32, n1), dtype=torch.int32, device="cuda")
+        keep = [t(raddr), t(addr), t(f), t(d)]  # live until the asynchronous call is done
+        e.mem_ports_dev(d_luts.data_ptr(), luts.shape[0], 512, keep[0].data_ptr(), 7,
+                        d_rout.data_ptr(), d_ram.data_ptr(), v, w, keep[1].data_ptr(),
+                        keep[2].data_ptr(), keep[3].data_ptr(), d_ro.data_ptr())
+        torch.cuda.synchronize()
+        rom_o = o.rom_read(luts, 512, raddr)
+        ro_o, ram_o = o.ram_cycle(ram_o, v, w, addr, f, d)
+        assert np.array_equal(d_rout.cpu().numpy().view(np.uint32), rom_o)
+        assert np.array_equal(d_ro.cpu().numpy().view(np.uint32), ro_o)
+        assert np.array_equal(d_ram.cpu().numpy().view(np.uint32), ram_o)
+        assert dec_word(o, ro_o) == words[A]
+        if wf:
+            words[A] = X
