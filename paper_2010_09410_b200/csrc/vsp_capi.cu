@@ -944,6 +944,41 @@ void ram_cycle_dev(vsp_ctx* c, uint32_t* d_ram, int v, int w, const uint32_t* d_
     }
     run_chains(c, tasks, st);
     uint32_t* lw = c->tasks.as<uint32_t>(cells * n1);
+    // noise refresh: cell = BR(IKS(SE(t, 0))).  Arranged so the key switch of the
+    // whole-wave cells runs UNDER the remainder wave (which holds half of each SM): key
+    // switch the remainder cells, then their blind rotations (high-priority stream) beside
+    // the whole-wave cells' key switch (low-priority stream), then the whole waves.
+    const long wave8 = 8L * c->sms;
+    const int T = (int)cells;
+    const int full = (p.fft && !getenv("VSP_BR_WARPS") && br_warps_for(T, c->sms) == 8 &&
+                      T > wave8 && T > 2 * c->sms) ? (int)(T / wave8 * wave8) : 0;
+    const int rem = T - full;
+    if (full && rem) {
+        std::vector<int2> gt(full);
+        std::vector<int> gl(full);
+        for (int i = 0; i < full; i++) {
+            gt[i] = make_int2(i, -1);
+            gl[i] = i;
+        }
+        int2* d_gt = c->gtask.as<int2>(full);
+        int* d_gl = c->glist.as<int>(full);
+        VSP_CUDA_CHECK(cudaMemcpyAsync(d_gt, gt.data(), full * sizeof(int2), cudaMemcpyHostToDevice, st));
+        VSP_CUDA_CHECK(cudaMemcpyAsync(d_gl, gl.data(), full * sizeof(int), cudaMemcpyHostToDevice, st));
+        // identity maps relative to each part's base pointers
+        launch_iks(c, chain_out + (size_t)full * cw, d_gt, d_gl, rem, lw + (size_t)full * n1, st);
+        c->ensure_aux_stream();
+        VSP_CUDA_CHECK(cudaEventRecord(c->ev_fork, st));
+        VSP_CUDA_CHECK(cudaStreamWaitEvent(c->hstream, c->ev_fork, 0));
+        VSP_CUDA_CHECK(cudaStreamWaitEvent(c->astream, c->ev_fork, 0));
+        launch_br(c, lw + (size_t)full * n1, d_ram + (size_t)full * cw, rem, c->hstream);
+        VSP_CUDA_CHECK(cudaEventRecord(c->ev_rem, c->hstream));
+        launch_iks(c, chain_out, d_gt, d_gl, full, lw, c->astream, nullptr, true);
+        VSP_CUDA_CHECK(cudaEventRecord(c->ev_join, c->astream));
+        VSP_CUDA_CHECK(cudaStreamWaitEvent(st, c->ev_rem, 0));
+        VSP_CUDA_CHECK(cudaStreamWaitEvent(st, c->ev_join, 0));
+        launch_br(c, lw, d_ram, full, st);
+        return;
+    }
     iks_of_trlwes(c, chain_out, (int)cells, nullptr, lw, st);
     launch_br(c, lw, d_ram, (int)cells, st);
 }

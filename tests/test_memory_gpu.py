@@ -234,3 +234,20 @@ def test_mem_ports_dev_equals_separate_calls_and_oracle(det):
         assert dec_word(o, ro_o) == words[A]
         if wf:
             words[A] = X
+
+
+def test_tfhe80_full_size_ram_cycles(prod_cb):
+    """BASELINE configs[1] geometry (v=8, w=16: 4,096 cells) on the FFT path, where the
+    write unit key-switches the whole-wave cells under the remainder blind-rotation wave:
+    two cycles against the plain model, every cell of the decrypted image checked."""
+    e, o, k, p = prod_cb
+    rng = np.random.default_rng(12)
+    v, w = 8, 16
+    model = [int(x) for x in rng.integers(0, 1 << w, 1 << v)]
+    ram = o.encrypt_ram(words_to_image(model, v, w), v, w)
+    for A, wf, X in [(200, 1, 0xBEEF), (200, 0, 0x1234), (17, 1, 0x0F0F)]:
+        ro, ram = e.ram_cycle(ram, v, w, enc_word(o, A, v), o.encrypt(wf), enc_word(o, X, w))
+        assert dec_word(o, ro) == model[A]
+        if wf:
+            model[A] = X
+    assert np.array_equal(o.decrypt_ram(ram, v, w), words_to_image(model, v, w))
