@@ -15,6 +15,8 @@
 // followed by two 512-point warp transforms (fft512 ROOT 1 / ROOT 2).
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include "fft512.cuh"
 
 namespace vsp {
@@ -241,6 +243,187 @@ __global__ void __launch_bounds__(256, 1)
     uint64_t* dst = out + (size_t)blockIdx.x * 4096;
     for (int q = tid; q < 4096; q += blockDim.x)
         dst[q] = (&sm.acc[0][0])[q];
+}
+
+// ---------------------------------------------------------------------------
+// Level-2 blind rotation on a CLUSTER of two CTAs per task (thread-block cluster, DSMEM).
+// CTA P of the pair owns accumulator polynomial P (0: a, 1: b) of the task:
+//   A. its four gadget rows (P, L), L < 4, digits + split + forward transforms, one
+//      (row, branch) per warp;
+//   B. partial MAC over its own four rows for all four outputs (a_lo, a_hi, b_lo, b_hi):
+//      only half of bk2[i] (rows 4P..4P+3, 256 KiB) streams through this SM; the two
+//      outputs of the OTHER polynomial go straight into the peer CTA's shared memory
+//      (st.shared::cluster, double-buffered by step parity), one cluster barrier per step;
+//   C. own outputs = rows 0..3 partial + rows 4..7 partial (the same association on both
+//      CTAs), inverse transforms split over warp pairs (fft512_inv_pair);
+//   D. inverse split stage, exact rounding, lo/hi recombination into acc[P].
+// Same arithmetic per output as br2_kernel up to the association of the row sums, and each
+// coefficient rounds back to the same exact integer.
+constexpr int kBr2cRegion = kFftXbufStride;
+
+struct Br2cSmem {
+    uint64_t acc[2048];                 // this CTA's polynomial
+    double2 reg[8][kBr2cRegion];        // (row L, branch b) -> 2L + b; MAC outputs (2k + b)
+    double2 part[2][4][512];            // peer's partial outputs, by step parity
+    double2 tw2[2][kTw2Entries * 32];
+};
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+    br2c_kernel(const uint32_t* __restrict__ tasks, int ninputs, const uint64_t* __restrict__ hv,
+                const double2* __restrict__ bk2fd, const double2* __restrict__ tw2g,
+                uint64_t* __restrict__ out, int n, int bgbits)
+{
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    Br2cSmem& sm = *reinterpret_cast<Br2cSmem*>(smem_raw);
+    const int P = (int)cluster.block_rank();
+    const int task = blockIdx.x >> 1;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t* lwe = tasks + (size_t)(task % ninputs) * (n + 1);
+    Br2cSmem* peer = cluster.map_shared_rank(&sm, P ^ 1);
+    for (int i = tid; i < 2 * kTw2Entries * 32; i += blockDim.x)
+        sm.tw2[i / (kTw2Entries * 32)][i % (kTw2Entries * 32)] = tw2g[kTw2Entries * 32 + i];
+    {
+        const uint64_t h2 = hv[task] / 2;
+        const uint32_t rot = (4096u - mod_switch_2n(lwe[n], 12)) & 4095u;
+        for (int q = tid; q < 2048; q += blockDim.x) {
+            uint64_t val = 0;
+            if (P == 1) {
+                if (rot < 2048)
+                    val = ((uint32_t)q < rot) ? (0ull - h2) : h2;
+                else
+                    val = ((uint32_t)q < rot - 2048) ? h2 : (0ull - h2);
+            }
+            sm.acc[q] = val;
+        }
+    }
+    cluster.sync();  // both CTAs initialised before any remote store
+    const uint64_t half = 1ull << (bgbits - 1);
+    const uint64_t mask = (1ull << bgbits) - 1;
+    uint64_t offset = 0;
+    for (int i = 1; i <= 4; i++)
+        offset += half << (64 - i * bgbits);
+
+    uint32_t a_next = lwe[0];
+#pragma unroll 1
+    for (int i = 0; i < n; i++) {
+        const uint32_t bara = mod_switch_2n(a_next, 12);
+        a_next = lwe[i + 1];
+        const int buf = i & 1;
+        // ---- A: warp = (row L, branch b)
+        {
+            const int L = warp & 3, b = warp >> 2;
+            const int sh = 64 - (L + 1) * bgbits;
+            auto digit = [&](uint32_t q) -> double {
+                const uint32_t idx = (q - bara) & 4095u;
+                const uint64_t r = idx < 2048 ? sm.acc[idx] : 0ull - sm.acc[idx - 2048];
+                const uint64_t v = r - sm.acc[q] + offset;
+                return (double)(int32_t)(int64_t)(((v >> sh) & mask) - half);
+            };
+            double2 z[16];
+#pragma unroll
+            for (int j = 0; j < 16; j++) {
+                const uint32_t p = lane + 32 * j;
+                const double2 u = make_double2(digit(p), digit(p + 1024));
+                const double2 v = make_double2(digit(p + 512), digit(p + 1536));
+                z[j] = split_fwd(u, v, b);
+            }
+            double2* rg = sm.reg[2 * L + b];
+            if (b == 0)
+                fft512_fwd<1>(z, rg, sm.tw2[0], lane);
+            else
+                fft512_fwd<2>(z, rg, sm.tw2[1], lane);
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < 16; j++)
+                rg[j * 32 + lane] = z[j];
+        }
+        __syncthreads();
+        // ---- B: partial MAC over rows 4P..4P+3 for the four outputs
+        {
+            const double2* K = bk2fd + (size_t)i * 8 * 4 * 1024 + (size_t)(4 * P) * 4 * 1024;
+#pragma unroll 1
+            for (int m = 0; m < 4; m++) {
+                const int f = tid + 256 * m;
+                const int b = f >> 9, s = f & 511;
+                double2 o[4];
+#pragma unroll
+                for (int q = 0; q < 4; q++)
+                    o[q] = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int L = 0; L < 4; L++) {
+                    const double2 d = sm.reg[2 * L + b][s];
+#pragma unroll
+                    for (int q = 0; q < 4; q++) {
+                        const double2 k = __ldg(K + ((size_t)(L * 4 + q)) * 1024 + f);
+                        o[q].x = fma(d.x, k.x, fma(-d.y, k.y, o[q].x));
+                        o[q].y = fma(d.x, k.y, fma(d.y, k.x, o[q].y));
+                    }
+                }
+                // own outputs q = 2P + k stay (in place of this thread's own Z slots), the
+                // other polynomial's go to the peer
+#pragma unroll
+                for (int k = 0; k < 2; k++) {
+                    sm.reg[2 * k + b][s] = o[2 * P + k];
+                    peer->part[buf][2 * k + b][s] = o[2 * (P ^ 1) + k];
+                }
+            }
+        }
+        cluster.sync();  // partials exchanged (and the peer is done with last step's buffer)
+        // ---- C: own outputs, inverse transforms on warp pairs (region g = 2k + b)
+        {
+            const int g = warp & 3, h = warp >> 2, b = g & 1;
+            double2* rg = sm.reg[g];
+            const int Lv = 16 * h + (lane & 15), e = lane >> 4;
+            double2 u[8];
+#pragma unroll
+            for (int t = 0; t < 8; t++) {
+                const int q = (2 * t + e) * 32 + Lv;
+                const double2 mine = rg[q], oth = sm.part[buf][g][q];
+                // rows 0..3 first, then rows 4..7, on both CTAs
+                u[t] = P == 0 ? make_double2(mine.x + oth.x, mine.y + oth.y)
+                              : make_double2(oth.x + mine.x, oth.y + mine.y);
+            }
+            asm volatile("bar.sync %0, 64;" ::"r"(1 + g) : "memory");  // inputs read
+            if (b == 0)
+                fft512_inv_pair<1>(u, rg, sm.tw2[0], lane, h, 1 + g);
+            else
+                fft512_inv_pair<2>(u, rg, sm.tw2[1], lane, h, 1 + g);
+            asm volatile("bar.sync %0, 64;" ::"r"(1 + g) : "memory");  // transpose reads done
+#pragma unroll
+            for (int t = 0; t < 8; t++)
+                rg[Lv + 32 * (t + 8 * e)] = u[t];
+        }
+        __syncthreads();
+        // ---- D: inverse split stage, exact rounding, lo/hi recombination into acc[P]
+        {
+            const double c = 0.70710678118654752440;
+#pragma unroll 1
+            for (int w = 0; w < 2; w++) {
+                const int p = tid + 256 * w;
+                int64_t part[2][4];
+#pragma unroll
+                for (int hh = 0; hh < 2; hh++) {
+                    const double2 A = sm.reg[2 * hh][p], B = sm.reg[2 * hh + 1][p];
+                    const double2 uu = make_double2(A.x + B.x, A.y + B.y);
+                    const double dx = A.x - B.x, dy = A.y - B.y;
+                    const double2 vv = make_double2(c * (dx + dy), c * (dy - dx));
+                    part[hh][0] = __double2ll_rn(uu.x);  // coefficient p
+                    part[hh][1] = __double2ll_rn(vv.x);  // p + 512
+                    part[hh][2] = __double2ll_rn(uu.y);  // p + 1024
+                    part[hh][3] = __double2ll_rn(vv.y);  // p + 1536
+                }
+#pragma unroll
+                for (int e4 = 0; e4 < 4; e4++)
+                    sm.acc[p + 512 * e4] += (uint64_t)part[0][e4] + ((uint64_t)part[1][e4] << 32);
+            }
+        }
+        __syncthreads();
+    }
+    uint64_t* dst = out + (size_t)task * 4096 + (size_t)P * 2048;
+    for (int q = tid; q < 2048; q += blockDim.x)
+        dst[q] = sm.acc[q];
 }
 
 // ---------------------------------------------------------------------------

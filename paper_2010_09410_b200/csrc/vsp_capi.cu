@@ -318,6 +318,22 @@ void set_br_attr()
 
 constexpr int kChainWarps = 8;
 
+// Level-2 blind rotation of T tasks: the two-CTA cluster kernel (one SM per accumulator
+// polynomial, br2c_kernel) unless VSP_BR2_CLUSTER=0 selects the one-CTA br2_kernel.
+void launch_br2(vsp_ctx* c, const uint32_t* d_lwe, int ninputs, const uint64_t* d_hv, int T,
+                uint64_t* d_acc, cudaStream_t st)
+{
+    static const bool single = getenv("VSP_BR2_CLUSTER") && atoi(getenv("VSP_BR2_CLUSTER")) == 0;
+    if (single)
+        br2_kernel<<<T, 256, sizeof(Br2Smem), st>>>(d_lwe, ninputs, d_hv, c->d_bk2fd, c->d_tw2,
+                                                     d_acc, (int)c->p.n, (int)c->p.Bg2Bits);
+    else
+        br2c_kernel<<<2 * T, 256, sizeof(Br2cSmem), st>>>(d_lwe, ninputs, d_hv, c->d_bk2fd,
+                                                            c->d_tw2, d_acc, (int)c->p.n,
+                                                            (int)c->p.Bg2Bits);
+    VSP_CUDA_CHECK(cudaGetLastError());
+}
+
 // after_full(full): called (host side) right after the whole-wave launch of a split
 // batch, before the remainder wave is launched -- the gate path uses it to start the key
 // switch of the finished tasks on a second stream, where it co-runs with the remainder
@@ -545,6 +561,8 @@ void configure_kernels()
     set_br_attr<1>();
     VSP_CUDA_CHECK(cudaFuncSetAttribute(br2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)sizeof(Br2Smem)));
+    VSP_CUDA_CHECK(cudaFuncSetAttribute(br2c_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)sizeof(Br2cSmem)));
     VSP_CUDA_CHECK(cudaFuncSetAttribute(cmux_chain1024_kernel<kChainWarps>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)sizeof(Chain1024Smem<kChainWarps>)));
@@ -752,8 +770,7 @@ void cb_batch(vsp_ctx* c, const uint32_t* d_lwe, int C, uint32_t* d_out, cudaStr
     VSP_CUDA_CHECK(cudaMemcpyAsync(d_rows + T2, rowB.data(), T2 * 4, cudaMemcpyHostToDevice, st));
     if (p.fft) {
         timed(c, "br2", st, [&] {
-            br2_kernel<<<T2, 256, sizeof(Br2Smem), st>>>(d_lwe, C, d_hv, c->d_bk2fd, c->d_tw2,
-                                                          d_acc2, (int)p.n, (int)p.Bg2Bits);
+            launch_br2(c, d_lwe, C, d_hv, T2, d_acc2, st);
         });
         c->launches++;
     }
@@ -1645,8 +1662,7 @@ int vsp_blind_rotate_lvl2_batch(vsp_ctx* c, const uint32_t* in, const uint64_t* 
         VSP_CUDA_CHECK(cudaMemcpyAsync(d_in, in, T * n1 * 4, cudaMemcpyHostToDevice, c->stream));
         VSP_CUDA_CHECK(cudaMemcpyAsync(d_h, h, T * 8, cudaMemcpyHostToDevice, c->stream));
         if (p.fft) {
-            br2_kernel<<<(unsigned)T, 256, sizeof(Br2Smem), c->stream>>>(
-                d_in, (int)T, d_h, c->d_bk2fd, c->d_tw2, d_acc, (int)p.n, (int)p.Bg2Bits);
+            launch_br2(c, d_in, (int)T, d_h, (int)T, d_acc, c->stream);
         }
         else {
             const int N = (int)N2;
