@@ -311,6 +311,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         const uint32_t bara = mod_switch_2n(a_next, 12);
         a_next = lwe[i + 1];
         const int buf = i & 1;
+        if (tid == 0 && i + 1 < n) {
+            // bring next step's half of bk2 (256 KiB, 4 x 64 KiB) into L2 while this step
+            // runs: the MAC's loads then hit L2 instead of HBM (bk2 does not fit in L2)
+            const char* nk = reinterpret_cast<const char*>(
+                bk2fd + (size_t)(i + 1) * 8 * 4 * 1024 + (size_t)(4 * P) * 4 * 1024);
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nk + q * 65536),
+                             "r"(65536)
+                             : "memory");
+        }
         // ---- A: warp = (row L, branch b)
         {
             const int L = warp & 3, b = warp >> 2;
