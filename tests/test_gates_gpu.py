@@ -181,3 +181,27 @@ def test_pipelined_host_batch_equals_single_device_call(prod):
     dec = vsp.decrypt(k["lv0"], out)
     want = np.array([TRUTH[kk](*(int(x) for x in b)) for kk, b in zip(kinds, bits)])
     assert np.array_equal(dec, want)
+
+
+@pytest.mark.parametrize("G", [1, 150, 2368, 2400])
+def test_wave_boundaries_host_and_device_paths(prod, G):
+    """Launch-policy boundaries: one task (latency kernel), 150 (two latency waves), exactly
+    two whole W=8 waves (no remainder), two whole waves + a 32-task remainder (key switch
+    forked under the remainder, host pipeline with an early download).  Host-pipelined and
+    device calls agree and every output decrypts right."""
+    import torch
+    e, o = prod
+    rng = np.random.default_rng(G)
+    k = oracle_keys("tfhe-80", 20200729, False)
+    p = vsp.ParameterSet("tfhe-80")
+    kid = rng.choice([GATE_KINDS.index("NAND"), GATE_KINDS.index("XOR")], G).astype(np.int32)
+    bits = rng.integers(0, 2, size=(G, 3)).astype(np.uint8)
+    ins = vsp.encrypt(p, k["lv0"], bits.reshape(-1), 5 + G).reshape(G, 3, p.n + 1)
+    out = e.hom_gate_batch(kid, ins)
+    d_in = torch.from_numpy(ins.view(np.int32)).cuda()
+    d_out = torch.empty((G, p.n + 1), dtype=torch.int32, device="cuda")
+    e.hom_gate_batch_dev(kid, d_in.data_ptr(), d_out.data_ptr(), G)
+    torch.cuda.synchronize()
+    assert np.array_equal(out, d_out.cpu().numpy().view(np.uint32))
+    want = np.array([TRUTH[GATE_KINDS[kk]](*(int(x) for x in b)) for kk, b in zip(kid, bits)])
+    assert np.array_equal(vsp.decrypt(k["lv0"], out), want)
