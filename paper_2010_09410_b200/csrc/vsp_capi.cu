@@ -788,9 +788,10 @@ void cb_batch(vsp_ctx* c, const uint32_t* d_lwe, int C, uint32_t* d_out, cudaStr
     VSP_CUDA_CHECK(cudaMemsetAsync(d_out, 0, (size_t)C * 2 * l * 2 * N1 * 4, st));
     const int islices = std::min<int>(64, (int)N2 + 1);
     const dim3 grid(islices, (unsigned)((2 * N1 + 511) / 512), 2);
-    const size_t smem = (size_t)((N2 + 1 + islices - 1) / islices) * 32 * 4;
+    constexpr int kPksGT = 16;  // gates per tile: 16 keeps 3+ CTAs per SM (more gathers in flight)
+    const size_t smem = (size_t)((N2 + 1 + islices - 1) / islices) * kPksGT * 4;
     timed(c, "pks", st, [&] {
-        pks_kernel<32><<<grid, 256, smem, st>>>(d_acc2, d_hv, T2, c->d_pks[0], c->d_pks[1], d_out,
+        pks_kernel<kPksGT><<<grid, 256, smem, st>>>(d_acc2, d_hv, T2, c->d_pks[0], c->d_pks[1], d_out,
                                                 d_rows, d_rows + T2, (int)N2, (int)N1,
                                                 (int)p.pksBaseBits, (int)p.pksLen);
     });
