@@ -8,18 +8,6 @@
 
 #include "fft512.cuh"
 
-#ifndef VSP_BR_INV2
-#define VSP_BR_INV2 1
-#endif
-#ifndef VSP_BR_Z0
-#define VSP_BR_Z0 1
-#endif
-#ifndef VSP_IKS_PAIR
-#define VSP_IKS_PAIR 0  // 16-way switch compiles to a divergent compare tree: 6.5 vs 3.4 ms
-#endif
-#ifndef VSP_BR_FWD2
-#define VSP_BR_FWD2 0  // measured slower (spills at 255 regs): 32.8 vs 30.2 ms
-#endif
 
 namespace vsp {
 
@@ -75,7 +63,7 @@ struct Br1024Smem {
     double2 tw2[kTw2Entries * 32];
     double2 xbuf[WARPS][kFftXbufStride];
     uint32_t acc[WARPS][2048];
-    uint32_t dig[WARPS][2][16 * 32];  // digits (2 levels), packed 2 x int16
+    uint32_t dig[WARPS][16 * 32];  // level-1 digits, packed 2 x 16-bit offset binary
     uint64_t full[S];
     uint32_t cnt[S];
 };
@@ -161,17 +149,13 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
             }
         }
     };
-    // diff = (X^bara - 1) * acc_P (polyMulByXkMinusOne, poly.hpp:51-57) computed once;
-    // both digit levels (decomposePoly, poly.hpp:79-97) are parked in smem as packed
-    // int16 pairs (coefficients p, p+512) so no transform registers are live.
+    // diff = (X^bara - 1) * acc_P (polyMulByXkMinusOne, poly.hpp:51-57) computed once per
+    // polynomial; of its two digit levels (decomposePoly, poly.hpp:79-97) level 0 goes
+    // straight into the transform registers z and level 1 is parked in smem as packed
+    // 16-bit offset-binary pairs (coefficients p, p+512) for the second transform.
     // lane + 32 j is recomputed from an opaque base every step so the compiler does not
     // hoist 32 loop-invariant indices into (spilled) registers.
-#if VSP_BR_Z0
-    // level-0 digits go straight into the transform registers z; level 1 is parked
     auto digits = [&](int P, uint32_t bara, double2 (&z)[16]) {
-#else
-    auto digits = [&](int P, uint32_t bara) {
-#endif
         const uint32_t* src = acc + P * 1024;
         const uint32_t lo = (uint32_t)lane + (uint32_t)opaque_zero();
         const uint32_t lk = lo - bara;
@@ -185,19 +169,15 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
             const uint32_t d1 = (v1 >> (32 - BG)) + (32768u - kHalf);
             const uint32_t e0 = ((v0 >> (32 - 2 * BG)) & kMask) + (32768u - kHalf);
             const uint32_t e1 = ((v1 >> (32 - 2 * BG)) & kMask) + (32768u - kHalf);
-#if VSP_BR_Z0
             z[j].x = ob_to_double<15>(d0);
             z[j].y = ob_to_double<15>(d1);
-#else
-            sm.dig[warp][0][j * 32 + lane] = d0 | (d1 << 16);
-#endif
-            sm.dig[warp][1][j * 32 + lane] = e0 | (e1 << 16);
+            sm.dig[warp][j * 32 + lane] = e0 | (e1 << 16);
         }
     };
-    auto load_digits = [&](double2 (&z)[16], int lvl) {
+    auto load_digits1 = [&](double2 (&z)[16]) {
 #pragma unroll
         for (int j = 0; j < 16; j++) {
-            const uint32_t w = sm.dig[warp][lvl][j * 32 + lane];
+            const uint32_t w = sm.dig[warp][j * 32 + lane];
             z[j].x = ob_to_double<15>(w & 0xffffu);
             z[j].y = ob_to_double<15>(w >> 16);
         }
@@ -207,59 +187,19 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     for (int i = 0; i < n; i++) {
         const uint32_t bara = mod_switch_2n(lwe[i], 11);
         const int c0 = i * 4;
-#if VSP_BR_FWD2
-        // rows 0, 1 (polynomial a, both digit levels): two transforms at once, while the
-        // MAC accumulators are not yet live; their products initialise accA / accB.
-        digits(0, bara);
-        {
-            double2 z0[16], z1[16];
-            load_digits(z0, 0);
-            load_digits(z1, 1);
-            fft512_fwd2(z0, z1, xbuf, sm.tw2, lane);
-            mbar_wait(&sm.full[c0 % S], (uint32_t)((c0 / S) & 1));
-            mbar_wait(&sm.full[(c0 + 1) % S], (uint32_t)(((c0 + 1) / S) & 1));
-            const double2* bk0 = sm.ring[c0 % S];
-            const double2* bk1 = sm.ring[(c0 + 1) % S];
-#pragma unroll
-            for (int j = 0; j < 16; j++) {
-                const double2 ba = bk0[j * 32 + lane];
-                const double2 bb = bk0[512 + j * 32 + lane];
-                const double2 ca = bk1[j * 32 + lane];
-                const double2 cb = bk1[512 + j * 32 + lane];
-                accA[j].x = fma(z1[j].x, ca.x, fma(-z1[j].y, ca.y, fma(z0[j].x, ba.x, -z0[j].y * ba.y)));
-                accA[j].y = fma(z1[j].x, ca.y, fma(z1[j].y, ca.x, fma(z0[j].x, ba.y, z0[j].y * ba.x)));
-                accB[j].x = fma(z1[j].x, cb.x, fma(-z1[j].y, cb.y, fma(z0[j].x, bb.x, -z0[j].y * bb.y)));
-                accB[j].y = fma(z1[j].x, cb.y, fma(z1[j].y, cb.x, fma(z0[j].x, bb.y, z0[j].y * bb.x)));
-            }
-        }
-        release(c0);
-        release(c0 + 1);
-        constexpr int P0 = 1;
-#else
 #pragma unroll
         for (int j = 0; j < 16; j++) {
             accA[j] = make_double2(0.0, 0.0);
             accB[j] = make_double2(0.0, 0.0);
         }
-        constexpr int P0 = 0;
-#endif
 #pragma unroll 1
-        for (int P = P0; P < 2; P++) {
-#if VSP_BR_Z0
+        for (int P = 0; P < 2; P++) {
             double2 z[16];
             digits(P, bara, z);
-#else
-            digits(P, bara);
-#endif
 #pragma unroll 1
             for (int lvl = 0; lvl < 2; lvl++) {
-#if VSP_BR_Z0
                 if (lvl)
-                    load_digits(z, 1);
-#else
-                double2 z[16];
-                load_digits(z, lvl);
-#endif
+                    load_digits1(z);
                 fft512_fwd(z, xbuf, sm.tw2, lane);
                 const int c = c0 + P * 2 + lvl;
                 const int s = c % S;
@@ -278,20 +218,13 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
             }
         }
         // inverse transforms, round (llrint, fft.hpp:47-50) and accumulate
-#if VSP_BR_INV2
         fft512_inv2(accA, accB, xbuf, sm.tw2, lane);
-#else
-        fft512_inv(accA, xbuf, sm.tw2, lane);
-#endif
 #pragma unroll
         for (int j = 0; j < 16; j++) {
             const int p = lane + 32 * j;
             acc[p] += (uint32_t)__double2ll_rn(accA[j].x);
             acc[p + 512] += (uint32_t)__double2ll_rn(accA[j].y);
         }
-#if !VSP_BR_INV2
-        fft512_inv(accB, xbuf, sm.tw2, lane);
-#endif
 #pragma unroll
         for (int j = 0; j < 16; j++) {
             const int p = lane + 32 * j;
@@ -795,57 +728,6 @@ __global__ void __launch_bounds__(128) iks_b2_kernel(
     };
 
     const int steps = islice * T;  // multiple of 8 (T = 8)
-#if VSP_IKS_PAIR
-    // Two digit steps (i, j), (i, j + 1) per gate at once: their 4 digit bits are
-    // contiguous, so one 16-way uniform branch picks both rows and IADD3 adds them
-    // together -- half the branches and adds of the one-step loop.
-    uint32_t rc[3][KPT], rd[3][KPT];
-    auto consume2 = [&](const uint32_t (&ca)[3][KPT], const uint32_t (&cb)[3][KPT], int s) {
-        const int ii = s >> 3, j = s & 7;  // j even
-        const uint4* dp = reinterpret_cast<const uint4*>(dig16 + ii * GT);
-        uint32_t dw[GT / 2];
-#pragma unroll
-        for (int q = 0; q < GT / 8; q++) {
-            const uint4 v = dp[q];
-            dw[4 * q] = v.x;
-            dw[4 * q + 1] = v.y;
-            dw[4 * q + 2] = v.z;
-            dw[4 * q + 3] = v.w;
-        }
-        const int sh = 12 - 2 * j;
-#pragma unroll
-        for (int g = 0; g < GT; g++) {
-            const uint32_t q = (dw[g >> 1] >> ((g & 1) * 16 + sh)) & 15u;  // d_j * 4 + d_j+1
-#define VSP_IKS_C(A, B)                                                   \
-    case (A) * 4 + (B):                                                   \
-        _Pragma("unroll") for (int kk = 0; kk < KPT; kk++)                \
-            acc[g][kk] += ((A) ? ca[(A) ? (A) - 1 : 0][kk] : 0u) +        \
-                          ((B) ? cb[(B) ? (B) - 1 : 0][kk] : 0u);         \
-        break;
-            switch (q) {
-                VSP_IKS_C(0, 1) VSP_IKS_C(0, 2) VSP_IKS_C(0, 3)
-                VSP_IKS_C(1, 0) VSP_IKS_C(1, 1) VSP_IKS_C(1, 2) VSP_IKS_C(1, 3)
-                VSP_IKS_C(2, 0) VSP_IKS_C(2, 1) VSP_IKS_C(2, 2) VSP_IKS_C(2, 3)
-                VSP_IKS_C(3, 0) VSP_IKS_C(3, 1) VSP_IKS_C(3, 2) VSP_IKS_C(3, 3)
-            default: break;
-            }
-#undef VSP_IKS_C
-        }
-    };
-    load(ra);
-    load(rb);
-#pragma unroll 1
-    for (int s = 0; s < steps; s += 4) {
-        load(rc);
-        load(rd);
-        consume2(ra, rb, s);
-        if (s + 4 < steps) {
-            load(ra);
-            load(rb);
-        }
-        consume2(rc, rd, s + 2);
-    }
-#else
     load(ra);
 #pragma unroll 1
     for (int s = 0; s < steps; s += 2) {
@@ -855,7 +737,6 @@ __global__ void __launch_bounds__(128) iks_b2_kernel(
             load(ra);
         consume(rb, s + 1);
     }
-#endif
 #pragma unroll
     for (int g = 0; g < GT; g++) {
         if (g >= ng)

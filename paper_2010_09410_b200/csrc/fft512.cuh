@@ -435,75 +435,6 @@ __device__ __forceinline__ void fft512_inv2(double2 (&va)[16], double2 (&vb)[16]
     }
 }
 
-// Two forward transforms at once (shared per-lane twiddle loads, two independent streams).
-template <int ROOT = 0>
-__device__ __forceinline__ void fft512_fwd2(double2 (&va)[16], double2 (&vb)[16], void* xbuf,
-                                            const double2* tw2, int lane)
-{
-    const double2* tw1t = &c_tw1t[ROOT][0] + opaque_zero();
-    const double2* tw2t = tw2 + kTw2Plain * 32;
-#pragma unroll
-    for (int d = 0; d < 4; d++) {
-        const int h = 8 >> d;
-#pragma unroll
-        for (int j = 0; j < 16; j++)
-            if ((j & h) == 0) {
-                const int b = j >> (4 - d);
-                const double2 kt = tw1t[(1 << d) - 1 + b];
-                if (tw_form_a(ROOT, d, b)) {
-                    bf_fwd_tan<true>(va[j], va[j + h], kt);
-                    bf_fwd_tan<true>(vb[j], vb[j + h], kt);
-                }
-                else {
-                    bf_fwd_tan<false>(va[j], va[j + h], kt);
-                    bf_fwd_tan<false>(vb[j], vb[j + h], kt);
-                }
-            }
-    }
-    xpose_fwd<false>(va, xbuf, lane);
-    xpose_fwd<false>(vb, xbuf, lane);
-#pragma unroll
-    for (int d = 4; d < 8; d++) {
-        const int h = 8 >> (d - 4);
-#pragma unroll
-        for (int j = 0; j < 16; j++)
-            if ((j & h) == 0) {
-                const int k = tw_k(d, j >> (8 - d));
-                const double2 w = tw2t[tw_entry(d, k & 3) * 32 + lane];
-                if (k >> 2) {
-                    bf_fwd_tq<1>(va[j], va[j + h], w);
-                    bf_fwd_tq<1>(vb[j], vb[j + h], w);
-                }
-                else {
-                    bf_fwd_tq<0>(va[j], va[j + h], w);
-                    bf_fwd_tq<0>(vb[j], vb[j + h], w);
-                }
-            }
-    }
-    const bool odd = lane & 1;
-#pragma unroll
-    for (int k = 0; k < 8; k++) {
-        const double2 ra = shfl_xor_d2(odd ? va[k] : va[k + 8], 1);
-        const double2 rb = shfl_xor_d2(odd ? vb[k] : vb[k + 8], 1);
-        double2 ua = odd ? ra : va[k], wa = odd ? va[k + 8] : ra;
-        double2 ub = odd ? rb : vb[k], wb = odd ? vb[k + 8] : rb;
-        const int br = bitrev_const(k, 3);
-        const double2 t = tw2t[tw_entry(8, br & 3) * 32 + lane];
-        if (br >> 2) {
-            bf_fwd_tq<1>(ua, wa, t);
-            bf_fwd_tq<1>(ub, wb, t);
-        }
-        else {
-            bf_fwd_tq<0>(ua, wa, t);
-            bf_fwd_tq<0>(ub, wb, t);
-        }
-        va[k] = ua;
-        va[k + 8] = wa;
-        vb[k] = ub;
-        vb[k + 8] = wb;
-    }
-}
-
 // Inverse transform of one block split over a warp pair (64 lanes x 8 values), for the
 // latency kernel.  Lane l of pair half h stands for virtual lane L = 16h + (l & 15) of
 // fft512_inv's layout and half e = l >> 4 of that lane's 16 values:
