@@ -376,8 +376,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
                 // other polynomial's go to the peer
 #pragma unroll
                 for (int k = 0; k < 2; k++) {
-                    sm.reg[2 * k + b][s] = o[2 * P + k];
-                    peer->part[buf][2 * k + b][s] = o[2 * (P ^ 1) + k];
+                    // (static register indices: P selects, it does not index)
+                    sm.reg[2 * k + b][s] = P ? o[2 + k] : o[k];
+                    peer->part[buf][2 * k + b][s] = P ? o[k] : o[2 + k];
                 }
             }
         }
