@@ -33,9 +33,12 @@ struct Chain1024Smem {
     double2 tw2[kTw2Entries * 32];
     double2 xbuf[WARPS][kFftXbufStride];
     uint32_t acc[WARPS][2048];
+    uint32_t dig[WARPS][512];  // level-1 digits of the current polynomial (2 x 16 bit)
 };
 
-template <int WARPS>
+// MODE is the chains' mode (every task of a launch has the same one: run_chains splits
+// mixed batches), so the digit loop carries one code path.
+template <int WARPS, int MODE>
 __global__ void __launch_bounds__(WARPS * 32, 1)
     cmux_chain1024_kernel(const ChainTask* __restrict__ tasks, int T,
                           const double2* __restrict__ sels, const double2* __restrict__ tw2g,
@@ -61,7 +64,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     const int sh1 = 32 - bgbits, sh2 = 32 - 2 * bgbits;
     double2* xbuf = sm.xbuf[warp];
     const uint32_t* base = task.c0;
-    const int mode = task.mode;
+    constexpr int mode = MODE;
 
 #pragma unroll 1
     for (int s = 0; s < task.nsteps; s++) {
@@ -77,28 +80,40 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
         for (int P = 0; P < 2; P++) {
             const uint32_t* src = acc + P * 1024;
             const uint32_t* bsrc = base + P * 1024;
+            // d = c1' - c0' once per polynomial; level 0 digits straight into z, level 1
+            // parked as 16-bit offset-binary pairs (decomposePoly, poly.hpp:79-97)
+            double2 z[16];
+#pragma unroll
+            for (int j = 0; j < 16; j++) {
+                const uint32_t p0 = lane + 32 * j, p1 = p0 + 512;
+                uint32_t d0, d1;
+                if (mode == 0) {
+                    d0 = src[p0] - __ldg(bsrc + p0);
+                    d1 = src[p1] - __ldg(bsrc + p1);
+                }
+                else {
+                    const uint32_t i0 = (p0 - rot) & 2047u, i1 = (p1 - rot) & 2047u;
+                    const uint32_t r0 = i0 < 1024 ? src[i0] : 0u - src[i0 - 1024];
+                    const uint32_t r1 = i1 < 1024 ? src[i1] : 0u - src[i1 - 1024];
+                    d0 = r0 - src[p0];
+                    d1 = r1 - src[p1];
+                }
+                const uint32_t v0 = d0 + offset, v1 = d1 + offset;
+                z[j].x = ob_to_double<15>((v0 >> sh1) + (32768u - half));
+                z[j].y = ob_to_double<15>((v1 >> sh1) + (32768u - half));
+                sm.dig[warp][j * 32 + lane] = (((v0 >> sh2) & mask) + (32768u - half)) |
+                                              ((((v1 >> sh2) & mask) + (32768u - half)) << 16);
+            }
 #pragma unroll 1
             for (int lvl = 0; lvl < 2; lvl++) {
-                const int sh = lvl == 0 ? sh1 : sh2;
-                double2 z[16];
+                if (lvl) {
+                    __syncwarp();
 #pragma unroll
-                for (int j = 0; j < 16; j++) {
-                    const uint32_t p0 = lane + 32 * j, p1 = p0 + 512;
-                    uint32_t d0, d1;
-                    if (mode == 0) {
-                        d0 = src[p0] - __ldg(bsrc + p0);
-                        d1 = src[p1] - __ldg(bsrc + p1);
+                    for (int j = 0; j < 16; j++) {
+                        const uint32_t w = sm.dig[warp][j * 32 + lane];
+                        z[j].x = ob_to_double<15>(w & 0xffffu);
+                        z[j].y = ob_to_double<15>(w >> 16);
                     }
-                    else {
-                        const uint32_t i0 = (p0 - rot) & 2047u, i1 = (p1 - rot) & 2047u;
-                        const uint32_t r0 = i0 < 1024 ? src[i0] : 0u - src[i0 - 1024];
-                        const uint32_t r1 = i1 < 1024 ? src[i1] : 0u - src[i1 - 1024];
-                        d0 = r0 - src[p0];
-                        d1 = r1 - src[p1];
-                    }
-                    const uint32_t v0 = d0 + offset, v1 = d1 + offset;
-                    z[j].x = (double)(int32_t)(((v0 >> sh) & mask) - half);
-                    z[j].y = (double)(int32_t)(((v1 >> sh) & mask) - half);
                 }
                 fft512_fwd(z, xbuf, sm.tw2, lane);
                 const double2* row = S + (size_t)(P * 2 + lvl) * 1024;
@@ -112,6 +127,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
                     accB[j].y = fma(z[j].x, bb.y, fma(z[j].y, bb.x, accB[j].y));
                 }
             }
+            __syncwarp();
         }
         // acc <- c0' + round(inverse): mode 0 c0' = base, mode 1 c0' = acc
         fft512_inv(accA, xbuf, sm.tw2, lane);

@@ -563,7 +563,10 @@ void configure_kernels()
                                         (int)sizeof(Br2Smem)));
     VSP_CUDA_CHECK(cudaFuncSetAttribute(br2c_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)sizeof(Br2cSmem)));
-    VSP_CUDA_CHECK(cudaFuncSetAttribute(cmux_chain1024_kernel<kChainWarps>,
+    VSP_CUDA_CHECK(cudaFuncSetAttribute(cmux_chain1024_kernel<kChainWarps, 0>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)sizeof(Chain1024Smem<kChainWarps>)));
+    VSP_CUDA_CHECK(cudaFuncSetAttribute(cmux_chain1024_kernel<kChainWarps, 1>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)sizeof(Chain1024Smem<kChainWarps>)));
     const int ik = 1024 * 8 * 8;
@@ -835,11 +838,18 @@ void run_chains(vsp_ctx* c, const std::vector<ChainTask>& tasks, cudaStream_t st
                                    cudaMemcpyHostToDevice, st));
     const int T = (int)tasks.size();
     if (p.fft) {
+        for (const auto& t : tasks)
+            if (t.mode != tasks[0].mode)
+                throw std::logic_error("run_chains: mixed chain modes in one launch");
         timed(c, "cmux_chain", st, [&] {
-            cmux_chain1024_kernel<kChainWarps>
-                <<<(T + kChainWarps - 1) / kChainWarps, kChainWarps * 32,
-                   sizeof(Chain1024Smem<kChainWarps>), st>>>(d, T, c->selfd.as<double2>(0),
-                                                             c->d_tw2, (int)p.Bg1Bits);
+            const dim3 grid((T + kChainWarps - 1) / kChainWarps);
+            const size_t smem = sizeof(Chain1024Smem<kChainWarps>);
+            if (tasks[0].mode == 0)
+                cmux_chain1024_kernel<kChainWarps, 0><<<grid, kChainWarps * 32, smem, st>>>(
+                    d, T, c->selfd.as<double2>(0), c->d_tw2, (int)p.Bg1Bits);
+            else
+                cmux_chain1024_kernel<kChainWarps, 1><<<grid, kChainWarps * 32, smem, st>>>(
+                    d, T, c->selfd.as<double2>(0), c->d_tw2, (int)p.Bg1Bits);
         });
     }
     else {
