@@ -205,3 +205,24 @@ def test_wave_boundaries_host_and_device_paths(prod, G):
     assert np.array_equal(out, d_out.cpu().numpy().view(np.uint32))
     want = np.array([TRUTH[GATE_KINDS[kk]](*(int(x) for x in b)) for kk, b in zip(kid, bits)])
     assert np.array_equal(vsp.decrypt(k["lv0"], out), want)
+
+
+def test_not_only_and_mux_heavy_batches_tfhe80(prod):
+    """Batches without any blind rotation (all NOT: the host pipeline uploads and negates
+    only) and MUX-heavy batches (two tasks per gate across the wave boundary)."""
+    e, o = prod
+    rng = np.random.default_rng(33)
+    x = np.zeros((40, 3, o.n + 1), np.uint32)
+    bits = rng.integers(0, 2, 40)
+    for i, b in enumerate(bits):
+        x[i, 0] = o.encrypt(int(b))
+    out = e.hom_gate_batch(["NOT"] * 40, x)
+    assert [o.decrypt(c) for c in out] == [1 - int(b) for b in bits]
+    G = 700  # 1,400 blind-rotation tasks: one whole wave + a remainder
+    k = oracle_keys("tfhe-80", 20200729, False)
+    p = vsp.ParameterSet("tfhe-80")
+    mb = rng.integers(0, 2, size=(G, 3)).astype(np.uint8)
+    ins = vsp.encrypt(p, k["lv0"], mb.reshape(-1), 44).reshape(G, 3, p.n + 1)
+    out = e.hom_gate_batch(["MUX"] * G, ins)
+    want = np.array([TRUTH["MUX"](*(int(v) for v in b)) for b in mb])
+    assert np.array_equal(vsp.decrypt(k["lv0"], out), want)
