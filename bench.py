@@ -37,6 +37,24 @@ UNIT = "gates/s"
 # Algorithmic work per external product and per level-1 bootstrap:
 # F_EP = (2l+2)*5*M*log2(M) + 2l*2*8*M with M = 512, l = 2.
 F_EP = (2 * 2 + 2) * 5 * 512 * 9 + 2 * 2 * 2 * 8 * 512
+# level-2 external product (circuit bootstrap): M = 1024, l2 = 4
+F_EP2 = (2 * 4 + 2) * 5 * 1024 * 10 + 2 * 4 * 2 * 8 * 1024
+
+
+def work_roofline(counters: dict, n: int, seconds: float, peak: float) -> dict:
+    """FFT-compute roofline of a memory access / clock cycle from the op counters: every
+    level-1 blind rotation is n external products, every CMUX one, every circuit bootstrap
+    l1 = 2 level-2 blind rotations of n level-2 external products."""
+    flops = (counters["blindRotate"] * n * F_EP + counters["cmux"] * F_EP +
+             counters["circuitBootstrap"] * 2 * n * F_EP2)
+    achieved = flops / seconds / 1e12
+    return {"bound": "fp64", "achieved": round(achieved, 3), "peak": round(peak, 3),
+            "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "flops": int(flops),
+            "t_roof_s": round(flops / (peak * 1e12), 5),
+            "flops_rule": "blindRotate*n*F_EP + cmux*F_EP + circuitBootstrap*2*n*F_EP2, "
+                          "F_EP = 171008, F_EP2 = 643072",
+            "note": "the narrow levels are latency-bound (n dependent external products per "
+                    "level), so a cycle cannot reach the throughput roofline"}
 KERNEL_TIMERS = ("br1024", "br_lat", "iks", "gate_prep", "cmux_chain", "br2", "pks")
 
 
@@ -451,6 +469,7 @@ def run_memory(args, world, rank, local):
         return
     val = float(np.mean(dev_ms)) / 1e3
     host_val = float(np.mean(times)) + float(np.mean(times_rom))
+    cpa = {k: v // max(args.steps, 1) for k, v in eng.counters().items()}
     cpu = None
     if not args.no_cpu_baseline and available("ref"):
         r = CpuTfhe("ref", "tfhe-80", n_override=args.n, seed=1)
@@ -479,7 +498,8 @@ def run_memory(args, world, rank, local):
                 "rom_read_s": round(float(np.mean(times_rom)), 5),
                 "api": "vsp_ram_cycle + vsp_rom_read host calls (RAM image 32 MiB H2D + D2H "
                        "per access, as the reference's EncryptedRam round-trip)"},
-        "counters_per_access": {k: v // max(args.steps, 1) for k, v in eng.counters().items()},
+        "counters_per_access": cpa,
+        "roofline": work_roofline(cpa, p.n, val, vsp.fp64_peak_tflops(local)),
         "cpu_baseline": cpu}), flush=True)
 
 
@@ -562,6 +582,7 @@ def run_cycle(args, world, rank, local):
             dist.destroy_process_group()
         return
     st = N.netlist_stats(nl)
+    cpc = {k: v // max(args.steps, 1) for k, v in eng.counters().items()}
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         cpu = _cycle_cpu_baseline(p, keys, nl, ram, v, w, luts, dff0, ins)
@@ -574,7 +595,8 @@ def run_cycle(args, world, rank, local):
                    "gates": sum(st["count_by_kind"][k] for k in N.GATES),
                    "dffs": st["dff_count"], "depth": st["depth"], "gmax": st["gmax"],
                    "rom": "512 B, 7 addr bits", "ram": "v=8 w=16", "n": p.n},
-        "counters_per_cycle": {k: v // max(args.steps, 1) for k, v in eng.counters().items()},
+        "counters_per_cycle": cpc,
+        "roofline": work_roofline(cpc, p.n, float(np.mean(secs)), vsp.fp64_peak_tflops(local)),
         "kernel_ms_per_cycle": kernels, "cpu_baseline": cpu,
         "timing": "CUDA events around each device-resident cycle (max over ranks)"}), flush=True)
     if dist:
