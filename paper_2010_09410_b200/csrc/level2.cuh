@@ -351,11 +351,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
                 rg[j * 32 + lane] = z[j];
         }
         __syncthreads();
-        // ---- B: partial MAC over rows 4P..4P+3 for the four outputs
+        // ---- B: partial MAC over rows 4P..4P+3 for the four outputs.  Bound by the L2
+        // latency of the bk2 loads: the loads of the next point are issued before the FMAs
+        // of the current one (two register sets of 16 x double2; the compiler barrier at the
+        // end of each point keeps ptxas from hoisting more)
         {
             const double2* K = bk2fd + (size_t)i * 8 * 4 * 1024 + (size_t)(4 * P) * 4 * 1024;
-#pragma unroll 1
+            double2 kc[16], kn[16];
+            auto load = [&](double2 (&kk)[16], int m) {
+                const int f = tid + 256 * m;
+#pragma unroll
+                for (int u = 0; u < 16; u++)
+                    kk[u] = __ldg(K + (size_t)u * 1024 + f);  // u = L * 4 + q
+            };
+            load(kc, 0);
+#pragma unroll
             for (int m = 0; m < 4; m++) {
+                if (m < 3)
+                    load(kn, m + 1);
                 const int f = tid + 256 * m;
                 const int b = f >> 9, s = f & 511;
                 double2 o[4];
@@ -367,7 +380,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
                     const double2 d = sm.reg[2 * L + b][s];
 #pragma unroll
                     for (int q = 0; q < 4; q++) {
-                        const double2 k = __ldg(K + ((size_t)(L * 4 + q)) * 1024 + f);
+                        const double2 k = kc[L * 4 + q];
                         o[q].x = fma(d.x, k.x, fma(-d.y, k.y, o[q].x));
                         o[q].y = fma(d.x, k.y, fma(d.y, k.x, o[q].y));
                     }
@@ -379,6 +392,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
                     // (static register indices: P selects, it does not index)
                     sm.reg[2 * k + b][s] = P ? o[2 + k] : o[k];
                     peer->part[buf][2 * k + b][s] = P ? o[k] : o[2 + k];
+                }
+                asm volatile("" ::: "memory");
+                if (m < 3) {
+#pragma unroll
+                    for (int u = 0; u < 16; u++)
+                        kc[u] = kn[u];
                 }
             }
         }
