@@ -33,6 +33,11 @@ __constant__ double2 c_tw1[3][15];
 // zeta = kappa (1 + i tau) (form A, |tan| <= 1) or zeta = kappa (tau + i) (form B,
 // |cot| < 1); the form of each (root, d, b) is known at compile time (tw_form_a).
 __constant__ double2 c_tw1t[3][15];
+// The same twiddles, all in form A (kappa, tau) = (cos, tan) of the half angle: used where
+// the twiddle is chosen per lane (fft512_fwd_pair) so one butterfly formula serves both
+// candidates.  tau may be large (angle near pi/2); kappa*tau keeps the rounding bound and
+// no angle here is exactly pi/2.
+__constant__ double2 c_tw1a[3][15];
 
 __host__ __device__ constexpr int bitrev_const(int b, int d)
 {
@@ -528,6 +533,98 @@ __device__ __forceinline__ void fft512_inv_pair(double2 (&u)[8], double2* xbuf,
             const double2 d = make_double2(fma(sg, u[t].x, o.x), fma(sg, u[t].y, o.y));
             u[t] = cmul(d, c);
         }
+    }
+}
+
+// Forward transform of one block split over a warp pair (the mirror of fft512_inv_pair).
+// Lane l of pair half h: virtual lane L = 16h + (l & 15), half e = l >> 4:
+//   input  u[t] = z at time position L + 32 (t + 8e)   (z_p = x_p + i x_{p+512})
+//   output u[t] = v_L[2t + e]                          (frequency slot (2t + e) * 32 + L)
+// i.e. exactly fft512_fwd's butterflies, twiddles and output slots.  Stage 0 and stage 7
+// pair the halves through __shfl_xor 16, stage 8's lane pairs (L, L^1) use __shfl_xor 1.
+template <int ROOT = 0>
+__device__ __forceinline__ void fft512_fwd_pair(double2 (&u)[8], double2* xbuf,
+                                                const double2* tw2, int lane, int h, int bar_id)
+{
+    const int L = 16 * h + (lane & 15);
+    const int e = lane >> 4;
+    const bool oddL = L & 1;
+    const double2* tw2t = tw2 + kTw2Plain * 32;
+    // cross-half butterfly (a = half 0's value, b = half 1's): half 0 keeps a + zeta b,
+    // half 1 a - zeta b; zeta = k (1 + i t) in form A, Q multiplies it by i
+    auto cross = [&](double2& mine, const double2 kt, bool Q) {
+        const double2 o = shfl_xor_d2(mine, 16);
+        const double2 a = e ? o : mine;
+        double2 b = e ? mine : o;
+        if (Q)
+            b = make_double2(-b.y, b.x);
+        const double tx = fma(-kt.y, b.y, b.x), ty = fma(kt.y, b.x, b.y);
+        const double sk = e ? -kt.x : kt.x;
+        mine = make_double2(fma(sk, tx, a.x), fma(sk, ty, a.y));
+    };
+    // ---- pass 1 (stages 0..3) on j = t + 8e
+    {
+        const double2* tw1a = &c_tw1a[ROOT][0] + opaque_zero();
+        const double2 k0 = tw1a[0];
+#pragma unroll
+        for (int t = 0; t < 8; t++)
+            cross(u[t], k0, false);
+#pragma unroll
+        for (int d = 1; d < 4; d++) {
+            const int hh = 8 >> d;
+#pragma unroll
+            for (int t = 0; t < 8; t++)
+                if ((t & hh) == 0) {
+                    const int base = (1 << d) - 1 + (t >> (4 - d));
+                    const double2 w0 = tw1a[base], w1 = tw1a[base + (8 >> (4 - d))];
+                    bf_fwd_tan<true>(u[t], u[t + hh], e ? w1 : w0);
+                }
+        }
+    }
+    // ---- transpose through the pair's buffer (fft512_fwd's xpose_fwd element mapping)
+#pragma unroll
+    for (int t = 0; t < 8; t++)
+        xbuf[L + 34 * (t + 8 * e)] = u[t];
+    asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+    {
+        const int rbase = (L & 1) + 34 * (L >> 1) + 2 * e;
+#pragma unroll
+        for (int t = 0; t < 8; t++)
+            u[t] = xbuf[rbase + 4 * t];
+    }
+    // ---- pass 2 on j = 2t + e: stages 4, 5, 6 local, stage 7 across the halves
+#pragma unroll
+    for (int d = 4; d < 7; d++) {
+        const int hh = 1 << (6 - d);
+#pragma unroll
+        for (int t = 0; t < 8; t++)
+            if ((t & hh) == 0) {
+                const int k = tw_k(d, t >> (7 - d));
+                const double2 w = tw2t[tw_entry(d, k & 3) * 32 + L];
+                if (k >> 2)
+                    bf_fwd_tq<1>(u[t], u[t + hh], w);
+                else
+                    bf_fwd_tq<0>(u[t], u[t + hh], w);
+            }
+    }
+#pragma unroll
+    for (int t = 0; t < 8; t++) {
+        const int k = tw_k(7, t);
+        cross(u[t], tw2t[tw_entry(7, k & 3) * 32 + L], (k >> 2) != 0);
+    }
+    // ---- stage 8: k = 2 tp + e, Q = e (bitrev3(k) = (e << 2) | bitrev2(tp))
+#pragma unroll
+    for (int tp = 0; tp < 4; tp++) {
+        const double2 recv = shfl_xor_d2(oddL ? u[tp] : u[tp + 4], 1);
+        double2 a = oddL ? recv : u[tp];
+        double2 b = oddL ? u[tp + 4] : recv;
+        const double2 kt = tw2t[tw_entry(8, bitrev_const(tp, 2)) * 32 + L];
+        const double2 bq = e ? make_double2(-b.y, b.x) : b;  // i^Q b, Q = e
+        const double tx = fma(-kt.y, bq.y, bq.x), ty = fma(kt.y, bq.x, bq.y);
+        b = make_double2(fma(-kt.x, tx, a.x), fma(-kt.x, ty, a.y));
+        a = make_double2(fma(kt.x, tx, a.x), fma(kt.x, ty, a.y));
+        u[tp] = a;
+        u[tp + 4] = b;
     }
 }
 

@@ -458,6 +458,212 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
 }
 
 // ---------------------------------------------------------------------------
+// Level-2 blind rotation on a cluster of FOUR CTAs per task.  CTA (P, b) owns accumulator
+// polynomial P and branch b of the level-2 split Y^1024 = +-sqrt(i) (the two 512-point
+// halves of every transform):
+//   A. digits of its polynomial's four rows and their branch-b forward transforms, each
+//      split over a warp pair (fft512_fwd_pair);
+//   B. partial MAC over its four rows for all four outputs at the branch-b points (a
+//      quarter of bk2[i], 128 KiB, per SM); the other polynomial's two outputs go to CTA
+//      (1-P, b) through DSMEM;
+//   C. own outputs (rows 0..3 first, then 4..7), branch-b inverse transforms on warp pairs;
+//      the results also go to the branch partner (P, 1-b);
+//   D. both CTAs of polynomial P recombine branches, lo/hi halves and round exactly into
+//      identical copies of acc[P].
+// Two cluster barriers per step; each exchange buffer is written and read between the
+// same pair of barriers, so single buffers suffice.
+struct Br2qSmem {
+    uint64_t acc[2048];                 // polynomial P (identical on both branch CTAs)
+    double2 reg[4][kBr2cRegion];        // row L (forward), then own outputs k (2 x)
+    double2 part[2][512];               // MAC partials from (1-P, b), by output k
+    double2 xin[2][512];                // branch 1-b inverse outputs from (P, 1-b)
+    double2 tw2[kTw2Entries * 32];      // this branch's root (1 + b)
+};
+
+__global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(256, 1)
+    br2q_kernel(const uint32_t* __restrict__ tasks, int ninputs, const uint64_t* __restrict__ hv,
+                const double2* __restrict__ bk2fd, const double2* __restrict__ tw2g,
+                uint64_t* __restrict__ out, int n, int bgbits)
+{
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    Br2qSmem& sm = *reinterpret_cast<Br2qSmem*>(smem_raw);
+    const int cr = (int)cluster.block_rank();
+    const int P = cr >> 1, br = cr & 1;
+    const int task = blockIdx.x >> 2;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t* lwe = tasks + (size_t)(task % ninputs) * (n + 1);
+    Br2qSmem* mac_peer = cluster.map_shared_rank(&sm, cr ^ 2);  // (1-P, b)
+    Br2qSmem* br_peer = cluster.map_shared_rank(&sm, cr ^ 1);   // (P, 1-b)
+    for (int i = tid; i < kTw2Entries * 32; i += blockDim.x)
+        sm.tw2[i] = tw2g[(1 + br) * kTw2Entries * 32 + i];
+    {
+        const uint64_t h2 = hv[task] / 2;
+        const uint32_t rot = (4096u - mod_switch_2n(lwe[n], 12)) & 4095u;
+        for (int q = tid; q < 2048; q += blockDim.x) {
+            uint64_t val = 0;
+            if (P == 1) {
+                if (rot < 2048)
+                    val = ((uint32_t)q < rot) ? (0ull - h2) : h2;
+                else
+                    val = ((uint32_t)q < rot - 2048) ? h2 : (0ull - h2);
+            }
+            sm.acc[q] = val;
+        }
+    }
+    cluster.sync();
+    const uint64_t half = 1ull << (bgbits - 1);
+    const uint64_t mask = (1ull << bgbits) - 1;
+    uint64_t offset = 0;
+    for (int i = 1; i <= 4; i++)
+        offset += half << (64 - i * bgbits);
+
+    uint32_t a_next = lwe[0];
+#pragma unroll 1
+    for (int i = 0; i < n; i++) {
+        const uint32_t bara = mod_switch_2n(a_next, 12);
+        a_next = lwe[i + 1];
+        // ---- A: row L on the warp pair (L, L + 4), branch br
+        {
+            const int L = warp & 3, h = warp >> 2;
+            const int Lv = 16 * h + (lane & 15), e = lane >> 4;
+            const int sh = 64 - (L + 1) * bgbits;
+            auto digit = [&](uint32_t q) -> double {
+                const uint32_t idx = (q - bara) & 4095u;
+                const uint64_t r = idx < 2048 ? sm.acc[idx] : 0ull - sm.acc[idx - 2048];
+                const uint64_t v = r - sm.acc[q] + offset;
+                return (double)(int32_t)(int64_t)(((v >> sh) & mask) - half);
+            };
+            double2 z[8];
+#pragma unroll
+            for (int t = 0; t < 8; t++) {
+                const uint32_t p = (uint32_t)(Lv + 32 * (t + 8 * e));
+                const double2 u = make_double2(digit(p), digit(p + 1024));
+                const double2 v = make_double2(digit(p + 512), digit(p + 1536));
+                z[t] = split_fwd(u, v, br);
+            }
+            double2* rg = sm.reg[L];
+            if (br == 0)
+                fft512_fwd_pair<1>(z, rg, sm.tw2, lane, h, 1 + L);
+            else
+                fft512_fwd_pair<2>(z, rg, sm.tw2, lane, h, 1 + L);
+            asm volatile("bar.sync %0, 64;" ::"r"(1 + L) : "memory");  // transpose reads done
+#pragma unroll
+            for (int t = 0; t < 8; t++)
+                rg[(2 * t + e) * 32 + Lv] = z[t];
+        }
+        __syncthreads();
+        // ---- B: partial MAC at this branch's 512 points, 2 per thread
+        {
+            const double2* K = bk2fd + (size_t)i * 8 * 4 * 1024 + (size_t)(4 * P) * 4 * 1024 +
+                               (size_t)br * 512;
+            double2 kc[16], kn[16];
+            auto load = [&](double2 (&kk)[16], int m) {
+                const int s = tid + 256 * m;
+#pragma unroll
+                for (int u = 0; u < 16; u++)
+                    kk[u] = __ldg(K + (size_t)u * 1024 + s);  // u = L * 4 + q
+            };
+            load(kc, 0);
+#pragma unroll
+            for (int m = 0; m < 2; m++) {
+                if (m < 1)
+                    load(kn, m + 1);
+                const int s = tid + 256 * m;
+                double2 o[4];
+#pragma unroll
+                for (int q = 0; q < 4; q++)
+                    o[q] = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int L = 0; L < 4; L++) {
+                    const double2 d = sm.reg[L][s];
+#pragma unroll
+                    for (int q = 0; q < 4; q++) {
+                        const double2 k = kc[L * 4 + q];
+                        o[q].x = fma(d.x, k.x, fma(-d.y, k.y, o[q].x));
+                        o[q].y = fma(d.x, k.y, fma(d.y, k.x, o[q].y));
+                    }
+                }
+                // own outputs in place of this thread's own row slots (only it reads them)
+#pragma unroll
+                for (int k = 0; k < 2; k++) {
+                    sm.reg[k][s] = P ? o[2 + k] : o[k];
+                    mac_peer->part[k][s] = P ? o[k] : o[2 + k];
+                }
+                asm volatile("" ::: "memory");
+                if (m < 1) {
+#pragma unroll
+                    for (int u = 0; u < 16; u++)
+                        kc[u] = kn[u];
+                }
+            }
+        }
+        cluster.sync();  // partials exchanged
+        // ---- C: own outputs k = 0, 1 (lo, hi) on warp pairs (k, k + 4); warps 2, 3, 6, 7
+        // idle here
+        {
+            const int k = warp & 3, h = warp >> 2;
+            if (k < 2) {
+                double2* rg = sm.reg[k];
+                const int Lv = 16 * h + (lane & 15), e = lane >> 4;
+                double2 u[8];
+#pragma unroll
+                for (int t = 0; t < 8; t++) {
+                    const int q = (2 * t + e) * 32 + Lv;
+                    const double2 mine = rg[q], oth = sm.part[k][q];
+                    u[t] = P == 0 ? make_double2(mine.x + oth.x, mine.y + oth.y)
+                                  : make_double2(oth.x + mine.x, oth.y + mine.y);
+                }
+                asm volatile("bar.sync %0, 64;" ::"r"(5 + k) : "memory");  // inputs read
+                if (br == 0)
+                    fft512_inv_pair<1>(u, rg, sm.tw2, lane, h, 5 + k);
+                else
+                    fft512_inv_pair<2>(u, rg, sm.tw2, lane, h, 5 + k);
+                asm volatile("bar.sync %0, 64;" ::"r"(5 + k) : "memory");  // transpose reads done
+#pragma unroll
+                for (int t = 0; t < 8; t++) {
+                    const int pos = Lv + 32 * (t + 8 * e);
+                    rg[pos] = u[t];
+                    br_peer->xin[k][pos] = u[t];
+                }
+            }
+        }
+        cluster.sync();  // both branches' inverse outputs in place
+        // ---- D: inverse split stage, exact rounding, lo/hi recombination into acc[P]
+        {
+            const double c = 0.70710678118654752440;
+#pragma unroll 1
+            for (int w = 0; w < 2; w++) {
+                const int p = tid + 256 * w;
+                int64_t part[2][4];
+#pragma unroll
+                for (int hh = 0; hh < 2; hh++) {
+                    const double2 mine = sm.reg[hh][p], oth = sm.xin[hh][p];
+                    const double2 A = br == 0 ? mine : oth, B = br == 0 ? oth : mine;
+                    const double2 uu = make_double2(A.x + B.x, A.y + B.y);
+                    const double dx = A.x - B.x, dy = A.y - B.y;
+                    const double2 vv = make_double2(c * (dx + dy), c * (dy - dx));
+                    part[hh][0] = __double2ll_rn(uu.x);  // coefficient p
+                    part[hh][1] = __double2ll_rn(vv.x);  // p + 512
+                    part[hh][2] = __double2ll_rn(uu.y);  // p + 1024
+                    part[hh][3] = __double2ll_rn(vv.y);  // p + 1536
+                }
+#pragma unroll
+                for (int e4 = 0; e4 < 4; e4++)
+                    sm.acc[p + 512 * e4] += (uint64_t)part[0][e4] + ((uint64_t)part[1][e4] << 32);
+            }
+        }
+        __syncthreads();
+    }
+    if (br == 0) {
+        uint64_t* dst = out + (size_t)task * 4096 + (size_t)P * 2048;
+        for (int q = tid; q < 2048; q += blockDim.x)
+            dst[q] = sm.acc[q];
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Batched private key switch (ops.cpp:681-708), fused with sampleExtract(acc2, 0)
 // and b += h/2 (ops.cpp:928-930).  Input task g: level-2 accumulator acc2[g]
 // (a[2048], b[2048] u64); out_rows[g] receives -sum_{i,j} table[i][j][d-1] for

@@ -109,7 +109,7 @@ double2 zeta_root(long double theta0, int d, uint32_t b)
 long double root_theta(int root) { return root == 0 ? kPi / 2 : root == 1 ? kPi / 4 : 5 * kPi / 4; }
 
 // tw1 (15 constants), their tangent forms, and the per-lane tw2 table [23][32] of one root.
-void twiddles(int root, double2* tw1, double2* tw1t, std::vector<double2>& tw2)
+void twiddles(int root, double2* tw1, double2* tw1t, double2* tw1a, std::vector<double2>& tw2)
 {
     const long double t0 = root_theta(root);
     for (int d = 0; d < 4; d++)
@@ -123,6 +123,7 @@ void twiddles(int root, double2* tw1, double2* tw1t, std::vector<double2>& tw2)
             tw1t[(1 << d) - 1 + b] =
                 tw_form_a(root, d, b) ? make_double2((double)cosl(a), (double)tanl(a))
                                       : make_double2((double)sinl(a), (double)(cosl(a) / sinl(a)));
+            tw1a[(1 << d) - 1 + b] = make_double2((double)cosl(a), (double)tanl(a));
         }
     // compressed per-lane table (fft512.cuh, kTw2Entries): store the q = 0 twiddles and
     // check that every q = 1 twiddle is i times a stored one
@@ -318,17 +319,22 @@ void set_br_attr()
 
 constexpr int kChainWarps = 8;
 
-// Level-2 blind rotation of T tasks: the two-CTA cluster kernel (one SM per accumulator
-// polynomial, br2c_kernel) unless VSP_BR2_CLUSTER=0 selects the one-CTA br2_kernel.
+// Level-2 blind rotation of T tasks on a cluster of 4 CTAs per task (br2q_kernel: one SM
+// per (accumulator polynomial, split branch)).  VSP_BR2_CLUSTER = 2 selects the two-CTA
+// br2c_kernel, 0 the one-CTA br2_kernel (comparisons).
 void launch_br2(vsp_ctx* c, const uint32_t* d_lwe, int ninputs, const uint64_t* d_hv, int T,
                 uint64_t* d_acc, cudaStream_t st)
 {
-    static const bool single = getenv("VSP_BR2_CLUSTER") && atoi(getenv("VSP_BR2_CLUSTER")) == 0;
-    if (single)
+    static const int cl = getenv("VSP_BR2_CLUSTER") ? atoi(getenv("VSP_BR2_CLUSTER")) : 4;
+    if (cl == 0)
         br2_kernel<<<T, 256, sizeof(Br2Smem), st>>>(d_lwe, ninputs, d_hv, c->d_bk2fd, c->d_tw2,
                                                      d_acc, (int)c->p.n, (int)c->p.Bg2Bits);
-    else
+    else if (cl == 2)
         br2c_kernel<<<2 * T, 256, sizeof(Br2cSmem), st>>>(d_lwe, ninputs, d_hv, c->d_bk2fd,
+                                                            c->d_tw2, d_acc, (int)c->p.n,
+                                                            (int)c->p.Bg2Bits);
+    else
+        br2q_kernel<<<4 * T, 256, sizeof(Br2qSmem), st>>>(d_lwe, ninputs, d_hv, c->d_bk2fd,
                                                             c->d_tw2, d_acc, (int)c->p.n,
                                                             (int)c->p.Bg2Bits);
     VSP_CUDA_CHECK(cudaGetLastError());
@@ -563,6 +569,8 @@ void configure_kernels()
                                         (int)sizeof(Br2Smem)));
     VSP_CUDA_CHECK(cudaFuncSetAttribute(br2c_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)sizeof(Br2cSmem)));
+    VSP_CUDA_CHECK(cudaFuncSetAttribute(br2q_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)sizeof(Br2qSmem)));
     VSP_CUDA_CHECK(cudaFuncSetAttribute(cmux_chain1024_kernel<kChainWarps, 0>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)sizeof(Chain1024Smem<kChainWarps>)));
@@ -1178,15 +1186,16 @@ vsp_ctx* vsp_create(const vsp_params* params, int device)
         VSP_CUDA_CHECK(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device));
         VSP_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         // twiddles of the 512-point negacyclic transform
-        double2 tw1[3][15], tw1t[3][15];
+        double2 tw1[3][15], tw1t[3][15], tw1a[3][15];
         std::vector<double2> tw2all;
         for (int root = 0; root < 3; root++) {
             std::vector<double2> tw2;
-            twiddles(root, tw1[root], tw1t[root], tw2);
+            twiddles(root, tw1[root], tw1t[root], tw1a[root], tw2);
             tw2all.insert(tw2all.end(), tw2.begin(), tw2.end());
         }
         VSP_CUDA_CHECK(cudaMemcpyToSymbol(c_tw1, tw1, sizeof(tw1)));
         VSP_CUDA_CHECK(cudaMemcpyToSymbol(c_tw1t, tw1t, sizeof(tw1t)));
+        VSP_CUDA_CHECK(cudaMemcpyToSymbol(c_tw1a, tw1a, sizeof(tw1a)));
         VSP_CUDA_CHECK(cudaMalloc(&c->d_tw2, tw2all.size() * sizeof(double2)));
         VSP_CUDA_CHECK(cudaMemcpy(c->d_tw2, tw2all.data(), tw2all.size() * sizeof(double2),
                                   cudaMemcpyHostToDevice));
