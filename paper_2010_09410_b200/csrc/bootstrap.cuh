@@ -66,6 +66,9 @@ struct Br1024Smem {
     uint32_t dig[WARPS][16 * 32];  // level-1 digits, packed 2 x 16-bit offset binary
     uint64_t full[S];
     uint32_t cnt[S];
+    uint64_t tfull[2];  // TM variant: chunk copied into TMEM slot (tcgen05.commit)
+    uint32_t tcnt[2];   // TM variant: warps done with a TMEM slot
+    uint32_t taddr;     // TM variant: TMEM base (256 columns: two 128-column slots)
 };
 
 // (X^k p)[q] mod X^N + 1 (polyRotate, poly.hpp:32-48) = +-p[(q-k) mod 2N]; qk = q - k.
@@ -77,11 +80,19 @@ __device__ __forceinline__ uint32_t rot_coef1024(const uint32_t* src, uint32_t q
     return (x ^ (0u - neg)) + neg;
 }
 
-template <int WARPS, int S, int BG>
+// TM: the bootstrapping-key rows reach the warps through TENSOR MEMORY instead of shared-
+// memory loads: each 16 KiB chunk, staged in smem by the bulk-copy engine (S = 3 slots), is
+// copied once per CTA into one of two 128-column TMEM slots by tcgen05.cp (multicast to the
+// four warp quadrants; every warp needs the same per-lane data) and each warp reads its
+// lane's 32 values with tcgen05.ld -- the key no longer crosses the shared-memory read
+// port once per warp.  The last warp to release TMEM slot c % 2 issues the copy of chunk
+// c + 2 into it and the bulk copy of chunk c + 3 into the smem slot chunk c has vacated.
+template <int WARPS, int S, int BG, bool TM = false>
 __global__ void __launch_bounds__(WARPS * 32, 1)
     br1024_kernel(const uint32_t* __restrict__ tasks, const double2* __restrict__ bkfd,
                   const double2* __restrict__ tw2g, uint32_t* __restrict__ out, int T, int n)
 {
+    static_assert(!TM || S == 3, "TM uses a three-slot smem ring");
     extern __shared__ __align__(128) uint8_t smem_raw[];
     auto& sm = *reinterpret_cast<Br1024Smem<WARPS, S>*>(smem_raw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -99,12 +110,43 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
             mbar_init(&sm.full[s], 1);
             sm.cnt[s] = 0;
         }
+        if constexpr (TM) {
+            for (int s = 0; s < 2; s++) {
+                mbar_init(&sm.tfull[s], 1);
+                sm.tcnt[s] = 0;
+            }
+        }
+    }
+    if constexpr (TM) {
+        if (warp == 0) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+                             smem_u32(&sm.taddr))
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        }
+        tmem_fence_before();
     }
     __syncthreads();
+    if constexpr (TM)
+        tmem_fence_after();
+    // TM: copy chunk cn (smem slot cn % S) into TMEM slot cn % 2, completion on tfull
+    auto issue_cp = [&](int cn) {
+        const int s3 = cn % S;
+        mbar_wait(&sm.full[s3], (uint32_t)((cn / S) & 1));
+        const uint32_t tb = sm.taddr + (uint32_t)((cn & 1) * 128);
+#pragma unroll 1
+        for (int q = 0; q < 32; q++)  // row q = (poly, j): 32 lanes x 16 bytes
+            tmem_cp_32x128b_x4(tb + (uint32_t)(q * 4), &sm.ring[s3][q * 32]);
+        tmem_commit(&sm.tfull[cn & 1]);
+    };
     if (threadIdx.x == 0) {
         for (int s = 0; s < S && s < nchunks; s++) {
             mbar_arrive_expect_tx(&sm.full[s], 16384);
             bulk_g2s(sm.ring[s], bkfd + (size_t)s * 1024, 16384, &sm.full[s]);
+        }
+        if constexpr (TM) {
+            for (int cn = 0; cn < 2 && cn < nchunks; cn++)
+                issue_cp(cn);
         }
     }
 
@@ -134,6 +176,26 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
 
     // Slot release: the last warp to finish with chunk c refills its slot with c + S.
     auto release = [&](int c) {
+        if constexpr (TM) {
+            tmem_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                const uint32_t old = atomicAdd(&sm.tcnt[c & 1], 1u);
+                if (old == WARPS - 1) {
+                    sm.tcnt[c & 1] = 0;
+                    tmem_fence_after();
+                    if (c + 2 < nchunks)
+                        issue_cp(c + 2);
+                    if (c + S < nchunks) {  // chunk c's smem slot: read by its (finished) copy
+                        const int s3 = c % S;
+                        fence_proxy_async();
+                        mbar_arrive_expect_tx(&sm.full[s3], 16384);
+                        bulk_g2s(sm.ring[s3], bkfd + (size_t)(c + S) * 1024, 16384, &sm.full[s3]);
+                    }
+                }
+            }
+            return;
+        }
         __syncwarp();
         if (lane == 0) {
             const int s = c % S;
@@ -202,17 +264,46 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
                     load_digits1(z);
                 fft512_fwd(z, xbuf, sm.tw2, lane);
                 const int c = c0 + P * 2 + lvl;
-                const int s = c % S;
-                mbar_wait(&sm.full[s], (uint32_t)((c / S) & 1));
-                const double2* bk = sm.ring[s];
+                if constexpr (TM) {
+                    mbar_wait(&sm.tfull[c & 1], (uint32_t)((c >> 1) & 1));
+                    tmem_fence_after();
+                    const uint32_t tb = sm.taddr + ((uint32_t)(32 * (warp & 3)) << 16) +
+                                        (uint32_t)((c & 1) * 128);
 #pragma unroll
-                for (int j = 0; j < 16; j++) {
-                    const double2 ba = bk[j * 32 + lane];
-                    const double2 bb = bk[512 + j * 32 + lane];
-                    accA[j].x = fma(z[j].x, ba.x, fma(-z[j].y, ba.y, accA[j].x));
-                    accA[j].y = fma(z[j].x, ba.y, fma(z[j].y, ba.x, accA[j].y));
-                    accB[j].x = fma(z[j].x, bb.x, fma(-z[j].y, bb.y, accB[j].x));
-                    accB[j].y = fma(z[j].x, bb.y, fma(z[j].y, bb.x, accB[j].y));
+                    for (int jb = 0; jb < 16; jb += 4) {
+                        uint32_t ra[16], rb[16];
+                        tmem_ld_x16(tb + (uint32_t)(jb * 4), ra);         // poly a, j..j+3
+                        tmem_ld_x16(tb + (uint32_t)((16 + jb) * 4), rb);  // poly b
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int u = 0; u < 4; u++) {
+                            const int j = jb + u;
+                            const double2 ba = make_double2(
+                                __hiloint2double((int)ra[4 * u + 1], (int)ra[4 * u]),
+                                __hiloint2double((int)ra[4 * u + 3], (int)ra[4 * u + 2]));
+                            const double2 bb = make_double2(
+                                __hiloint2double((int)rb[4 * u + 1], (int)rb[4 * u]),
+                                __hiloint2double((int)rb[4 * u + 3], (int)rb[4 * u + 2]));
+                            accA[j].x = fma(z[j].x, ba.x, fma(-z[j].y, ba.y, accA[j].x));
+                            accA[j].y = fma(z[j].x, ba.y, fma(z[j].y, ba.x, accA[j].y));
+                            accB[j].x = fma(z[j].x, bb.x, fma(-z[j].y, bb.y, accB[j].x));
+                            accB[j].y = fma(z[j].x, bb.y, fma(z[j].y, bb.x, accB[j].y));
+                        }
+                    }
+                }
+                else {
+                    const int s = c % S;
+                    mbar_wait(&sm.full[s], (uint32_t)((c / S) & 1));
+                    const double2* bk = sm.ring[s];
+#pragma unroll
+                    for (int j = 0; j < 16; j++) {
+                        const double2 ba = bk[j * 32 + lane];
+                        const double2 bb = bk[512 + j * 32 + lane];
+                        accA[j].x = fma(z[j].x, ba.x, fma(-z[j].y, ba.y, accA[j].x));
+                        accA[j].y = fma(z[j].x, ba.y, fma(z[j].y, ba.x, accA[j].y));
+                        accB[j].x = fma(z[j].x, bb.x, fma(-z[j].y, bb.y, accB[j].x));
+                        accB[j].y = fma(z[j].x, bb.y, fma(z[j].y, bb.x, accB[j].y));
+                    }
                 }
                 release(c);
             }
@@ -238,6 +329,13 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
         const uint4* s4 = reinterpret_cast<const uint4*>(acc);
         for (int q = lane; q < 512; q += 32)
             dst[q] = s4[q];
+    }
+    if constexpr (TM) {
+        tmem_fence_before();
+        __syncthreads();
+        if (warp == 0)
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(sm.taddr)
+                         : "memory");
     }
 }
 

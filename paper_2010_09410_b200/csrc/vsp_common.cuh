@@ -83,6 +83,52 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
+// ---------------------------------------------------------------------------
+// Tensor memory (tcgen05) helpers: allocation, smem -> TMEM copies, TMEM -> register loads.
+
+// Shared-memory matrix descriptor (no swizzle, sm100 version 1) for tcgen05.cp: rows of
+// 16 bytes, 8-row core matrices `sbo` bytes apart.
+__device__ __forceinline__ uint64_t tmem_desc_noswizzle(const void* p, uint32_t sbo)
+{
+    uint64_t d = (uint64_t)((smem_u32(p) >> 4) & 0x3FFF);
+    d |= (uint64_t)((128u >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;
+    return d;
+}
+
+// 32 rows x 16 bytes of smem (row r = lane r) -> TMEM columns [col, col + 4) of lanes
+// 32q + r in all four warp quadrants (multicast).
+__device__ __forceinline__ void tmem_cp_32x128b_x4(uint32_t taddr, const void* src)
+{
+    asm volatile("tcgen05.cp.cta_group::1.32x128b.warpx4 [%0], %1;" ::"r"(taddr),
+                 "l"(tmem_desc_noswizzle(src, 128))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tmem_commit(uint64_t* bar)
+{
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tmem_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// 16 consecutive TMEM columns of this thread's lane -> 4 double2 (after tmem_wait_ld).
+__device__ __forceinline__ void tmem_ld_x16(uint32_t taddr, uint32_t (&r)[16])
+{
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+        "%11, %12, %13, %14, %15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+          "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+}
+
 // modSwitch(2N, phase) (ops.cpp:49-55) for 2N = 2^log2_2N: the reference computes
 // ((phase<<32) + interval/2) / interval with interval = 2^(64-log2_2N), wrapping
 // mod 2^64; that equals (phase + 2^(31-log2_2N)) >> (32-log2_2N) in u32 arithmetic.
