@@ -66,9 +66,10 @@ struct Br1024Smem {
     uint32_t dig[WARPS][16 * 32];  // level-1 digits, packed 2 x 16-bit offset binary
     uint64_t full[S];
     uint32_t cnt[S];
-    uint64_t tfull[2];  // TM variant: chunk copied into TMEM slot (tcgen05.commit)
-    uint32_t tcnt[2];   // TM variant: warps done with a TMEM slot
-    uint32_t taddr;     // TM variant: TMEM base (256 columns: two 128-column slots)
+    uint64_t tfull[3];  // TM variant: chunk copied into TMEM slot (tcgen05.commit)
+    uint32_t tcnt[3];   // TM variant: warps done with a TMEM slot
+    uint32_t tstart[3]; // TM variant: warps that started a chunk (the first refills smem)
+    uint32_t taddr;     // TM variant: TMEM base (512 columns: three 128-column slots)
 };
 
 // (X^k p)[q] mod X^N + 1 (polyRotate, poly.hpp:32-48) = +-p[(q-k) mod 2N]; qk = q - k.
@@ -82,11 +83,12 @@ __device__ __forceinline__ uint32_t rot_coef1024(const uint32_t* src, uint32_t q
 
 // TM: the bootstrapping-key rows reach the warps through TENSOR MEMORY instead of shared-
 // memory loads: each 16 KiB chunk, staged in smem by the bulk-copy engine (S = 3 slots), is
-// copied once per CTA into one of two 128-column TMEM slots by tcgen05.cp (multicast to the
-// four warp quadrants; every warp needs the same per-lane data) and each warp reads its
+// copied once per CTA into one of three 128-column TMEM slots by tcgen05.cp (multicast to
+// the four warp quadrants; every warp needs the same per-lane data) and each warp reads its
 // lane's 32 values with tcgen05.ld -- the key no longer crosses the shared-memory read
-// port once per warp.  The last warp to release TMEM slot c % 2 issues the copy of chunk
-// c + 2 into it and the bulk copy of chunk c + 3 into the smem slot chunk c has vacated.
+// port once per warp.  Chunk c lives in smem slot and TMEM slot c % 3: the first warp to
+// start chunk c (its copy is complete) bulk-loads chunk c + 3 into the smem slot, the last
+// warp to finish it copies chunk c + 3 into the TMEM slot.
 template <int WARPS, int S, int BG, bool TM = false>
 __global__ void __launch_bounds__(WARPS * 32, 1)
     br1024_kernel(const uint32_t* __restrict__ tasks, const double2* __restrict__ bkfd,
@@ -111,15 +113,16 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
             sm.cnt[s] = 0;
         }
         if constexpr (TM) {
-            for (int s = 0; s < 2; s++) {
+            for (int s = 0; s < 3; s++) {
                 mbar_init(&sm.tfull[s], 1);
                 sm.tcnt[s] = 0;
+                sm.tstart[s] = 0;
             }
         }
     }
     if constexpr (TM) {
         if (warp == 0) {
-            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
                              smem_u32(&sm.taddr))
                          : "memory");
             asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
@@ -129,15 +132,15 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     __syncthreads();
     if constexpr (TM)
         tmem_fence_after();
-    // TM: copy chunk cn (smem slot cn % S) into TMEM slot cn % 2, completion on tfull
+    // TM: copy chunk cn (smem slot cn % 3) into TMEM slot cn % 3, completion on tfull
     auto issue_cp = [&](int cn) {
-        const int s3 = cn % S;
-        mbar_wait(&sm.full[s3], (uint32_t)((cn / S) & 1));
-        const uint32_t tb = sm.taddr + (uint32_t)((cn & 1) * 128);
+        const int s3 = cn % 3;
+        mbar_wait(&sm.full[s3], (uint32_t)((cn / 3) & 1));
+        const uint32_t tb = sm.taddr + (uint32_t)(s3 * 128);
 #pragma unroll 1
         for (int q = 0; q < 32; q++)  // row q = (poly, j): 32 lanes x 16 bytes
             tmem_cp_32x128b_x4(tb + (uint32_t)(q * 4), &sm.ring[s3][q * 32]);
-        tmem_commit(&sm.tfull[cn & 1]);
+        tmem_commit(&sm.tfull[s3]);
     };
     if (threadIdx.x == 0) {
         for (int s = 0; s < S && s < nchunks; s++) {
@@ -145,7 +148,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
             bulk_g2s(sm.ring[s], bkfd + (size_t)s * 1024, 16384, &sm.full[s]);
         }
         if constexpr (TM) {
-            for (int cn = 0; cn < 2 && cn < nchunks; cn++)
+            for (int cn = 0; cn < 3 && cn < nchunks; cn++)
                 issue_cp(cn);
         }
     }
@@ -180,18 +183,13 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
             tmem_fence_before();
             __syncwarp();
             if (lane == 0) {
-                const uint32_t old = atomicAdd(&sm.tcnt[c & 1], 1u);
+                const int s3 = c % 3;
+                const uint32_t old = atomicAdd(&sm.tcnt[s3], 1u);
                 if (old == WARPS - 1) {
-                    sm.tcnt[c & 1] = 0;
+                    sm.tcnt[s3] = 0;
                     tmem_fence_after();
-                    if (c + 2 < nchunks)
-                        issue_cp(c + 2);
-                    if (c + S < nchunks) {  // chunk c's smem slot: read by its (finished) copy
-                        const int s3 = c % S;
-                        fence_proxy_async();
-                        mbar_arrive_expect_tx(&sm.full[s3], 16384);
-                        bulk_g2s(sm.ring[s3], bkfd + (size_t)(c + S) * 1024, 16384, &sm.full[s3]);
-                    }
+                    if (c + 3 < nchunks)
+                        issue_cp(c + 3);  // TMEM slot free; waits for the bulk load of c + 3
                 }
             }
             return;
@@ -265,10 +263,24 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
                 fft512_fwd(z, xbuf, sm.tw2, lane);
                 const int c = c0 + P * 2 + lvl;
                 if constexpr (TM) {
-                    mbar_wait(&sm.tfull[c & 1], (uint32_t)((c >> 1) & 1));
+                    const int s3 = c % 3;
+                    mbar_wait(&sm.tfull[s3], (uint32_t)((c / 3) & 1));
                     tmem_fence_after();
+                    if (lane == 0 && c + 3 < nchunks) {
+                        // the first warp to start chunk c refills its smem slot with c + 3
+                        // (chunk c's copy into TMEM has completed)
+                        const uint32_t st = atomicAdd(&sm.tstart[s3], 1u);
+                        if (st == 0) {
+                            fence_proxy_async();
+                            mbar_arrive_expect_tx(&sm.full[s3], 16384);
+                            bulk_g2s(sm.ring[s3], bkfd + (size_t)(c + 3) * 1024, 16384,
+                                     &sm.full[s3]);
+                        }
+                        if (st == WARPS - 1)
+                            atomicExch(&sm.tstart[s3], 0u);
+                    }
                     const uint32_t tb = sm.taddr + ((uint32_t)(32 * (warp & 3)) << 16) +
-                                        (uint32_t)((c & 1) * 128);
+                                        (uint32_t)(s3 * 128);
 #pragma unroll
                     for (int jb = 0; jb < 16; jb += 4) {
                         uint32_t ra[16], rb[16];
@@ -334,7 +346,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
         tmem_fence_before();
         __syncthreads();
         if (warp == 0)
-            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(sm.taddr)
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(sm.taddr)
                          : "memory");
     }
 }

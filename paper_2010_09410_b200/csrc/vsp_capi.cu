@@ -298,7 +298,7 @@ int br_warps_for(int T, int sms)
 }
 
 // VSP_BR_TMEM=1: the bootstrapping key reaches the warps through tensor memory (br1024
-// TM variant, W >= 4: at most two CTAs per SM, 256 TMEM columns each).
+// TM variant, W >= 5: one CTA per SM, all 512 TMEM columns).
 bool br_tmem()
 {
     static const bool on = getenv("VSP_BR_TMEM") && atoi(getenv("VSP_BR_TMEM")) == 1;
@@ -308,7 +308,7 @@ bool br_tmem()
 template <int W>
 void launch_br_w(vsp_ctx* c, const uint32_t* d_tasks, uint32_t* d_trlwe, int T, cudaStream_t st)
 {
-    if constexpr (W >= 4) {
+    if constexpr (W >= 5) {
         if (br_tmem()) {
             br1024_kernel<W, 3, kBrBg, true><<<(T + W - 1) / W, W * 32, sizeof(Br1024Smem<W, 3>),
                                                st>>>(d_tasks, c->d_bk1fd, c->d_tw2, d_trlwe, T,
@@ -331,7 +331,7 @@ void set_br_attr()
     // key-switch CTAs that co-run with the remainder wave
     VSP_CUDA_CHECK(cudaFuncSetAttribute(br1024_kernel<W, kBrSlots, kBrBg>,
                                         cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    if constexpr (W >= 4) {
+    if constexpr (W >= 5) {
         VSP_CUDA_CHECK(cudaFuncSetAttribute(br1024_kernel<W, 3, kBrBg, true>,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)sizeof(Br1024Smem<W, 3>)));
