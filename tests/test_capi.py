@@ -43,3 +43,16 @@ def test_engine_fails_loudly_without_device():
         pass
     with pytest.raises(RuntimeError):
         vsp.Engine("test-det")
+
+
+def test_gate_kind_ids_names_ints_and_arrays():
+    """GateKind ids (ops.hpp:183-194) from names, ints or an int array (the array path
+    does no per-gate Python work); unknown names raise like homGate."""
+    import numpy as np
+    ids = vsp.Engine._kind_ids(["AND", "MUX", "XOR", 5])
+    assert ids.dtype == np.int32 and list(ids) == [0, 2, 9, 5]
+    arr = np.array([3, 9, 9, 3], np.int64)
+    out = vsp.Engine._kind_ids(arr)
+    assert out.dtype == np.int32 and out.flags["C_CONTIGUOUS"] and list(out) == [3, 9, 9, 3]
+    with pytest.raises(ValueError):
+        vsp.Engine._kind_ids(["NAND", "XAND"])
