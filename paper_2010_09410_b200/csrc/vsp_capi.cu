@@ -698,15 +698,20 @@ void hom_gate_dev(vsp_ctx* c, const int32_t* kinds, const uint32_t* d_in, uint32
         c->launches++;
     };
     // first gate with a task >= t (NOT gates belong to the preceding task range)
-    auto gate_of_task = [&](int t) -> size_t {
-        size_t g = 0;
-        while (g < G) {
+    // tasks_end[g] = tasks of gates [0, g]; the first gate with a task >= t is the first g
+    // with tasks_end[g] > t (binary search; gates' tasks are assigned in gate order)
+    std::vector<int> tasks_end;
+    if (io) {
+        tasks_end.resize(G);
+        int acc_t = 0;
+        for (size_t g = 0; g < G; g++) {
             const int2 tt = pl.gtask[g];
-            if (tt.x >= 0 && std::max(tt.x, tt.y) >= t)
-                break;
-            g++;
+            acc_t += tt.x < 0 ? 0 : (tt.y >= 0 ? 2 : 1);
+            tasks_end[g] = acc_t;
         }
-        return g;
+    }
+    auto gate_of_task = [&](int t) -> size_t {
+        return (size_t)(std::upper_bound(tasks_end.begin(), tasks_end.end(), t) - tasks_end.begin());
     };
     size_t prepped = 0;
     std::function<void(int, int)> before_part;
