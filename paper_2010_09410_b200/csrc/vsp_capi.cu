@@ -230,6 +230,25 @@ struct vsp_ctx {
             VSP_CUDA_CHECK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     }
 
+    // The context's scratch buffers are shared by all calls: a call on a different stream
+    // than the previous one first waits for the previous call's work (ev_last).
+    cudaEvent_t ev_last = nullptr;
+    cudaStream_t last_stream = nullptr;
+    bool has_last = false;
+    void stream_enter(cudaStream_t st)
+    {
+        if (has_last && st != last_stream)
+            VSP_CUDA_CHECK(cudaStreamWaitEvent(st, ev_last, 0));
+    }
+    void stream_leave(cudaStream_t st)
+    {
+        if (!ev_last)
+            VSP_CUDA_CHECK(cudaEventCreateWithFlags(&ev_last, cudaEventDisableTiming));
+        VSP_CUDA_CHECK(cudaEventRecord(ev_last, st));
+        last_stream = st;
+        has_last = true;
+    }
+
     void set_device() const { VSP_CUDA_CHECK(cudaSetDevice(device)); }
     size_t ksk_words() const
     {
@@ -1272,6 +1291,8 @@ void vsp_destroy(vsp_ctx* c)
         for (cudaEvent_t e : {c->ev_fork, c->ev_join, c->ev_full, c->ev_rem})
             cudaEventDestroy(e);
     }
+    if (c->ev_last)
+        cudaEventDestroy(c->ev_last);
     cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -1372,8 +1393,10 @@ int vsp_hom_gate_batch_dev(vsp_ctx* c, const int32_t* kinds, const uint32_t* d_i
     return guard([&] {
         std::lock_guard<std::mutex> lk(c->mu);
         c->set_device();
+        c->stream_enter(static_cast<cudaStream_t>(stream));
         cudaStream_t st = static_cast<cudaStream_t>(stream);
         hom_gate_dev(c, kinds, d_in, d_out, G, st);
+        c->stream_leave(static_cast<cudaStream_t>(stream));
     });
 }
 
@@ -1383,6 +1406,7 @@ int vsp_hom_gate_batch(vsp_ctx* c, const int32_t* kinds, const uint32_t* in, uin
     return guard([&] {
         std::lock_guard<std::mutex> lk(c->mu);
         c->set_device();
+        c->stream_enter(c->stream);
         for (size_t g = 0; g < G; g++)
             if (kinds[g] < 0 || kinds[g] > kXor)
                 throw std::invalid_argument("homGate: unknown kind");
@@ -1606,6 +1630,7 @@ int vsp_ram_cycle(vsp_ctx* c, uint32_t v, uint32_t w, uint32_t* ram, const uint3
     return guard([&] {
         std::lock_guard<std::mutex> lk(c->mu);
         c->set_device();
+        c->stream_enter(c->stream);
         const Params& p = c->p;
         const size_t n1 = p.n + 1, cw = 2 * (size_t)p.N1, cells = (size_t)w << v;
         if (v == 0 || w == 0)
@@ -1636,10 +1661,12 @@ int vsp_ram_cycle_dev(vsp_ctx* c, uint32_t v, uint32_t w, uint32_t* d_ram, const
     return guard([&] {
         std::lock_guard<std::mutex> lk(c->mu);
         c->set_device();
+        c->stream_enter(static_cast<cudaStream_t>(stream));
         if (v == 0 || w == 0)
             throw std::invalid_argument("ramCycle: address width mismatch");
         ram_cycle_dev(c, d_ram, (int)v, (int)w, d_addr, d_wflag, d_wdata, d_readout,
                       static_cast<cudaStream_t>(stream));
+        c->stream_leave(static_cast<cudaStream_t>(stream));
     });
 }
 
@@ -1652,11 +1679,13 @@ int vsp_mem_ports_dev(vsp_ctx* c, uint32_t depth_bytes, const uint32_t* d_luts, 
     return guard([&] {
         std::lock_guard<std::mutex> lk(c->mu);
         c->set_device();
+        c->stream_enter(static_cast<cudaStream_t>(stream));
         if (v == 0 || w == 0)
             throw std::invalid_argument("ramCycle: address width mismatch");
         mem_pair_dev(c, d_luts, (int)nluts, depth_bytes, d_rom_addr, (int)vrom, d_rom_out, d_ram,
                      (int)v, (int)w, d_ram_addr, d_wflag, d_wdata, d_readout,
                      static_cast<cudaStream_t>(stream));
+        c->stream_leave(static_cast<cudaStream_t>(stream));
     });
 }
 
@@ -1666,8 +1695,10 @@ int vsp_rom_read_dev(vsp_ctx* c, uint32_t depth_bytes, const uint32_t* d_luts, u
     return guard([&] {
         std::lock_guard<std::mutex> lk(c->mu);
         c->set_device();
+        c->stream_enter(static_cast<cudaStream_t>(stream));
         rom_read_dev(c, d_luts, (int)nluts, depth_bytes, d_addr, (int)vrom, d_out,
                      static_cast<cudaStream_t>(stream));
+        c->stream_leave(static_cast<cudaStream_t>(stream));
     });
 }
 
@@ -1677,6 +1708,7 @@ int vsp_rom_read(vsp_ctx* c, uint32_t depth_bytes, const uint32_t* luts, uint32_
     return guard([&] {
         std::lock_guard<std::mutex> lk(c->mu);
         c->set_device();
+        c->stream_enter(c->stream);
         const Params& p = c->p;
         const size_t n1 = p.n + 1, cw = 2 * (size_t)p.N1;
         uint32_t* d_luts = c->romio.as<uint32_t>(std::max<size_t>(nluts, 1) * cw);
@@ -1941,6 +1973,7 @@ int vsp_netlist_run(vsp_netlist* nl, uint64_t cycles, double* stats)
         vsp_ctx* c = nl->ctx;
         std::lock_guard<std::mutex> lk(c->mu);
         c->set_device();
+        c->stream_enter(c->stream);
         cudaEvent_t a, b;
         VSP_CUDA_CHECK(cudaEventCreate(&a));
         VSP_CUDA_CHECK(cudaEventCreate(&b));
@@ -2137,8 +2170,10 @@ int vsp_hom_gate_level_dev(vsp_ctx* c, const int32_t* kinds, const uint32_t* d_i
     return guard([&] {
         std::lock_guard<std::mutex> lk(c->mu);
         c->set_device();
+        c->stream_enter((cudaStream_t)stream);
         hom_gate_level_dev(c, kinds, d_in, d_out, G, (cudaStream_t)stream);
         VSP_CUDA_CHECK(cudaGetLastError());
+        c->stream_leave((cudaStream_t)stream);
     });
 }
 
