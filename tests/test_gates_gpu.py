@@ -226,3 +226,31 @@ def test_not_only_and_mux_heavy_batches_tfhe80(prod):
     out = e.hom_gate_batch(["MUX"] * G, ins)
     want = np.array([TRUTH["MUX"](*(int(v) for v in b)) for b in mb])
     assert np.array_equal(vsp.decrypt(k["lv0"], out), want)
+
+
+def test_back_to_back_calls_on_different_streams(prod):
+    """Two device calls on two streams without a host sync in between: the second waits for
+    the first (the context's scratch buffers are shared), both results are right."""
+    import torch
+    e, o = prod
+    k = oracle_keys("tfhe-80", 20200729, False)
+    p = vsp.ParameterSet("tfhe-80")
+    rng = np.random.default_rng(77)
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    jobs = []
+    for G in (1500, 300):
+        kid = rng.integers(0, len(GATE_KINDS), G).astype(np.int32)
+        bits = rng.integers(0, 2, size=(G, 3)).astype(np.uint8)
+        ins = vsp.encrypt(p, k["lv0"], bits.reshape(-1), G).reshape(G, 3, p.n + 1)
+        d_in = torch.from_numpy(ins.view(np.int32)).cuda()
+        d_out = torch.empty((G, p.n + 1), dtype=torch.int32, device="cuda")
+        want = np.array([TRUTH[GATE_KINDS[kk]](*(int(x) for x in b)) for kk, b in zip(kid, bits)])
+        jobs.append((kid, d_in, d_out, G, want))
+    torch.cuda.synchronize()
+    for s, (kid, d_in, d_out, G, _) in zip(streams, jobs):  # no host sync in between
+        e.hom_gate_batch_dev(kid, d_in.data_ptr(), d_out.data_ptr(), G, s.cuda_stream)
+    outs = [j[2] for j in jobs]
+    wants = [j[4] for j in jobs]
+    torch.cuda.synchronize()
+    for d_out, want in zip(outs, wants):
+        assert np.array_equal(vsp.decrypt(k["lv0"], d_out.cpu().numpy().view(np.uint32)), want)
