@@ -846,7 +846,7 @@ void cb_batch(vsp_ctx* c, const uint32_t* d_lwe, int C, uint32_t* d_out, cudaStr
     VSP_CUDA_CHECK(cudaMemsetAsync(d_out, 0, (size_t)C * 2 * l * 2 * N1 * 4, st));
     const int islices = std::min<int>(64, (int)N2 + 1);
     const dim3 grid(islices, (unsigned)((2 * N1 + 511) / 512), 2);
-    constexpr int kPksGT = 16;  // gates per tile: 16 keeps 3+ CTAs per SM (more gathers in flight)
+    constexpr int kPksGT = 8;  // gates per tile: fewer registers, more CTAs and gathers in flight (16: 2.07 ms, 8: 1.54, 4: 1.85 per access)
     const size_t smem = (size_t)((N2 + 1 + islices - 1) / islices) * kPksGT * 4;
     timed(c, "pks", st, [&] {
         pks_kernel<kPksGT><<<grid, 256, smem, st>>>(d_acc2, d_hv, T2, c->d_pks[0], c->d_pks[1], d_out,
