@@ -1293,6 +1293,11 @@ void vsp_destroy(vsp_ctx* c)
     }
     if (c->ev_last)
         cudaEventDestroy(c->ev_last);
+    for (auto& kv : c->timers)  // profiling events never read back
+        for (auto& e : kv.second.pending) {
+            cudaEventDestroy(e.first);
+            cudaEventDestroy(e.second);
+        }
     cudaStreamDestroy(c->stream);
     delete c;
 }
