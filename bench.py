@@ -305,6 +305,19 @@ def run_ours(args, world, rank, local):
                 "peak_source": "measured live: vsp_fp64_peak_probe (DFMA loop) on this GPU",
                 "flops_per_launch": flops,
                 "flops_rule": "G * n * F_EP, F_EP = (2l+2)*5*M*log2 M + 2l*2*8*M = 171008"}
+    # the kernel's other ceiling: shared-memory wavefronts (1 per SM-cycle).  Per external
+    # product of one task it moves 2,080 of them by design (key 512, transposes
+    # 768, twiddles 240, accumulator 256, level-1 digits 64, conflicts ~20) + 192 shuffles
+    sm_clk = float((clk or {}).get("sm_max_mhz") or 1965.0) * 1e6
+    props = torch.cuda.get_device_properties(local)
+    wf = 2080.0 * G * p.n
+    wf_rate = wf / (avg_br * 1e-3)
+    wf_peak = props.multi_processor_count * sm_clk
+    roofline["secondary"] = {"bound": "smem", "achieved": round(wf_rate / 1e9, 2),
+                             "peak": round(wf_peak / 1e9, 2), "unit": "Gwavefronts/s",
+                             "frac": round(wf_rate / wf_peak, 4),
+                             "rule": "2,080 shared-memory wavefronts per external product "
+                                     "(algorithmic count; ncu measures 67% of peak)"}
     share = {"br1024_ms_per_step": round(br_ms / args.steps, 3),
              "iks_ms_per_step": round(iks_ms / args.steps, 3),
              "gate_prep_ms_per_step": round(prep_ms / args.steps, 3)}
