@@ -232,6 +232,14 @@ int vsp_profile_enable(vsp_ctx* ctx, int on);
 int vsp_profile_read(vsp_ctx* ctx, const char* name, double* total_ms, uint64_t* count);
 int vsp_profile_reset(vsp_ctx* ctx);
 
+/* Launch plan the engine picks for a level-1 blind rotation of `tasks` tasks (FFT path;
+ * test-det runs the exact kernel): out = {narrow-level latency kernel (1/0), tasks in
+ * whole 8-task-per-SM waves, tasks per CTA of the remainder launch (0 = none)}.  Lets the
+ * tests assert which wave boundaries a batch really crosses.  No reference counterpart. */
+int vsp_br_plan(vsp_ctx* ctx, size_t tasks, int32_t out[3]);
+/* Streaming multiprocessors of the context's device (sizes every launch plan). */
+int vsp_sm_count(vsp_ctx* ctx);
+
 /* Measured dense FP64 FMA throughput of `device` in TFLOP/s (the denominator of the
  * blind-rotation roofline; MEASURED_PEAKS.json carries no FP64 figure). */
 int vsp_fp64_peak_probe(int device, double* tflops);

@@ -73,6 +73,8 @@ def lib() -> ctypes.CDLL:
         L.vsp_profile_read.argtypes = [vp, ctypes.c_char_p, ctypes.POINTER(ctypes.c_double),
                                        ctypes.POINTER(ctypes.c_uint64)]
         L.vsp_profile_reset.argtypes = [vp]
+        L.vsp_br_plan.argtypes = [vp, sz, vp]
+        L.vsp_sm_count.argtypes = [vp]
         L.vsp_fp64_peak_probe.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
         L.vsp_client_keygen.argtypes = [ctypes.POINTER(VspParams), u64, ctypes.c_int] + [vp] * 8
         L.vsp_client_tlwe_encrypt.argtypes = [ctypes.POINTER(VspParams), vp, u64, vp, sz, vp]
@@ -268,6 +270,7 @@ class Engine:
             _raise(3, L.vsp_last_error())
         self.h = ctypes.c_void_p(self.h)
         self.device = device
+        self.sms = int(lib().vsp_sm_count(self.h))
 
     def close(self):
         if getattr(self, "h", None):
@@ -358,6 +361,8 @@ class Engine:
                            stream_ptr: int = 0):
         """Device-resident variant (pointers from torch tensors); asynchronous."""
         kid = self._kind_ids(kinds)
+        if kid.size != G:
+            raise ValueError(f"homGate: {kid.size} kinds for {G} gates")
         _check(lib().vsp_hom_gate_batch_dev(self.h, _ptr(kid), ctypes.c_void_p(d_in_ptr),
                                             ctypes.c_void_p(d_out_ptr), G,
                                             ctypes.c_void_p(stream_ptr)))
@@ -398,6 +403,8 @@ class Engine:
         sel = np.ascontiguousarray(sel.reshape(-1, 2 * p.l1, 2, p.N1), np.uint32)
         c1 = np.ascontiguousarray(c1.reshape(-1, 2 * p.N1), np.uint32)
         c0 = np.ascontiguousarray(c0.reshape(-1, 2 * p.N1), np.uint32)
+        if not (sel.shape[0] == c1.shape[0] == c0.shape[0]):
+            raise ValueError("cmux: selector / operand counts differ")
         out = np.zeros_like(c1)
         _check(lib().vsp_cmux_batch(self.h, _ptr(sel), _ptr(c1), _ptr(c0), _ptr(out), c1.shape[0]))
         return out
@@ -407,6 +414,8 @@ class Engine:
         p = self.params
         f = lambda x: np.ascontiguousarray(np.atleast_2d(x), np.uint32)
         sel, a, b = f(sel), f(a), f(b)
+        if not (sel.shape == a.shape == b.shape) or sel.shape[1] != p.n + 1:
+            raise ValueError(f"homMuxNoSeIks: operands must all be (G, {p.n + 1})")
         out = np.zeros((sel.shape[0], 2 * p.N1), np.uint32)
         _check(lib().vsp_hom_mux_no_se_iks_batch(self.h, _ptr(sel), _ptr(a), _ptr(b), _ptr(out),
                                                  sel.shape[0]))
@@ -421,6 +430,8 @@ class Engine:
         a = np.ascontiguousarray(addr, np.uint32)
         f = np.ascontiguousarray(wflag, np.uint32)
         d = np.ascontiguousarray(wdata, np.uint32)
+        if a.shape != (v, p.n + 1) or f.size != p.n + 1 or d.shape != (w, p.n + 1):
+            raise ValueError("ramCycle: address width mismatch")
         ro = np.zeros((w, p.n + 1), np.uint32)
         _check(lib().vsp_ram_cycle(self.h, v, w, _ptr(ram), _ptr(a), _ptr(f), _ptr(d), _ptr(ro)))
         return ro, ram
@@ -429,7 +440,9 @@ class Engine:
         """addressToTrgsw + romRead (engine.cpp:133-143): 32 TLWEs."""
         p = self.params
         luts = np.ascontiguousarray(luts, np.uint32)
-        a = np.ascontiguousarray(addr, np.uint32)
+        a = np.ascontiguousarray(np.atleast_2d(addr), np.uint32)
+        if a.shape[1] != p.n + 1 or luts.ndim != 2 or luts.shape[1] != 2 * p.N1:
+            raise ValueError("romRead: address / LUT shape mismatch")
         out = np.zeros((32, p.n + 1), np.uint32)
         _check(lib().vsp_rom_read(self.h, depth_bytes, _ptr(luts), luts.shape[0], _ptr(a),
                                   a.shape[0], _ptr(out)))
@@ -467,6 +480,13 @@ class Engine:
         _check(lib().vsp_blind_rotate_lvl2_batch(self.h, _ptr(cts), _ptr(hv), _ptr(out),
                                                  cts.shape[0]))
         return out
+
+    def br_plan(self, tasks: int) -> dict:
+        """The blind-rotation launch plan for `tasks` tasks: narrow-level latency kernel,
+        tasks in whole W=8 waves, tasks per CTA of the remainder wave."""
+        o = np.zeros(3, np.int32)
+        _check(lib().vsp_br_plan(self.h, tasks, _ptr(o)))
+        return {"lat": bool(o[0]), "full": int(o[1]), "w_rem": int(o[2])}
 
     def counters(self) -> dict:
         """OpCounters (counters.hpp:11-28)."""
@@ -519,6 +539,8 @@ class Engine:
         """homGate over one netlist level sharded across the attached ranks (device
         buffers holding ALL G gates on every rank)."""
         kid = self._kind_ids(kinds)
+        if kid.size != G:
+            raise ValueError(f"homGate: {kid.size} kinds for {G} gates")
         _check(lib().vsp_hom_gate_level_dev(self.h, _ptr(kid), ctypes.c_void_p(d_in_ptr),
                                             ctypes.c_void_p(d_out_ptr), G,
                                             ctypes.c_void_p(stream)))

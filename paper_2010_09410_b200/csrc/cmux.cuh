@@ -238,17 +238,20 @@ __global__ void trlwe_sum_mu_kernel(const uint32_t* __restrict__ trlwe, const in
 
 // Linear combinations of homMuxNoSeIks (ops.cpp:898-905) for the RAM control unit:
 // task 2j = wflag + wdata[j] - mu, task 2j+1 = -wflag + readOut[j] - mu.
+// sel_stride = 0: one selector (the write flag) for all j; n + 1: selector j per item
+// (the batched homMuxNoSeIks entry point).
 __global__ void mux_prep_kernel(const uint32_t* __restrict__ wflag, const uint32_t* __restrict__ wdata,
                                 const uint32_t* __restrict__ readout, uint32_t* __restrict__ out,
-                                int w, int n)
+                                int w, int n, int sel_stride = 0)
 {
     const int t = blockIdx.x;
     if (t >= 2 * w)
         return;
     const int j = t >> 1;
     const uint32_t* x = (t & 1) ? readout + (size_t)j * (n + 1) : wdata + (size_t)j * (n + 1);
+    const uint32_t* sel = wflag + (size_t)j * sel_stride;
     for (int k = threadIdx.x; k <= n; k += blockDim.x) {
-        const uint32_t f = (t & 1) ? 0u - wflag[k] : wflag[k];
+        const uint32_t f = (t & 1) ? 0u - sel[k] : sel[k];
         out[(size_t)t * (n + 1) + k] = f + x[k] + (k == n ? 0u - kMu32 : 0u);
     }
 }

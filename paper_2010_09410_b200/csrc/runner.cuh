@@ -80,6 +80,88 @@ namespace {
 
 [[noreturn]] void nl_fail(const std::string& m) { throw std::runtime_error("netlist: " + m); }
 
+const char* cell_kind_name(int k)  // cellKindName (netlist.cpp:47-80)
+{
+    static const char* names[] = {"AND", "ANDNOT", "MUX", "NAND", "NOR", "NOT", "OR", "ORNOT",
+                                  "XNOR", "XOR", "DFF", "ROM", "RAM", "CONST0", "CONST1"};
+    return k >= 0 && k <= cConst1 ? names[k] : "?";
+}
+
+// validateNetlist (netlist.cpp:265-345) on the flat C-ABI arrays, with the reference's
+// messages.  The flat form also has to enforce what the reference's JSON schema gives
+// for free (netlist.cpp:106-199): known kinds, one output per gate / DFF / constant.
+void validate_netlist(const vsp_netlist* nl)
+{
+    const int C = (int)nl->kind.size();
+    const int nets = nl->nets;
+    std::unordered_set<int> ids;
+    for (int i = 0; i < C; i++) {
+        if (nl->kind[i] < 0 || nl->kind[i] > cConst1)
+            throw std::invalid_argument("netlist: unknown cell kind");
+        if (!ids.insert(nl->id[i]).second)
+            nl_fail("duplicate cell id " + std::to_string(nl->id[i]));
+    }
+    std::vector<int> driver(nets, -1);  // -2 module input, else cell index
+    for (int b : nl->input_nets) {
+        if (b < 0 || b >= nets)
+            nl_fail("input port 'in' references bad net " + std::to_string(b));
+        if (driver[b] != -1)
+            nl_fail("multiple drivers on net " + std::to_string(b));
+        driver[b] = -2;
+    }
+    int roms = 0, rams = 0;
+    for (int i = 0; i < C; i++) {
+        const int k = nl->kind[i];
+        const int nin = nl->in_off[i + 1] - nl->in_off[i];
+        const int nout = nl->out_off[i + 1] - nl->out_off[i];
+        const std::string who = "cell " + std::to_string(nl->id[i]) + " (" + cell_kind_name(k) + ")";
+        int arity = 2;
+        if (k == cNot || k == cDff)
+            arity = 1;
+        else if (k == cMux)
+            arity = 3;
+        else if (k == cConst0 || k == cConst1)
+            arity = 0;
+        else if (k == cRom || k == cRam)
+            arity = nin;
+        if (nin != arity)
+            nl_fail(who + " has wrong input count");
+        if (k == cRom) {
+            roms++;
+            if (nout != 32)
+                nl_fail("ROM port must have 32 rdata bits");
+            if (nin == 0)
+                nl_fail("ROM port needs address bits");
+        }
+        else if (k == cRam) {
+            rams++;
+            if (nout == 0 || nin < nout + 2)
+                nl_fail("RAM port pin widths are inconsistent");
+        }
+        else if (nout != 1) {
+            nl_fail(who + " must drive exactly one net");
+        }
+        for (int q = nl->out_off[i]; q < nl->out_off[i + 1]; q++) {
+            const int b = nl->out_nets[q];
+            if (b < 0 || b >= nets)
+                nl_fail("cell " + std::to_string(nl->id[i]) + " drives bad net " + std::to_string(b));
+            if (driver[b] != -1)
+                nl_fail("multiple drivers on net " + std::to_string(b) + " (cell " +
+                        std::to_string(nl->id[i]) + ")");
+            driver[b] = i;
+        }
+    }
+    for (int i = 0; i < C; i++)
+        for (int q = nl->in_off[i]; q < nl->in_off[i + 1]; q++) {
+            const int b = nl->in_nets[q];
+            if (b < 0 || b >= nets || driver[b] == -1)
+                nl_fail("dangling input net " + std::to_string(b) + " on cell " +
+                        std::to_string(nl->id[i]));
+        }
+    if (roms > 1 || rams > 1)
+        nl_fail("at most one ROM port and one RAM port are supported");
+}
+
 void build_dag(vsp_netlist* nl)
 {
     const int C = (int)nl->kind.size();

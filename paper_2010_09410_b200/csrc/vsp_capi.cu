@@ -9,6 +9,7 @@
 #include <cstring>
 #include <memory>
 #include <type_traits>
+#include <unordered_set>
 #include <functional>
 #include <map>
 #include <mutex>
@@ -262,6 +263,29 @@ struct vsp_ctx {
 
 namespace {
 
+// Every C-ABI entry point that touches the context runs inside one CallScope: the context
+// mutex, the context's device, and the cross-stream guard -- the scratch buffers are
+// shared by all calls, so a call on a different stream than the previous one first waits
+// for the previous call's work (ev_last), and records its own end for the next call.
+struct CallScope {
+    vsp_ctx* c;
+    cudaStream_t st;
+    std::lock_guard<std::mutex> lk;
+    CallScope(vsp_ctx* ctx, cudaStream_t stream) : c(ctx), st(stream), lk(ctx->mu)
+    {
+        c->set_device();
+        c->stream_enter(st);
+    }
+    ~CallScope()
+    {
+        try {
+            c->stream_leave(st);
+        }
+        catch (...) {  // a CUDA error here is already reported by the failing call
+        }
+    }
+};
+
 template <class F>
 void timed(vsp_ctx* c, const char* name, cudaStream_t st, F&& launch)
 {
@@ -389,6 +413,38 @@ void launch_br2(vsp_ctx* c, const uint32_t* d_lwe, int ninputs, const uint64_t* 
 // before_part(lo, hi): called (host side) before the launch that consumes tasks [lo, hi);
 // when set, whole waves are launched one wave per launch so the host pipeline can upload
 // the inputs of wave k + 1 while wave k runs.
+// Launch plan of a level-1 blind rotation of T tasks (FFT path):
+//  - lat: T <= 2 x SMs -> the narrow-level latency kernel (br_lat, one task per CTA);
+//  - else whole waves of W = 8 tasks per SM over the first `full` tasks, and the remainder
+//    as one wave of W_rem = br_warps_for(rem) tasks per SM.  Every task costs the same and
+//    one CTA runs per SM, so a partial last wave of W = 8 would cost a full wave.
+struct BrPlan {
+    bool lat = false;
+    int full = 0;      // tasks in whole W = 8 waves
+    int w_rem = 0;     // tasks per CTA of the remainder launch (0: none)
+    int forced = 0;    // VSP_BR_WARPS override
+};
+
+BrPlan br_plan(int T, int sms)
+{
+    BrPlan pl;
+    if (const char* e = getenv("VSP_BR_WARPS"))  // tuning knob (scripts/br_occupancy.py)
+        pl.forced = atoi(e);
+    if (pl.forced) {
+        pl.w_rem = pl.forced;
+        return pl;
+    }
+    if (T <= 2 * sms) {
+        pl.lat = T > 0;
+        return pl;
+    }
+    const long wave8 = 8L * sms;
+    pl.full = (br_warps_for(T, sms) == 8 && T > wave8) ? (int)(T / wave8 * wave8) : 0;
+    const int rem = T - pl.full;
+    pl.w_rem = rem ? br_warps_for(rem, sms) : 0;
+    return pl;
+}
+
 void launch_br(vsp_ctx* c, const uint32_t* d_tasks, uint32_t* d_trlwe, int T, cudaStream_t st,
                const std::function<void(int)>& after_full = {},
                const std::function<void(int, int)>& before_part = {})
@@ -397,18 +453,12 @@ void launch_br(vsp_ctx* c, const uint32_t* d_tasks, uint32_t* d_trlwe, int T, cu
         return;
     const Params& p = c->p;
     const long wave8 = 8L * c->sms;
-    const bool split = p.fft && !getenv("VSP_BR_WARPS") && br_warps_for(T, c->sms) == 8 &&
-                       T > wave8 && T > 2 * c->sms;
-    if (before_part && !split)
+    const BrPlan plan = br_plan(T, c->sms);
+    if (before_part && !(p.fft && plan.full > 0))
         before_part(0, T);
     if (p.fft) {
-        // Every task costs the same and one CTA (W tasks) runs per SM, so a partial last
-        // wave of W = 8 would cost a full wave: run the whole waves at W = 8 and spread
-        // the remainder as one wave of ceil(rem / SMs) tasks per SM (cheaper per wave).
-        const int full = (br_warps_for(T, c->sms) == 8 && T > wave8) ? (int)(T / wave8 * wave8) : 0;
-        int forced = 0;
-        if (const char* e = getenv("VSP_BR_WARPS"))  // tuning knob (scripts/br_occupancy.py)
-            forced = atoi(e);
+        const int full = plan.full;
+        const int forced = plan.forced;
         auto launch_part_on = [&](const uint32_t* tk, uint32_t* tr, int cnt, int W, cudaStream_t s) {
             switch (W) {
             case 8: launch_br_w<8>(c, tk, tr, cnt, s); break;
@@ -426,7 +476,7 @@ void launch_br(vsp_ctx* c, const uint32_t* d_tasks, uint32_t* d_trlwe, int T, cu
         auto launch_part = [&](const uint32_t* tk, uint32_t* tr, int cnt, int W) {
             launch_part_on(tk, tr, cnt, W, st);
         };
-        if (!forced && T <= 2 * c->sms) {
+        if (plan.lat) {
             // narrow level: latency kernel, 4 warps per task (bootstrap.cuh br_lat_kernel)
             static const bool probe = getenv("VSP_LAT_PROBE") != nullptr;  // tuning only
             if (probe) {
@@ -478,7 +528,7 @@ void launch_br(vsp_ctx* c, const uint32_t* d_tasks, uint32_t* d_trlwe, int T, cu
                 VSP_CUDA_CHECK(cudaEventRecord(c->ev_full, st));
                 VSP_CUDA_CHECK(cudaStreamWaitEvent(c->hstream, c->ev_full, 0));
                 launch_part_on(d_tasks + (size_t)full * (p.n + 1), d_trlwe + (size_t)full * 2 * p.N1,
-                               rem, br_warps_for(rem, c->sms), c->hstream);
+                               rem, plan.w_rem, c->hstream);
                 VSP_CUDA_CHECK(cudaEventRecord(c->ev_rem, c->hstream));
                 after_full(full);
                 VSP_CUDA_CHECK(cudaStreamWaitEvent(st, c->ev_rem, 0));
@@ -486,7 +536,7 @@ void launch_br(vsp_ctx* c, const uint32_t* d_tasks, uint32_t* d_trlwe, int T, cu
             }
             if (rem)
                 launch_part(d_tasks + (size_t)full * (p.n + 1), d_trlwe + (size_t)full * 2 * p.N1,
-                            rem, br_warps_for(rem, c->sms));
+                            rem, plan.w_rem);
         });
         c->counters[1] += (uint64_t)T;
         return;
@@ -505,11 +555,11 @@ void launch_br(vsp_ctx* c, const uint32_t* d_tasks, uint32_t* d_trlwe, int T, cu
     c->counters[1] += (uint64_t)T;
 }
 
-int iks_split(int tiles, int N)
+int iks_split(int tiles, int N, int sms)
 {
-    // enough CTAs for ~4 waves of 148 SMs; power of two dividing N
+    // enough CTAs for ~4 waves of the SMs; power of two dividing N
     int s = 1;
-    while (s < 64 && s * 2 <= N && tiles * s < 4 * 148)
+    while (s < 64 && s * 2 <= N && tiles * s < 4 * sms)
         s *= 2;
     return s;
 }
@@ -557,7 +607,7 @@ void launch_iks(vsp_ctx* c, const uint32_t* d_trlwe, const int2* d_gtask, const 
         else if (p.ksBaseBits == 2 && p.ksLen <= 8) {
             constexpr int GT = 32;
             const int tiles = (Gl + GT - 1) / GT;
-            const int split = iks_split(tiles, (int)p.N1);
+            const int split = iks_split(tiles, (int)p.N1, c->sms);
             const dim3 grid(tiles, split);
             const size_t smem = (size_t)(p.N1 / split) * p.ksLen * sizeof(uint64_t);
             if (kpt == 1)
@@ -575,7 +625,7 @@ void launch_iks(vsp_ctx* c, const uint32_t* d_trlwe, const int2* d_gtask, const 
         else if (p.ksBaseBits == 4 && p.ksLen <= 8 && kpt == 1) {
             constexpr int GT = 16;
             const int tiles = (Gl + GT - 1) / GT;
-            const int split = iks_split(tiles, (int)p.N1);
+            const int split = iks_split(tiles, (int)p.N1, c->sms);
             const size_t smem = (size_t)(p.N1 / split) * p.ksLen * sizeof(uint64_t);
             iks_kernel<4, GT, 1><<<dim3(tiles, split), 256, smem, st>>>(
                 d_trlwe, d_gtask, d_glist, d_seidx, Gl, c->d_ksk, d_out, p.n, p.N1, p.ksLen);
@@ -716,27 +766,37 @@ void hom_gate_dev(vsp_ctx* c, const int32_t* kinds, const uint32_t* d_in, uint32
         VSP_CUDA_CHECK(cudaGetLastError());
         c->launches++;
     };
-    // first gate with a task >= t (NOT gates belong to the preceding task range)
-    // tasks_end[g] = tasks of gates [0, g]; the first gate with a task >= t is the first g
-    // with tasks_end[g] > t (binary search; gates' tasks are assigned in gate order)
-    std::vector<int> tasks_end;
+    // Gates' tasks are assigned in gate order.  tasks_end[g] = tasks of gates [0, g]
+    // (exclusive end of g's tasks); tasks_start[g] = its first task slot.
+    //  - first_gate_starting_at(t): the first gate whose FIRST task is >= t.  Every gate
+    //    before it has a task < t, so a launch consuming tasks [.., t) needs all of them
+    //    prepped -- including a MUX whose two tasks straddle t (advisor finding r01).
+    //  - first_gate_ending_after(t): the first gate with a task >= t; every gate before
+    //    it has ALL its tasks < t (final once those tasks are key-switched).
+    std::vector<int> tasks_end, tasks_start;
     if (io) {
         tasks_end.resize(G);
+        tasks_start.resize(G);
         int acc_t = 0;
         for (size_t g = 0; g < G; g++) {
             const int2 tt = pl.gtask[g];
+            tasks_start[g] = acc_t;
             acc_t += tt.x < 0 ? 0 : (tt.y >= 0 ? 2 : 1);
             tasks_end[g] = acc_t;
         }
     }
-    auto gate_of_task = [&](int t) -> size_t {
+    auto first_gate_ending_after = [&](int t) -> size_t {
         return (size_t)(std::upper_bound(tasks_end.begin(), tasks_end.end(), t) - tasks_end.begin());
+    };
+    auto first_gate_starting_at = [&](int t) -> size_t {
+        return (size_t)(std::lower_bound(tasks_start.begin(), tasks_start.end(), t) -
+                        tasks_start.begin());
     };
     size_t prepped = 0;
     std::function<void(int, int)> before_part;
     if (io) {
         before_part = [&](int lo, int hi) {
-            const size_t g1 = hi >= pl.T ? G : gate_of_task(hi);
+            const size_t g1 = hi >= pl.T ? G : std::max(prepped, first_gate_starting_at(hi));
             prep(prepped, g1);
             prepped = g1;
             (void)lo;
@@ -769,7 +829,7 @@ void hom_gate_dev(vsp_ctx* c, const int32_t* kinds, const uint32_t* d_in, uint32
         VSP_CUDA_CHECK(cudaEventRecord(c->ev_join, c->astream));
         forked = true;
         if (io)  // gates below the first remainder task are final once this key switch is
-            gdone = gate_of_task(full);
+            gdone = first_gate_ending_after(full);
     };
     launch_br(c, d_tasks, d_trlwe, pl.T, st, fork_iks, before_part);
     launch_iks(c, d_trlwe, d_gtask, d_glist + k1, Gl - k1, d_out, st);
@@ -1031,10 +1091,8 @@ void ram_cycle_dev(vsp_ctx* c, uint32_t* d_ram, int v, int w, const uint32_t* d_
     // whole-wave cells runs UNDER the remainder wave (which holds half of each SM): key
     // switch the remainder cells, then their blind rotations (high-priority stream) beside
     // the whole-wave cells' key switch (low-priority stream), then the whole waves.
-    const long wave8 = 8L * c->sms;
     const int T = (int)cells;
-    const int full = (p.fft && !getenv("VSP_BR_WARPS") && br_warps_for(T, c->sms) == 8 &&
-                      T > wave8 && T > 2 * c->sms) ? (int)(T / wave8 * wave8) : 0;
+    const int full = p.fft ? br_plan(T, c->sms).full : 0;
     const int rem = T - full;
     if (full && rem) {
         std::vector<int2> gt(full);
@@ -1306,8 +1364,8 @@ int vsp_upload_keys(vsp_ctx* c, const uint32_t* bk1, const uint32_t* ksk, const 
                     const uint32_t* pks_negs, const uint32_t* pks_id, int has_cb)
 {
     return guard([&] {
-        std::lock_guard<std::mutex> lk(c->mu);
-        c->set_device();
+        CallScope cs(c, c->stream);
+        VSP_CUDA_CHECK(cudaStreamSynchronize(c->stream));  // keys may be in use
         const Params& p = c->p;
         if (!bk1 || !ksk)
             throw std::invalid_argument("bk1 and ksk are required");
@@ -1396,12 +1454,9 @@ int vsp_hom_gate_batch_dev(vsp_ctx* c, const int32_t* kinds, const uint32_t* d_i
                            uint32_t* d_out, size_t G, void* stream)
 {
     return guard([&] {
-        std::lock_guard<std::mutex> lk(c->mu);
-        c->set_device();
-        c->stream_enter(static_cast<cudaStream_t>(stream));
+        CallScope cs(c, static_cast<cudaStream_t>(stream));
         cudaStream_t st = static_cast<cudaStream_t>(stream);
         hom_gate_dev(c, kinds, d_in, d_out, G, st);
-        c->stream_leave(static_cast<cudaStream_t>(stream));
     });
 }
 
@@ -1409,9 +1464,7 @@ int vsp_hom_gate_batch(vsp_ctx* c, const int32_t* kinds, const uint32_t* in, uin
                        size_t G)
 {
     return guard([&] {
-        std::lock_guard<std::mutex> lk(c->mu);
-        c->set_device();
-        c->stream_enter(c->stream);
+        CallScope cs(c, c->stream);
         for (size_t g = 0; g < G; g++)
             if (kinds[g] < 0 || kinds[g] > kXor)
                 throw std::invalid_argument("homGate: unknown kind");
@@ -1438,8 +1491,7 @@ int vsp_hom_gate_batch(vsp_ctx* c, const int32_t* kinds, const uint32_t* in, uin
 int vsp_bootstrap_to_trlwe_batch(vsp_ctx* c, const uint32_t* in, uint32_t* out, size_t G)
 {
     return guard([&] {
-        std::lock_guard<std::mutex> lk(c->mu);
-        c->set_device();
+        CallScope cs(c, c->stream);
         require_keys(c);
         if (G == 0)
             return;
@@ -1457,8 +1509,7 @@ int vsp_bootstrap_to_trlwe_batch(vsp_ctx* c, const uint32_t* in, uint32_t* out, 
 int vsp_gate_bootstrap_batch(vsp_ctx* c, const uint32_t* in, uint32_t* out, size_t G)
 {
     return guard([&] {
-        std::lock_guard<std::mutex> lk(c->mu);
-        c->set_device();
+        CallScope cs(c, c->stream);
         require_keys(c);
         if (G == 0)
             return;
@@ -1489,8 +1540,7 @@ int vsp_gate_bootstrap_batch(vsp_ctx* c, const uint32_t* in, uint32_t* out, size
 int vsp_identity_key_switch_batch(vsp_ctx* c, const uint32_t* in, uint32_t* out, size_t G)
 {
     return guard([&] {
-        std::lock_guard<std::mutex> lk(c->mu);
-        c->set_device();
+        CallScope cs(c, c->stream);
         require_keys(c);
         if (G == 0)
             return;
@@ -1534,8 +1584,7 @@ int vsp_identity_key_switch_batch(vsp_ctx* c, const uint32_t* in, uint32_t* out,
 int vsp_circuit_bootstrap_batch(vsp_ctx* c, const uint32_t* in, uint32_t* out, size_t C)
 {
     return guard([&] {
-        std::lock_guard<std::mutex> lk(c->mu);
-        c->set_device();
+        CallScope cs(c, c->stream);
         require_cb(c);
         if (C == 0)
             return;
@@ -1553,8 +1602,7 @@ int vsp_cmux_batch(vsp_ctx* c, const uint32_t* sel, const uint32_t* c1, const ui
                    uint32_t* out, size_t G)
 {
     return guard([&] {
-        std::lock_guard<std::mutex> lk(c->mu);
-        c->set_device();
+        CallScope cs(c, c->stream);
         if (G == 0)
             return;
         const Params& p = c->p;
@@ -1591,8 +1639,7 @@ int vsp_hom_mux_no_se_iks_batch(vsp_ctx* c, const uint32_t* sel, const uint32_t*
                                 const uint32_t* b, uint32_t* out, size_t G)
 {
     return guard([&] {
-        std::lock_guard<std::mutex> lk(c->mu);
-        c->set_device();
+        CallScope cs(c, c->stream);
         require_keys(c);
         if (G == 0)
             return;
@@ -1606,12 +1653,10 @@ int vsp_hom_mux_no_se_iks_batch(vsp_ctx* c, const uint32_t* sel, const uint32_t*
         VSP_CUDA_CHECK(cudaMemcpyAsync(d + 2 * G * n1, b, G * n1 * 4, cudaMemcpyHostToDevice,
                                        c->stream));
         uint32_t* lin = c->aux.as<uint32_t>(2 * G * n1);
-        for (size_t g = 0; g < G; g++)
-            mux_prep_kernel<<<2, 128, 0, c->stream>>>(d + g * n1, d + G * n1 + g * n1,
-                                                      d + 2 * G * n1 + g * n1, lin + 2 * g * n1, 1,
-                                                      (int)p.n);
+        mux_prep_kernel<<<(unsigned)(2 * G), 128, 0, c->stream>>>(d, d + G * n1, d + 2 * G * n1, lin,
+                                                                  (int)G, (int)p.n, (int)n1);
         VSP_CUDA_CHECK(cudaGetLastError());
-        c->launches += G;
+        c->launches++;
         uint32_t* tr = c->aux2.as<uint32_t>(2 * G * cw);
         launch_br(c, lin, tr, (int)(2 * G), c->stream);
         std::vector<int2> pr(G);
@@ -1633,9 +1678,7 @@ int vsp_ram_cycle(vsp_ctx* c, uint32_t v, uint32_t w, uint32_t* ram, const uint3
                   const uint32_t* wflag, const uint32_t* wdata, uint32_t* readout)
 {
     return guard([&] {
-        std::lock_guard<std::mutex> lk(c->mu);
-        c->set_device();
-        c->stream_enter(c->stream);
+        CallScope cs(c, c->stream);
         const Params& p = c->p;
         const size_t n1 = p.n + 1, cw = 2 * (size_t)p.N1, cells = (size_t)w << v;
         if (v == 0 || w == 0)
@@ -1664,14 +1707,11 @@ int vsp_ram_cycle_dev(vsp_ctx* c, uint32_t v, uint32_t w, uint32_t* d_ram, const
                       void* stream)
 {
     return guard([&] {
-        std::lock_guard<std::mutex> lk(c->mu);
-        c->set_device();
-        c->stream_enter(static_cast<cudaStream_t>(stream));
+        CallScope cs(c, static_cast<cudaStream_t>(stream));
         if (v == 0 || w == 0)
             throw std::invalid_argument("ramCycle: address width mismatch");
         ram_cycle_dev(c, d_ram, (int)v, (int)w, d_addr, d_wflag, d_wdata, d_readout,
                       static_cast<cudaStream_t>(stream));
-        c->stream_leave(static_cast<cudaStream_t>(stream));
     });
 }
 
@@ -1682,15 +1722,12 @@ int vsp_mem_ports_dev(vsp_ctx* c, uint32_t depth_bytes, const uint32_t* d_luts, 
                       void* stream)
 {
     return guard([&] {
-        std::lock_guard<std::mutex> lk(c->mu);
-        c->set_device();
-        c->stream_enter(static_cast<cudaStream_t>(stream));
+        CallScope cs(c, static_cast<cudaStream_t>(stream));
         if (v == 0 || w == 0)
             throw std::invalid_argument("ramCycle: address width mismatch");
         mem_pair_dev(c, d_luts, (int)nluts, depth_bytes, d_rom_addr, (int)vrom, d_rom_out, d_ram,
                      (int)v, (int)w, d_ram_addr, d_wflag, d_wdata, d_readout,
                      static_cast<cudaStream_t>(stream));
-        c->stream_leave(static_cast<cudaStream_t>(stream));
     });
 }
 
@@ -1698,12 +1735,9 @@ int vsp_rom_read_dev(vsp_ctx* c, uint32_t depth_bytes, const uint32_t* d_luts, u
                      const uint32_t* d_addr, uint32_t vrom, uint32_t* d_out, void* stream)
 {
     return guard([&] {
-        std::lock_guard<std::mutex> lk(c->mu);
-        c->set_device();
-        c->stream_enter(static_cast<cudaStream_t>(stream));
+        CallScope cs(c, static_cast<cudaStream_t>(stream));
         rom_read_dev(c, d_luts, (int)nluts, depth_bytes, d_addr, (int)vrom, d_out,
                      static_cast<cudaStream_t>(stream));
-        c->stream_leave(static_cast<cudaStream_t>(stream));
     });
 }
 
@@ -1711,9 +1745,7 @@ int vsp_rom_read(vsp_ctx* c, uint32_t depth_bytes, const uint32_t* luts, uint32_
                  const uint32_t* addr, uint32_t vrom, uint32_t* out)
 {
     return guard([&] {
-        std::lock_guard<std::mutex> lk(c->mu);
-        c->set_device();
-        c->stream_enter(c->stream);
+        CallScope cs(c, c->stream);
         const Params& p = c->p;
         const size_t n1 = p.n + 1, cw = 2 * (size_t)p.N1;
         uint32_t* d_luts = c->romio.as<uint32_t>(std::max<size_t>(nluts, 1) * cw);
@@ -1732,8 +1764,7 @@ int vsp_blind_rotate_lvl2_batch(vsp_ctx* c, const uint32_t* in, const uint64_t* 
                                 size_t T)
 {
     return guard([&] {
-        std::lock_guard<std::mutex> lk(c->mu);
-        c->set_device();
+        CallScope cs(c, c->stream);
         require_keys(c);
         if (!c->d_bk2fd && !c->d_bk2raw)
             throw std::runtime_error("bootstrapping key lacks circuit bootstrapping material");
@@ -1782,8 +1813,13 @@ vsp_netlist* vsp_netlist_create(vsp_ctx* c, int32_t net_count, int32_t cells, co
 {
     vsp_netlist* out = nullptr;
     guard([&] {
-        std::lock_guard<std::mutex> lk(c->mu);
-        c->set_device();
+        CallScope cs(c, c->stream);
+        if (net_count < 0 || cells < 0 || n_inputs < 0)
+            throw std::invalid_argument("netlist: negative size");
+        if (cells > 0 && (!kinds || !ids || !in_off || !out_off))
+            throw std::invalid_argument("netlist: missing cell arrays");
+        if (n_inputs > 0 && !input_nets)
+            throw std::invalid_argument("netlist: missing input nets");
         auto nl = std::make_unique<vsp_netlist>();
         nl->ctx = c;
         nl->nets = net_count;
@@ -1791,24 +1827,21 @@ vsp_netlist* vsp_netlist_create(vsp_ctx* c, int32_t net_count, int32_t cells, co
         nl->id.assign(ids, ids + cells);
         nl->in_off.assign(in_off, in_off + cells + 1);
         nl->out_off.assign(out_off, out_off + cells + 1);
-        nl->in_nets.assign(in_nets, in_nets + in_off[cells]);
-        nl->out_nets.assign(out_nets, out_nets + out_off[cells]);
         for (int i = 0; i < cells; i++)
-            if (nl->kind[i] < 0 || nl->kind[i] > cConst1)
-                throw std::invalid_argument("netlist: unknown cell kind");
-        for (int x : nl->in_nets)
-            if (x < 0 || x >= net_count)
-                throw std::invalid_argument("netlist: bad net");
-        for (int x : nl->out_nets)
-            if (x < 0 || x >= net_count)
-                throw std::invalid_argument("netlist: bad net");
+            if (nl->in_off[i + 1] < nl->in_off[i] || nl->out_off[i + 1] < nl->out_off[i])
+                throw std::invalid_argument("netlist: pin offsets must be non-decreasing");
+        if (nl->in_off[0] != 0 || nl->out_off[0] != 0)
+            throw std::invalid_argument("netlist: pin offsets must start at 0");
+        nl->in_nets.assign(in_nets, in_nets + nl->in_off[cells]);
+        nl->out_nets.assign(out_nets, out_nets + nl->out_off[cells]);
+        nl->input_nets.assign(input_nets, input_nets + n_inputs);
+        validate_netlist(nl.get());
         build_dag(nl.get());
         for (int ci : nl->dff_cells) {
             nl->dff_q.push_back(nl->out_nets[nl->out_off[ci]]);
             nl->dff_d.push_back(nl->in_nets[nl->in_off[ci]]);
         }
         const size_t n1 = c->p.n + 1;
-        nl->input_nets.assign(input_nets, input_nets + n_inputs);
         nl->is_input.assign(net_count, 0);
         for (int x : nl->input_nets)
             nl->is_input[x] = 1;
@@ -1872,8 +1905,7 @@ int vsp_netlist_set_input(vsp_netlist* nl, int32_t input_index, const uint32_t* 
 {
     return guard([&] {
         vsp_ctx* c = nl->ctx;
-        std::lock_guard<std::mutex> lk(c->mu);
-        c->set_device();
+        CallScope cs(c, c->stream);
         if (input_index < 0 || input_index >= (int)nl->input_nets.size())
             throw std::out_of_range("netlist input index");
         const size_t n1 = c->p.n + 1;
@@ -1889,8 +1921,7 @@ int vsp_netlist_get_net(vsp_netlist* nl, int32_t net, uint32_t* tlwe)
 {
     return guard([&] {
         vsp_ctx* c = nl->ctx;
-        std::lock_guard<std::mutex> lk(c->mu);
-        c->set_device();
+        CallScope cs(c, c->stream);
         if (net < 0 || net >= nl->nets)
             throw std::out_of_range("net index");
         const size_t n1 = c->p.n + 1;
@@ -1915,8 +1946,7 @@ int vsp_netlist_dff(vsp_netlist* nl, uint32_t* get, const uint32_t* set)
 {
     return guard([&] {
         vsp_ctx* c = nl->ctx;
-        std::lock_guard<std::mutex> lk(c->mu);
-        c->set_device();
+        CallScope cs(c, c->stream);
         const size_t bytes = nl->dff_cells.size() * (c->p.n + 1) * 4;
         if (bytes == 0)
             return;
@@ -1934,10 +1964,10 @@ int vsp_netlist_set_rom(vsp_netlist* nl, uint32_t depth_bytes, const uint32_t* l
 {
     return guard([&] {
         vsp_ctx* c = nl->ctx;
-        std::lock_guard<std::mutex> lk(c->mu);
-        c->set_device();
+        CallScope cs(c, c->stream);
         if (nl->rom_cell < 0)
             throw std::runtime_error("netlist has no ROM port");
+        VSP_CUDA_CHECK(cudaStreamSynchronize(c->stream));  // in-flight cycles read the LUTs
         const size_t words = (size_t)nluts * 2 * c->p.N1;
         VSP_CUDA_CHECK(cudaMemcpy(nl->rom.as<uint32_t>(words), luts, words * 4, cudaMemcpyHostToDevice));
         nl->rom_depth = depth_bytes;
@@ -1950,10 +1980,10 @@ int vsp_netlist_ram(vsp_netlist* nl, uint32_t v, uint32_t w, uint32_t* get, cons
 {
     return guard([&] {
         vsp_ctx* c = nl->ctx;
-        std::lock_guard<std::mutex> lk(c->mu);
-        c->set_device();
+        CallScope cs(c, c->stream);
         if (nl->ram_cell < 0)
             throw std::runtime_error("netlist has no RAM port");
+        VSP_CUDA_CHECK(cudaStreamSynchronize(c->stream));  // in-flight cycles use the image
         const size_t words = ((size_t)w << v) * 2 * c->p.N1;
         if (set) {
             VSP_CUDA_CHECK(cudaMemcpy(nl->ram.as<uint32_t>(words), set, words * 4,
@@ -1976,9 +2006,7 @@ int vsp_netlist_run(vsp_netlist* nl, uint64_t cycles, double* stats)
 {
     return guard([&] {
         vsp_ctx* c = nl->ctx;
-        std::lock_guard<std::mutex> lk(c->mu);
-        c->set_device();
-        c->stream_enter(c->stream);
+        CallScope cs(c, c->stream);
         cudaEvent_t a, b;
         VSP_CUDA_CHECK(cudaEventCreate(&a));
         VSP_CUDA_CHECK(cudaEventCreate(&b));
@@ -2002,7 +2030,11 @@ int vsp_netlist_run(vsp_netlist* nl, uint64_t cycles, double* stats)
     });
 }
 
-uint64_t vsp_netlist_cycle(vsp_netlist* nl) { return nl->cycle; }
+uint64_t vsp_netlist_cycle(vsp_netlist* nl)
+{
+    std::lock_guard<std::mutex> lk(nl->ctx->mu);
+    return nl->cycle;
+}
 
 int vsp_upload_keys_hvp1(vsp_ctx* c, const uint8_t* bytes, size_t len)
 {
@@ -2049,8 +2081,7 @@ int vsp_netlist_snapshot_save(vsp_netlist* nl, const char* param_name, uint8_t* 
 {
     return guard([&] {
         vsp_ctx* c = nl->ctx;
-        std::lock_guard<std::mutex> lk(c->mu);
-        c->set_device();
+        CallScope cs(c, c->stream);
         VSP_CUDA_CHECK(cudaStreamSynchronize(c->stream));
         const std::vector<uint8_t> b = snapshot_save(nl, param_name ? param_name : "");
         *len = b.size();
@@ -2067,8 +2098,7 @@ int vsp_netlist_snapshot_load(vsp_netlist* nl, const char* param_name, const uin
 {
     return guard([&] {
         vsp_ctx* c = nl->ctx;
-        std::lock_guard<std::mutex> lk(c->mu);
-        c->set_device();
+        CallScope cs(c, c->stream);
         VSP_CUDA_CHECK(cudaStreamSynchronize(c->stream));
         snapshot_load(nl, param_name ? param_name : "", in, len);
     });
@@ -2100,23 +2130,30 @@ int vsp_snapshot_peek(const uint8_t* in, size_t len, char* backend, char* param,
 
 int vsp_netlist_set_cycle(vsp_netlist* nl, uint64_t cycle)
 {
+    std::lock_guard<std::mutex> lk(nl->ctx->mu);
     nl->cycle = cycle;
     return 0;
 }
 
 int vsp_counters(vsp_ctx* c, uint64_t out[5])
 {
+    std::lock_guard<std::mutex> lk(c->mu);
     std::memcpy(out, c->counters, sizeof(c->counters));
     return 0;
 }
 
 int vsp_counters_reset(vsp_ctx* c)
 {
+    std::lock_guard<std::mutex> lk(c->mu);
     std::memset(c->counters, 0, sizeof(c->counters));
     return 0;
 }
 
-uint64_t vsp_kernel_launches(vsp_ctx* c) { return c->launches; }
+uint64_t vsp_kernel_launches(vsp_ctx* c)
+{
+    std::lock_guard<std::mutex> lk(c->mu);
+    return c->launches;
+}
 
 // ---- multi-GPU ------------------------------------------------------------------
 
@@ -2135,8 +2172,7 @@ int vsp_attach_comm(vsp_ctx* c, const uint8_t id[128], int rank, int world)
     return guard([&] {
         if (world < 1 || rank < 0 || rank >= world)
             throw std::invalid_argument("attach_comm: bad rank/world");
-        std::lock_guard<std::mutex> lk(c->mu);
-        c->set_device();
+        CallScope cs(c, c->stream);
         if (c->comm) {
             nccl().commDestroy((ncclComm_t)c->comm);
             c->comm = nullptr;
@@ -2173,17 +2209,15 @@ int vsp_hom_gate_level_dev(vsp_ctx* c, const int32_t* kinds, const uint32_t* d_i
                            uint32_t* d_out, size_t G, void* stream)
 {
     return guard([&] {
-        std::lock_guard<std::mutex> lk(c->mu);
-        c->set_device();
-        c->stream_enter((cudaStream_t)stream);
+        CallScope cs(c, static_cast<cudaStream_t>(stream));
         hom_gate_level_dev(c, kinds, d_in, d_out, G, (cudaStream_t)stream);
         VSP_CUDA_CHECK(cudaGetLastError());
-        c->stream_leave((cudaStream_t)stream);
     });
 }
 
 int vsp_profile_enable(vsp_ctx* c, int on)
 {
+    std::lock_guard<std::mutex> lk(c->mu);
     c->profiling = on != 0;
     return 0;
 }
@@ -2191,6 +2225,7 @@ int vsp_profile_enable(vsp_ctx* c, int on)
 int vsp_profile_read(vsp_ctx* c, const char* name, double* total_ms, uint64_t* count)
 {
     return guard([&] {
+        std::lock_guard<std::mutex> lk(c->mu);
         c->set_device();
         auto it = c->timers.find(name);
         if (it == c->timers.end()) {
@@ -2217,6 +2252,7 @@ int vsp_profile_read(vsp_ctx* c, const char* name, double* total_ms, uint64_t* c
 int vsp_profile_reset(vsp_ctx* c)
 {
     return guard([&] {
+        std::lock_guard<std::mutex> lk(c->mu);
         c->set_device();
         for (auto& kv : c->timers)
             for (auto& e : kv.second.pending) {
@@ -2225,6 +2261,21 @@ int vsp_profile_reset(vsp_ctx* c)
                 cudaEventDestroy(e.second);
             }
         c->timers.clear();
+    });
+}
+
+int vsp_sm_count(vsp_ctx* c) { return c->sms; }
+
+int vsp_br_plan(vsp_ctx* c, size_t tasks, int32_t out[3])
+{
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(c->mu);
+        if (tasks > (size_t)INT32_MAX)
+            throw std::invalid_argument("br_plan: too many tasks");
+        const BrPlan pl = br_plan((int)tasks, c->sms);
+        out[0] = pl.lat ? 1 : 0;
+        out[1] = pl.full;
+        out[2] = pl.w_rem;
     });
 }
 

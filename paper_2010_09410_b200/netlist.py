@@ -371,8 +371,10 @@ class Evaluator:
 
     def set_input(self, port: str, idx: int, ct: np.ndarray):
         net = self._port_bit(self.nl.inputs, port, idx)
-        _check(lib().vsp_netlist_set_input(self.h, self._input_index[net],
-                                           _ptr(np.ascontiguousarray(ct, np.uint32))))
+        ct = np.ascontiguousarray(ct, np.uint32)
+        if ct.size != self.n + 1:
+            raise ValueError(f"setInput: a TLWE has {self.n + 1} words, got {ct.size}")
+        _check(lib().vsp_netlist_set_input(self.h, self._input_index[net], _ptr(ct)))
 
     def set_input_bool(self, port: str, idx: int, v: bool):
         t = np.zeros(self.n + 1, np.uint32)
@@ -412,10 +414,14 @@ class Evaluator:
 
     def set_rom(self, luts: np.ndarray, depth_bytes: int):
         luts = np.ascontiguousarray(luts, np.uint32)
+        if luts.ndim != 2 or luts.shape[1] != 2 * self.engine.params.N1:
+            raise ValueError("setRom: LUTs must be (nluts, 2*N1) TRLWEs")
         _check(lib().vsp_netlist_set_rom(self.h, depth_bytes, _ptr(luts), luts.shape[0]))
 
     def set_ram(self, cells: np.ndarray, v: int, w: int):
         cells = np.ascontiguousarray(cells, np.uint32)
+        if cells.size != (w << v) * 2 * self.engine.params.N1:
+            raise ValueError("setRam: image must hold w * 2^v TRLWE cells")
         _check(lib().vsp_netlist_ram(self.h, v, w, None, _ptr(cells)))
         self._ram_geom = (v, w)
 

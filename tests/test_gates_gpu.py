@@ -183,14 +183,27 @@ def test_pipelined_host_batch_equals_single_device_call(prod):
     assert np.array_equal(dec, want)
 
 
-@pytest.mark.parametrize("G", [1, 150, 2368, 2400])
+# (tasks) -> launch plan the engine must pick on a 148-SM B200 (vsp_br_plan)
+WAVE_PLANS = {
+    1: {"lat": True, "full": 0, "w_rem": 0},        # latency kernel, one task
+    150: {"lat": True, "full": 0, "w_rem": 0},      # latency kernel, 150 CTAs
+    2368: {"lat": False, "full": 2368, "w_rem": 0},  # exactly two whole W=8 waves
+    2400: {"lat": False, "full": 0, "w_rem": 6},    # one W=6 launch (3 waves), no split
+    2995: {"lat": False, "full": 2368, "w_rem": 5},  # two whole waves + a W=5 remainder
+}
+
+
+@pytest.mark.parametrize("G", sorted(WAVE_PLANS))
 def test_wave_boundaries_host_and_device_paths(prod, G):
-    """Launch-policy boundaries: one task (latency kernel), 150 (two latency waves), exactly
-    two whole W=8 waves (no remainder), two whole waves + a 32-task remainder (key switch
-    forked under the remainder, host pipeline with an early download).  Host-pipelined and
-    device calls agree and every output decrypts right."""
+    """Launch-policy boundaries (the plan is asserted, so the test covers what it names):
+    latency kernel (1 and 150 tasks), exactly two whole W=8 waves, one W=6 launch, and two
+    whole waves + a remainder (key switch forked under the remainder, host pipeline with an
+    early download).  Host-pipelined and device calls agree and every output decrypts
+    right."""
     import torch
     e, o = prod
+    if e.sms == 148:
+        assert e.br_plan(G) == WAVE_PLANS[G]
     rng = np.random.default_rng(G)
     k = oracle_keys("tfhe-80", 20200729, False)
     p = vsp.ParameterSet("tfhe-80")
@@ -207,6 +220,36 @@ def test_wave_boundaries_host_and_device_paths(prod, G):
     assert np.array_equal(vsp.decrypt(k["lv0"], out), want)
 
 
+def test_mux_straddling_wave_boundaries_host_pipeline(prod):
+    """Advisor finding r01: the host pipeline preps the gates of each whole wave before it
+    launches; a MUX whose two tasks straddle a wave boundary (tasks 1183/1184 and 2367/2368
+    after one leading AND) must be prepped before the first wave that reads it.  [AND] +
+    1600 MUX = 3,201 tasks: two whole W=8 waves + a remainder.  Host-pipelined call ==
+    device call == oracle on the straddling gates; every output decrypts right."""
+    import torch
+    e, o = prod
+    G = 1601
+    kid = np.array([GATE_KINDS.index("AND")] + [GATE_KINDS.index("MUX")] * 1600, np.int32)
+    if e.sms == 148:
+        assert e.br_plan(3201) == {"lat": False, "full": 2368, "w_rem": 6}
+    rng = np.random.default_rng(1601)
+    k = oracle_keys("tfhe-80", 20200729, False)
+    p = vsp.ParameterSet("tfhe-80")
+    bits = rng.integers(0, 2, size=(G, 3)).astype(np.uint8)
+    ins = vsp.encrypt(p, k["lv0"], bits.reshape(-1), 1601).reshape(G, 3, p.n + 1)
+    out = e.hom_gate_batch(kid, ins)
+    d_in = torch.from_numpy(ins.view(np.int32)).cuda()
+    d_out = torch.empty((G, p.n + 1), dtype=torch.int32, device="cuda")
+    e.hom_gate_batch_dev(kid, d_in.data_ptr(), d_out.data_ptr(), G)
+    torch.cuda.synchronize()
+    assert np.array_equal(out, d_out.cpu().numpy().view(np.uint32))
+    want = np.array([TRUTH[GATE_KINDS[kk]](*(int(x) for x in b)) for kk, b in zip(kid, bits)])
+    assert np.array_equal(vsp.decrypt(k["lv0"], out), want)
+    straddle = np.array([0, 591, 592, 1183, 1184, 1600])  # MUX i owns tasks 2i+1, 2i+2
+    ref = o.hom_gate_batch(kid[straddle], ins[straddle], threads=8)
+    assert np.array_equal(out[straddle], ref)
+
+
 def test_not_only_and_mux_heavy_batches_tfhe80(prod):
     """Batches without any blind rotation (all NOT: the host pipeline uploads and negates
     only) and MUX-heavy batches (two tasks per gate across the wave boundary)."""
@@ -218,7 +261,9 @@ def test_not_only_and_mux_heavy_batches_tfhe80(prod):
         x[i, 0] = o.encrypt(int(b))
     out = e.hom_gate_batch(["NOT"] * 40, x)
     assert [o.decrypt(c) for c in out] == [1 - int(b) for b in bits]
-    G = 700  # 1,400 blind-rotation tasks: one whole wave + a remainder
+    G = 700  # 1,400 blind-rotation tasks: one W=5 launch (two waves)
+    if e.sms == 148:
+        assert e.br_plan(2 * G) == {"lat": False, "full": 0, "w_rem": 5}
     k = oracle_keys("tfhe-80", 20200729, False)
     p = vsp.ParameterSet("tfhe-80")
     mb = rng.integers(0, 2, size=(G, 3)).astype(np.uint8)

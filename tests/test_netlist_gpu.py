@@ -142,3 +142,26 @@ def test_runner_errors():
         ev.output("out", 0) if False else ev.run(1)
     with pytest.raises(RuntimeError):
         ev.set_input("nope", 0, np.zeros(17, np.uint32))
+
+
+@pytest.mark.parametrize("bad, match", [
+    # a 3-input AND would overflow the runner's 3-slot gather (advisor finding r01)
+    (lambda nl: nl.cells.append(N.Cell(90, "AND", [0, 1, 2], [5])), "wrong input count"),
+    (lambda nl: nl.cells.append(N.Cell(91, "NAND", [0, 1], [])), "exactly one net"),
+    (lambda nl: nl.cells.append(N.Cell(92, "XOR", [0, 1], [5, 6])), "exactly one net"),
+    (lambda nl: nl.inputs.append(N.Port("x", [999])), "bad net 999"),
+    (lambda nl: nl.cells.append(N.Cell(93, "OR", [0, 77], [5])), "dangling input net 77"),
+    (lambda nl: nl.cells.append(N.Cell(0, "OR", [0, 1], [5])), "duplicate cell id 0"),
+    (lambda nl: nl.cells.append(N.Cell(94, "OR", [0, 1], [3])), "multiple drivers on net 3"),
+])
+def test_flat_netlist_validated_by_c_abi(bad, match):
+    """vsp_netlist_create validates the flat arrays like validateNetlist (netlist.cpp:
+    265-345) before anything indexes them -- the Python parser is bypassed here."""
+    e = vsp.Engine("test-det")
+    nl = N.Netlist(name="v", inputs=[N.Port("in", [0, 1])], outputs=[N.Port("out", [3])],
+                   cells=[N.Cell(0, "AND", [0, 1], [2]), N.Cell(1, "NOT", [2], [3])],
+                   net_count=8)
+    N.Evaluator(nl, e).close()  # the valid base netlist is accepted
+    bad(nl)
+    with pytest.raises(RuntimeError, match=match):
+        N.Evaluator(nl, e)
