@@ -124,6 +124,23 @@ int vsp_ram_cycle(vsp_ctx* ctx, uint32_t v, uint32_t w, uint32_t* ram, const uin
 int vsp_rom_read(vsp_ctx* ctx, uint32_t depth_bytes, const uint32_t* luts, uint32_t nluts,
                  const uint32_t* addr, uint32_t vrom, uint32_t* out);
 
+/* The units of a RAM cycle and the ROM read on given address selectors (RamAddress: one
+ * raw TRGSW per address bit, LSB first, e.g. circuit-bootstrapped or client-encrypted);
+ * each prepares the selectors like prepareAddress (mem.cpp:21-36).
+ *   vsp_ram_read_unit    mem::ramReadUnit   (mem.cpp:49-72):  out = w TRLWEs
+ *   vsp_ram_control_unit mem::ramControlUnit (mem.cpp:74-90): read = w TRLWEs ->
+ *                        readout (w TLWEs), controlled (w TRLWEs)
+ *   vsp_ram_write_unit   mem::ramWriteUnit  (mem.cpp:92-120): ram updated in place
+ *   vsp_rom_read_sel     mem::romRead       (mem.cpp:137-177): 32 TLWEs */
+int vsp_ram_read_unit(vsp_ctx* ctx, uint32_t v, uint32_t w, const uint32_t* ram,
+                      const uint32_t* sel, uint32_t* out);
+int vsp_ram_control_unit(vsp_ctx* ctx, uint32_t w, const uint32_t* read, const uint32_t* wflag,
+                         const uint32_t* wdata, uint32_t* readout, uint32_t* controlled);
+int vsp_ram_write_unit(vsp_ctx* ctx, uint32_t v, uint32_t w, uint32_t* ram, const uint32_t* sel,
+                       const uint32_t* controlled);
+int vsp_rom_read_sel(vsp_ctx* ctx, uint32_t depth_bytes, const uint32_t* luts, uint32_t nluts,
+                     const uint32_t* sel, uint32_t vrom, uint32_t* out);
+
 /* Device-resident ramCycle / romRead (same arguments as device pointers, asynchronous on
  * `stream`, a cudaStream_t): the RAM image stays in HBM across cycles, as in the netlist
  * runner.  Replace the same reference calls (mem.cpp:122-135, :137-177). */

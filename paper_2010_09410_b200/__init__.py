@@ -64,6 +64,10 @@ def lib() -> ctypes.CDLL:
         L.vsp_ram_cycle.argtypes = [vp, u32, u32, vp, vp, vp, vp, vp]
         L.vsp_rom_read.argtypes = [vp, u32, vp, u32, vp, u32, vp]
         L.vsp_blind_rotate_lvl2_batch.argtypes = [vp, vp, vp, vp, sz]
+        L.vsp_ram_read_unit.argtypes = [vp, u32, u32, vp, vp, vp]
+        L.vsp_ram_control_unit.argtypes = [vp, u32, vp, vp, vp, vp, vp]
+        L.vsp_ram_write_unit.argtypes = [vp, u32, u32, vp, vp, vp]
+        L.vsp_rom_read_sel.argtypes = [vp, u32, vp, u32, vp, u32, vp]
         L.vsp_counters.argtypes = [vp, vp]
         L.vsp_counters_reset.argtypes = [vp]
         L.vsp_kernel_launches.argtypes = [vp]
@@ -446,6 +450,60 @@ class Engine:
         out = np.zeros((32, p.n + 1), np.uint32)
         _check(lib().vsp_rom_read(self.h, depth_bytes, _ptr(luts), luts.shape[0], _ptr(a),
                                   a.shape[0], _ptr(out)))
+        return out
+
+    # ---- the units of ramCycle / romRead on given selectors (mem.hpp:75-124) ----------
+    def _sel(self, sel) -> np.ndarray:
+        p = self.params
+        return np.ascontiguousarray(np.asarray(sel, np.uint32).reshape(-1, 2 * p.l1, 2, p.N1))
+
+    def ram_read_unit(self, ram: np.ndarray, v: int, w: int, sel) -> np.ndarray:
+        """mem::ramReadUnit (mem.cpp:49-72): sel = v raw TRGSWs (RamAddress, LSB first);
+        returns w TRLWEs (bit j of the addressed word at coefficient 0 of output j)."""
+        p = self.params
+        sel = self._sel(sel)
+        ram = np.ascontiguousarray(np.asarray(ram, np.uint32).reshape((w << v), 2 * p.N1))
+        if sel.shape[0] != v:
+            raise ValueError("ramReadUnit: address width mismatch")
+        out = np.zeros((w, 2 * p.N1), np.uint32)
+        _check(lib().vsp_ram_read_unit(self.h, v, w, _ptr(ram), _ptr(sel), _ptr(out)))
+        return out
+
+    def ram_control_unit(self, read: np.ndarray, wflag, wdata):
+        """mem::ramControlUnit (mem.cpp:74-90): returns (readOut (w, n+1),
+        controlled (w, 2*N1))."""
+        p = self.params
+        read = np.ascontiguousarray(np.asarray(read, np.uint32).reshape(-1, 2 * p.N1))
+        w = read.shape[0]
+        f = np.ascontiguousarray(wflag, np.uint32)
+        d = np.ascontiguousarray(wdata, np.uint32)
+        if f.size != p.n + 1 or d.shape != (w, p.n + 1):
+            raise ValueError("ramControlUnit: word width mismatch")
+        ro = np.zeros((w, p.n + 1), np.uint32)
+        ctl = np.zeros((w, 2 * p.N1), np.uint32)
+        _check(lib().vsp_ram_control_unit(self.h, w, _ptr(read), _ptr(f), _ptr(d), _ptr(ro),
+                                          _ptr(ctl)))
+        return ro, ctl
+
+    def ram_write_unit(self, ram: np.ndarray, v: int, w: int, sel, controlled) -> np.ndarray:
+        """mem::ramWriteUnit (mem.cpp:92-120): returns the new RAM image."""
+        p = self.params
+        sel = self._sel(sel)
+        ram = np.array(np.asarray(ram, np.uint32).reshape((w << v), 2 * p.N1), np.uint32)
+        ctl = np.ascontiguousarray(np.asarray(controlled, np.uint32).reshape(-1, 2 * p.N1))
+        if sel.shape[0] != v or ctl.shape[0] != w:
+            raise ValueError("ramWriteUnit: geometry mismatch")
+        _check(lib().vsp_ram_write_unit(self.h, v, w, _ptr(ram), _ptr(sel), _ptr(ctl)))
+        return ram
+
+    def rom_read_sel(self, luts: np.ndarray, depth_bytes: int, sel) -> np.ndarray:
+        """mem::romRead (mem.cpp:137-177) on given selectors (vrom raw TRGSWs)."""
+        p = self.params
+        sel = self._sel(sel)
+        luts = np.ascontiguousarray(luts, np.uint32)
+        out = np.zeros((32, p.n + 1), np.uint32)
+        _check(lib().vsp_rom_read_sel(self.h, depth_bytes, _ptr(luts), luts.shape[0], _ptr(sel),
+                                      sel.shape[0], _ptr(out)))
         return out
 
     def ram_cycle_dev(self, d_ram: int, v: int, w: int, d_addr: int, d_wflag: int,

@@ -1012,29 +1012,15 @@ void iks_of_trlwes(vsp_ctx* c, const uint32_t* d_trlwe, int count, const int* se
     launch_iks(c, d_trlwe, d_gt, d_gl, count, d_out, st, d_se);
 }
 
-// ramCycle (mem.cpp:122-135) on a device-resident RAM image (updated in place).
-// pre_raw: the address TRGSWs when the caller has already circuit-bootstrapped them
-// (the netlist runner batches the CBs of every memory port of a level into one launch).
-void ram_cycle_dev(vsp_ctx* c, uint32_t* d_ram, int v, int w, const uint32_t* d_addr,
-                   const uint32_t* d_wflag, const uint32_t* d_wdata, uint32_t* d_readout,
-                   cudaStream_t st, const uint32_t* pre_raw = nullptr)
+// ramReadUnit (mem.cpp:49-72) on the prepared selectors (prepare_selectors: sel[d] at
+// index d): layer d halves every one of the w trees with sel[d], the address LSB driving
+// the first layer.  Returns the w read TRLWEs (in layerA or layerB).
+const uint32_t* ram_read_unit_dev(vsp_ctx* c, const uint32_t* d_ram, int v, int w, cudaStream_t st)
 {
-    require_cb(c);
     const Params& p = c->p;
-    if (v < 1 || w < 1 || v > kChainMax)
-        throw std::invalid_argument("ramCycle: geometry out of range");
-    const size_t cw = 2 * (size_t)p.N1, words = (size_t)1 << v, n1 = p.n + 1;
-    // 1. addressToTrgsw + prepareAddress
-    const uint32_t* raw = pre_raw;
-    if (!raw) {
-        uint32_t* r = c->cbraw.as<uint32_t>(v * trgsw_words(p));
-        cb_batch(c, d_addr, v, r, st);
-        raw = r;
-    }
-    prepare_selectors(c, raw, v, st);
-    // 2. ramReadUnit (mem.cpp:49-72): layer d halves every tree with sel[d]
-    uint32_t* A = c->layerA.as<uint32_t>((size_t)w * (words / 2) * cw);
-    uint32_t* B = c->layerB.as<uint32_t>((size_t)w * (words / 2) * cw);
+    const size_t cw = 2 * (size_t)p.N1, words = (size_t)1 << v;
+    uint32_t* A = c->layerA.as<uint32_t>((size_t)w * std::max<size_t>(words / 2, 1) * cw);
+    uint32_t* B = c->layerB.as<uint32_t>((size_t)w * std::max<size_t>(words / 2, 1) * cw);
     const uint32_t* src = d_ram;
     size_t size = words;
     for (int d = 0; d < v; d++) {
@@ -1053,8 +1039,17 @@ void ram_cycle_dev(vsp_ctx* c, uint32_t* d_ram, int v, int w, const uint32_t* d_
         src = dst;
         size = half;
     }
-    const uint32_t* read = src;  // w TRLWEs
-    // 3. ramControlUnit (mem.cpp:74-90)
+    return src;
+}
+
+// ramControlUnit (mem.cpp:74-90): readOut[j] = IKS(SE(read[j], 0)) and
+// controlled[j] = homMuxNoSeIks(wflag, wdata[j], readOut[j]) (ops.cpp:898-909).
+void ram_control_unit_dev(vsp_ctx* c, const uint32_t* read, int w, const uint32_t* d_wflag,
+                          const uint32_t* d_wdata, uint32_t* d_readout, uint32_t* controlled,
+                          cudaStream_t st)
+{
+    const Params& p = c->p;
+    const size_t n1 = p.n + 1, cw = 2 * (size_t)p.N1;
     iks_of_trlwes(c, read, w, nullptr, d_readout, st);
     uint32_t* mux_in = c->aux.as<uint32_t>(2 * (size_t)w * n1);
     mux_prep_kernel<<<2 * w, 128, 0, st>>>(d_wflag, d_wdata, d_readout, mux_in, w, (int)p.n);
@@ -1067,12 +1062,19 @@ void ram_cycle_dev(vsp_ctx* c, uint32_t* d_ram, int v, int w, const uint32_t* d_
         pr[j] = make_int2(2 * j, 2 * j + 1);
     int2* d_pr = c->pairs.as<int2>(w);
     VSP_CUDA_CHECK(cudaMemcpyAsync(d_pr, pr.data(), w * sizeof(int2), cudaMemcpyHostToDevice, st));
-    uint32_t* controlled = (v % 2 == 1) ? B : A;  // the buffer not holding `read`
-    controlled = (controlled == read) ? ((controlled == A) ? B : A) : controlled;
     trlwe_sum_mu_kernel<<<w, 256, 0, st>>>(mux_tr, d_pr, controlled, w, (int)p.N1);
     VSP_CUDA_CHECK(cudaGetLastError());
     c->launches++;
-    // 4. ramWriteUnit (mem.cpp:92-120): address-match chains, then noise refresh
+}
+
+// ramWriteUnit (mem.cpp:92-120) on the prepared selectors (sel[d] at d, notSel[d] at v + d):
+// per cell (j, A) the address-match chain t = cmux(A_d ? sel[d] : notSel[d], t, old) from
+// t = controlled[j], then the noise refresh cell = BR(IKS(SE(t, 0))), in place.
+void ram_write_unit_dev(vsp_ctx* c, uint32_t* d_ram, int v, int w, const uint32_t* controlled,
+                        cudaStream_t st)
+{
+    const Params& p = c->p;
+    const size_t cw = 2 * (size_t)p.N1, words = (size_t)1 << v, n1 = p.n + 1;
     const size_t cells = (size_t)w * words;
     uint32_t* chain_out = c->ram.as<uint32_t>(cells * cw);
     std::vector<ChainTask> tasks;
@@ -1124,6 +1126,38 @@ void ram_cycle_dev(vsp_ctx* c, uint32_t* d_ram, int v, int w, const uint32_t* d_
     launch_br(c, lw, d_ram, (int)cells, st);
 }
 
+void check_ram_geometry(int v, int w)
+{
+    if (v < 1 || w < 1 || v > kChainMax)
+        throw std::invalid_argument("ramCycle: geometry out of range");
+}
+
+// ramCycle (mem.cpp:122-135) on a device-resident RAM image (updated in place):
+// addressToTrgsw -> prepareAddress -> ramReadUnit -> ramControlUnit -> ramWriteUnit.
+// pre_raw: the address TRGSWs when the caller has already circuit-bootstrapped them
+// (the netlist runner batches the CBs of every memory port of a level into one launch).
+void ram_cycle_dev(vsp_ctx* c, uint32_t* d_ram, int v, int w, const uint32_t* d_addr,
+                   const uint32_t* d_wflag, const uint32_t* d_wdata, uint32_t* d_readout,
+                   cudaStream_t st, const uint32_t* pre_raw = nullptr)
+{
+    require_cb(c);
+    check_ram_geometry(v, w);
+    const uint32_t* raw = pre_raw;
+    if (!raw) {
+        uint32_t* r = c->cbraw.as<uint32_t>(v * trgsw_words(c->p));
+        cb_batch(c, d_addr, v, r, st);
+        raw = r;
+    }
+    prepare_selectors(c, raw, v, st);
+    const uint32_t* read = ram_read_unit_dev(c, d_ram, v, w, st);
+    // controlled goes to the layer buffer that does not hold `read`
+    uint32_t* A = c->layerA.as<uint32_t>(0);
+    uint32_t* B = c->layerB.as<uint32_t>(0);
+    uint32_t* controlled = (read == A) ? B : A;
+    ram_control_unit_dev(c, read, w, d_wflag, d_wdata, d_readout, controlled, st);
+    ram_write_unit_dev(c, d_ram, v, w, controlled, st);
+}
+
 int ctz32(uint32_t x)
 {
     int r = 0;
@@ -1139,7 +1173,10 @@ void rom_read_dev(vsp_ctx* c, const uint32_t* d_luts, int nluts, uint32_t depth_
                   const uint32_t* d_addr, int vrom, uint32_t* d_out, cudaStream_t st,
                   const uint32_t* pre_raw = nullptr)
 {
-    require_cb(c);
+    if (pre_raw)
+        require_keys(c);  // selectors given: romRead(rom, PreparedAddress) needs no CB key
+    else
+        require_cb(c);
     const Params& p = c->p;
     const uint32_t blocks = depth_bytes / 4;
     if (depth_bytes == 0 || depth_bytes % 4 || (blocks & (blocks - 1)))
@@ -1756,6 +1793,90 @@ int vsp_rom_read(vsp_ctx* c, uint32_t depth_bytes, const uint32_t* luts, uint32_
                      c->stream);
         VSP_CUDA_CHECK(cudaMemcpyAsync(out, d_io + vrom * n1, 32 * n1 * 4, cudaMemcpyDeviceToHost,
                                        c->stream));
+        VSP_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int vsp_rom_read_sel(vsp_ctx* c, uint32_t depth_bytes, const uint32_t* luts, uint32_t nluts,
+                     const uint32_t* sel, uint32_t vrom, uint32_t* out)
+{
+    return guard([&] {
+        CallScope cs(c, c->stream);
+        const Params& p = c->p;
+        const size_t n1 = p.n + 1, cw = 2 * (size_t)p.N1, tw = trgsw_words(p);
+        uint32_t* d_luts = c->romio.as<uint32_t>(std::max<size_t>(nluts, 1) * cw);
+        uint32_t* d_sel = c->cbraw.as<uint32_t>(std::max<size_t>(vrom, 1) * tw);
+        uint32_t* d_out = c->out.as<uint32_t>(32 * n1);
+        VSP_CUDA_CHECK(cudaMemcpyAsync(d_luts, luts, nluts * cw * 4, cudaMemcpyHostToDevice, c->stream));
+        VSP_CUDA_CHECK(cudaMemcpyAsync(d_sel, sel, vrom * tw * 4, cudaMemcpyHostToDevice, c->stream));
+        rom_read_dev(c, d_luts, (int)nluts, depth_bytes, nullptr, (int)vrom, d_out, c->stream, d_sel);
+        VSP_CUDA_CHECK(cudaMemcpyAsync(out, d_out, 32 * n1 * 4, cudaMemcpyDeviceToHost, c->stream));
+        VSP_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int vsp_ram_read_unit(vsp_ctx* c, uint32_t v, uint32_t w, const uint32_t* ram, const uint32_t* sel,
+                      uint32_t* out)
+{
+    return guard([&] {
+        CallScope cs(c, c->stream);
+        require_keys(c);
+        check_ram_geometry((int)v, (int)w);
+        const Params& p = c->p;
+        const size_t cw = 2 * (size_t)p.N1, cells = (size_t)w << v, tw = trgsw_words(p);
+        uint32_t* d_ram = c->ramio.as<uint32_t>(cells * cw);
+        uint32_t* d_sel = c->cbraw.as<uint32_t>(v * tw);
+        VSP_CUDA_CHECK(cudaMemcpyAsync(d_ram, ram, cells * cw * 4, cudaMemcpyHostToDevice, c->stream));
+        VSP_CUDA_CHECK(cudaMemcpyAsync(d_sel, sel, v * tw * 4, cudaMemcpyHostToDevice, c->stream));
+        prepare_selectors(c, d_sel, (int)v, c->stream);
+        const uint32_t* read = ram_read_unit_dev(c, d_ram, (int)v, (int)w, c->stream);
+        VSP_CUDA_CHECK(cudaMemcpyAsync(out, read, w * cw * 4, cudaMemcpyDeviceToHost, c->stream));
+        VSP_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int vsp_ram_control_unit(vsp_ctx* c, uint32_t w, const uint32_t* read, const uint32_t* wflag,
+                         const uint32_t* wdata, uint32_t* readout, uint32_t* controlled)
+{
+    return guard([&] {
+        CallScope cs(c, c->stream);
+        require_keys(c);
+        if (w == 0)
+            throw std::invalid_argument("ramControlUnit: word width mismatch");
+        const Params& p = c->p;
+        const size_t n1 = p.n + 1, cw = 2 * (size_t)p.N1;
+        uint32_t* d_read = c->layerA.as<uint32_t>(w * cw);
+        uint32_t* d_ctl = c->layerB.as<uint32_t>(w * cw);
+        uint32_t* d_io = c->in.as<uint32_t>((1 + 2 * (size_t)w) * n1);
+        uint32_t *d_wflag = d_io, *d_wdata = d_io + n1, *d_ro = d_wdata + w * n1;
+        VSP_CUDA_CHECK(cudaMemcpyAsync(d_read, read, w * cw * 4, cudaMemcpyHostToDevice, c->stream));
+        VSP_CUDA_CHECK(cudaMemcpyAsync(d_wflag, wflag, n1 * 4, cudaMemcpyHostToDevice, c->stream));
+        VSP_CUDA_CHECK(cudaMemcpyAsync(d_wdata, wdata, w * n1 * 4, cudaMemcpyHostToDevice, c->stream));
+        ram_control_unit_dev(c, d_read, (int)w, d_wflag, d_wdata, d_ro, d_ctl, c->stream);
+        VSP_CUDA_CHECK(cudaMemcpyAsync(readout, d_ro, w * n1 * 4, cudaMemcpyDeviceToHost, c->stream));
+        VSP_CUDA_CHECK(cudaMemcpyAsync(controlled, d_ctl, w * cw * 4, cudaMemcpyDeviceToHost, c->stream));
+        VSP_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int vsp_ram_write_unit(vsp_ctx* c, uint32_t v, uint32_t w, uint32_t* ram, const uint32_t* sel,
+                       const uint32_t* controlled)
+{
+    return guard([&] {
+        CallScope cs(c, c->stream);
+        require_keys(c);
+        check_ram_geometry((int)v, (int)w);
+        const Params& p = c->p;
+        const size_t cw = 2 * (size_t)p.N1, cells = (size_t)w << v, tw = trgsw_words(p);
+        uint32_t* d_ram = c->ramio.as<uint32_t>(cells * cw);
+        uint32_t* d_sel = c->cbraw.as<uint32_t>(v * tw);
+        uint32_t* d_ctl = c->layerA.as<uint32_t>(w * cw);
+        VSP_CUDA_CHECK(cudaMemcpyAsync(d_ram, ram, cells * cw * 4, cudaMemcpyHostToDevice, c->stream));
+        VSP_CUDA_CHECK(cudaMemcpyAsync(d_sel, sel, v * tw * 4, cudaMemcpyHostToDevice, c->stream));
+        VSP_CUDA_CHECK(cudaMemcpyAsync(d_ctl, controlled, w * cw * 4, cudaMemcpyHostToDevice, c->stream));
+        prepare_selectors(c, d_sel, (int)v, c->stream);
+        ram_write_unit_dev(c, d_ram, (int)v, (int)w, d_ctl, c->stream);
+        VSP_CUDA_CHECK(cudaMemcpyAsync(ram, d_ram, cells * cw * 4, cudaMemcpyDeviceToHost, c->stream));
         VSP_CUDA_CHECK(cudaStreamSynchronize(c->stream));
     });
 }
