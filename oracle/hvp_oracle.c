@@ -421,9 +421,54 @@ static void poly_mul_acc_exact32(uint32_t* acc, const int32_t* digits, const uin
     }
 }
 
+/* Full product out[0..2n) = a * b over Z/2^64 by Karatsuba (ring arithmetic only, so it
+ * equals the schoolbook sum word for word).  scratch: 4n words. */
+static void kara64(const uint64_t* a, const uint64_t* b, size_t n, uint64_t* out,
+                   uint64_t* scratch)
+{
+    if (n <= 32) {
+        memset(out, 0, 8 * 2 * n);
+        for (size_t i = 0; i < n; i++) {
+            const uint64_t x = a[i];
+            if (x == 0)
+                continue;
+            for (size_t j = 0; j < n; j++)
+                out[i + j] += x * b[j];
+        }
+        return;
+    }
+    const size_t h = n / 2;
+    uint64_t *sa = scratch, *sb = scratch + h, *z1 = scratch + 2 * h, *rest = scratch + 4 * h;
+    kara64(a, b, h, out, rest);              /* z0 -> out[0, n) */
+    kara64(a + h, b + h, h, out + n, rest);  /* z2 -> out[n, 2n) */
+    for (size_t i = 0; i < h; i++) {
+        sa[i] = a[i] + a[h + i];
+        sb[i] = b[i] + b[h + i];
+    }
+    kara64(sa, sb, h, z1, rest);             /* (a0 + a1)(b0 + b1) */
+    for (size_t i = 0; i < n; i++)
+        z1[i] -= out[i] + out[n + i];
+    for (size_t i = 0; i < n; i++)
+        out[h + i] += z1[i];
+}
+
+/* polyMulAccExact (poly.hpp:15-29) at 64 bits: acc += digits * poly mod (X^N + 1).  Large N
+ * goes through Karatsuba + the negacyclic fold -- the same exact integers mod 2^64 as the
+ * schoolbook loop, fast enough for full-size level-2 blind rotations in the tests. */
 static void poly_mul_acc_exact64(uint64_t* acc, const int32_t* digits, const uint64_t* poly,
                                  size_t N)
 {
+    if (N >= 256 && (N & (N - 1)) == 0) {
+        uint64_t* buf = malloc(8 * (N + 2 * N + 8 * N));
+        uint64_t *a = buf, *prod = buf + N, *scratch = buf + 3 * N;
+        for (size_t i = 0; i < N; i++)
+            a[i] = (uint64_t)(int64_t)digits[i];
+        kara64(a, poly, N, prod, scratch);
+        for (size_t i = 0; i < N; i++)
+            acc[i] += prod[i] - prod[N + i];
+        free(buf);
+        return;
+    }
     for (size_t i = 0; i < N; i++) {
         const uint64_t d = (uint64_t)(int64_t)digits[i];
         if (d == 0)
@@ -1236,6 +1281,51 @@ int orc_blind_rotate_lvl2(orc_ctx* c, const uint32_t* in, const uint64_t* testve
     if (!c->has_cb)
         return fail("no circuit-bootstrapping material");
     blind_rotate64(c, in, testvec, out);
+    return 0;
+}
+
+/* T level-2 blind rotations (test vector b = h[t]/2 everywhere) on `threads` host threads:
+ * the level-2 half of circuitBootstrap (ops.cpp:914-935) for the parity tests. */
+typedef struct {
+    const orc_ctx* c;
+    const uint32_t* in;
+    const uint64_t* h;
+    uint64_t* out;
+    size_t T;
+    atomic_size_t next;
+} br2_job;
+
+static void* br2_worker(void* arg)
+{
+    br2_job* j = arg;
+    const uint32_t N = j->c->p.N2, n1 = j->c->p.n + 1;
+    uint64_t* tv = calloc(2 * (size_t)N, 8);
+    for (;;) {
+        const size_t t = atomic_fetch_add(&j->next, 1);
+        if (t >= j->T)
+            break;
+        for (uint32_t k = 0; k < N; k++)
+            tv[N + k] = j->h[t] / 2;
+        blind_rotate64(j->c, j->in + t * n1, tv, j->out + t * 2 * (size_t)N);
+    }
+    free(tv);
+    return NULL;
+}
+
+int orc_blind_rotate_lvl2_batch(orc_ctx* c, const uint32_t* in, const uint64_t* h,
+                                uint64_t* out, size_t T, unsigned threads)
+{
+    if (!c->has_cb)
+        return fail("no circuit-bootstrapping material");
+    if (threads < 1)
+        threads = 1;
+    br2_job j = {c, in, h, out, T, 0};
+    pthread_t* th = malloc(sizeof(pthread_t) * threads);
+    for (unsigned i = 0; i < threads; i++)
+        pthread_create(&th[i], NULL, br2_worker, &j);
+    for (unsigned i = 0; i < threads; i++)
+        pthread_join(th[i], NULL);
+    free(th);
     return 0;
 }
 

@@ -57,6 +57,9 @@ int orc_gate_bootstrap(orc_ctx* c, const uint32_t* in, uint32_t* out);
 int orc_bootstrap_to_trlwe(orc_ctx* c, const uint32_t* in, uint32_t* out);
 int orc_blind_rotate_lvl2(orc_ctx* c, const uint32_t* in, const uint64_t* testvec,
                           uint64_t* out);
+/* T level-2 blind rotations with test vectors b = h[t]/2 on `threads` threads. */
+int orc_blind_rotate_lvl2_batch(orc_ctx* c, const uint32_t* in, const uint64_t* h,
+                                uint64_t* out, size_t T, unsigned threads);
 int orc_identity_key_switch(orc_ctx* c, const uint32_t* in, uint32_t* out);
 int orc_sample_extract(orc_ctx* c, const uint32_t* trlwe, uint32_t k, uint32_t* out);
 int orc_external_product(orc_ctx* c, const uint32_t* trgsw, const uint32_t* trlwe,

@@ -60,6 +60,8 @@ def _lib(kind: str) -> ctypes.CDLL:
         getattr(L, f"{p}_trlwe_encrypt").argtypes = [vp, vp, ctypes.c_double, vp]
         getattr(L, f"{p}_trgsw_encrypt").argtypes = [vp, ctypes.c_int, ctypes.c_double, vp]
         getattr(L, f"{p}_hom_gate_batch").argtypes = [vp, vp, vp, vp, sz, ctypes.c_uint]
+        if kind == "orc":
+            L.orc_blind_rotate_lvl2_batch.argtypes = [vp, vp, vp, vp, sz, ctypes.c_uint]
         if kind == "ref":
             L.ref_eval_new.restype = vp
             L.ref_eval_new.argtypes = [vp, ctypes.c_char_p, ctypes.c_uint]
@@ -74,6 +76,10 @@ def _lib(kind: str) -> ctypes.CDLL:
             L.ref_serialize_tlwe.argtypes = [vp, vp, vp, sz, ctypes.POINTER(sz)]
             L.ref_serialize_ram.argtypes = [vp, u32, u32, vp, vp, sz, ctypes.POINTER(sz)]
             L.ref_serialize_rom.argtypes = [vp, u32, vp, u32, vp, sz, ctypes.POINTER(sz)]
+            L.ref_ram_read_unit.argtypes = [vp, u32, u32, vp, vp, vp, ctypes.c_uint]
+            L.ref_ram_control_unit.argtypes = [vp, u32, vp, vp, vp, vp, vp, ctypes.c_uint]
+            L.ref_ram_write_unit.argtypes = [vp, u32, u32, vp, vp, vp, ctypes.c_uint]
+            L.ref_rom_read_sel.argtypes = [vp, u32, vp, u32, vp, u32, vp, ctypes.c_uint]
             L.ref_eval_snapshot_load.restype = vp
             L.ref_eval_snapshot_load.argtypes = [vp, ctypes.c_char_p, vp, sz, ctypes.c_uint]
         _libs[kind] = L
@@ -267,6 +273,16 @@ class CpuTfhe:
                                                  _ptr(tv), _ptr(out)))
         return out
 
+    def blind_rotate_lvl2_batch(self, cts: np.ndarray, h, threads: int = 1) -> np.ndarray:
+        """T level-2 blind rotations with test vectors b = h[t]/2 (restatement only)."""
+        assert self.kind == "orc"
+        cts = np.ascontiguousarray(np.atleast_2d(cts), np.uint32)
+        hv = np.ascontiguousarray(np.broadcast_to(np.asarray(h, np.uint64), (cts.shape[0],)))
+        out = np.zeros((cts.shape[0], 2 * self.N2), np.uint64)
+        self._check(self.L.orc_blind_rotate_lvl2_batch(self.h, _ptr(cts), _ptr(hv), _ptr(out),
+                                                       cts.shape[0], threads))
+        return out
+
     def private_key_switch(self, t2: np.ndarray, which: int):
         out = np.zeros(2 * self.N1, np.uint32)
         self._check(self._f("private_key_switch")(self.h, _ptr(np.ascontiguousarray(t2)),
@@ -325,6 +341,46 @@ class CpuTfhe:
             rc = self.L.orc_rom_read(self.h, depth_bytes, _ptr(lu), lu.shape[0], _ptr(a), vrom,
                                      _ptr(out))
         self._check(rc)
+        return out
+
+    # ---- the units of ramCycle / romRead on given selectors (reference only) ----------
+    def _need_ref(self):
+        if self.kind != "ref":
+            raise NotImplementedError("memory units on selectors: reference checker only")
+
+    def ram_read_unit(self, ram, v, w, sel, threads: int = 1) -> np.ndarray:
+        self._need_ref()
+        out = np.zeros((w, 2 * self.N1), np.uint32)
+        self._check(self.L.ref_ram_read_unit(self.h, v, w, _ptr(np.ascontiguousarray(ram)),
+                                             _ptr(np.ascontiguousarray(sel)), _ptr(out),
+                                             threads))
+        return out
+
+    def ram_control_unit(self, read, wflag, wdata, threads: int = 1):
+        self._need_ref()
+        w = read.shape[0]
+        ro = np.zeros((w, self.n + 1), np.uint32)
+        ctl = np.zeros((w, 2 * self.N1), np.uint32)
+        self._check(self.L.ref_ram_control_unit(
+            self.h, w, _ptr(np.ascontiguousarray(read)), _ptr(np.ascontiguousarray(wflag)),
+            _ptr(np.ascontiguousarray(wdata)), _ptr(ro), _ptr(ctl), threads))
+        return ro, ctl
+
+    def ram_write_unit(self, ram, v, w, sel, controlled, threads: int = 1) -> np.ndarray:
+        self._need_ref()
+        ram = np.array(ram, np.uint32)
+        self._check(self.L.ref_ram_write_unit(self.h, v, w, _ptr(ram),
+                                              _ptr(np.ascontiguousarray(sel)),
+                                              _ptr(np.ascontiguousarray(controlled)), threads))
+        return ram
+
+    def rom_read_sel(self, luts, depth_bytes, sel, threads: int = 1) -> np.ndarray:
+        self._need_ref()
+        sel = np.ascontiguousarray(sel)
+        out = np.zeros((32, self.n + 1), np.uint32)
+        lu = np.ascontiguousarray(luts)
+        self._check(self.L.ref_rom_read_sel(self.h, depth_bytes, _ptr(lu), lu.shape[0],
+                                            _ptr(sel), sel.shape[0], _ptr(out), threads))
         return out
 
     def counters(self) -> np.ndarray:

@@ -522,6 +522,99 @@ int ref_rom_read(void* h, uint32_t depth_bytes, const uint32_t* luts, uint32_t n
     });
 }
 
+// The units of ramCycle / romRead on given selectors (RamAddress: v raw TRGSWs, LSB
+// first), each through prepareAddress (mem.cpp:21-36) -- mem.hpp:75-124.
+namespace {
+mem::EncryptedRam toRam(const uint32_t* ram, uint32_t v, uint32_t w, uint32_t N)
+{
+    mem::EncryptedRam r;
+    r.geom.v = v;
+    r.geom.w = w;
+    const size_t cells = size_t{w} << v;
+    for (size_t i = 0; i < cells; i++)
+        r.cells.push_back(toTrlwe(ram + i * 2 * N, N));
+    return r;
+}
+
+mem::RamAddress toAddr(const uint32_t* sel, uint32_t v, uint32_t N, uint32_t l)
+{
+    mem::RamAddress a;
+    for (uint32_t d = 0; d < v; d++)
+        a.bits.push_back(toTrgsw(sel + size_t{d} * 2 * l * 2 * N, N, l));
+    return a;
+}
+}  // namespace
+
+int ref_ram_read_unit(void* h, uint32_t v, uint32_t w, const uint32_t* ram, const uint32_t* sel,
+                      uint32_t* out, unsigned threads)
+{
+    auto* c = static_cast<RefCtx*>(h);
+    return guard([&] {
+        const ParameterSet& p = c->params;
+        auto res = mem::ramReadUnit(toRam(ram, v, w, p.N1),
+                                    mem::prepareAddress(toAddr(sel, v, p.N1, p.l1), p), threads);
+        for (size_t j = 0; j < res.size(); j++)
+            fromTrlwe(res[j], out + j * 2 * p.N1);
+    });
+}
+
+int ref_ram_control_unit(void* h, uint32_t w, const uint32_t* read, const uint32_t* wflag,
+                         const uint32_t* wdata, uint32_t* readout, uint32_t* controlled,
+                         unsigned threads)
+{
+    auto* c = static_cast<RefCtx*>(h);
+    return guard([&] {
+        const ParameterSet& p = c->params;
+        std::vector<Trlwe> rd;
+        std::vector<Tlwe> d;
+        for (uint32_t j = 0; j < w; j++) {
+            rd.push_back(toTrlwe(read + size_t{j} * 2 * p.N1, p.N1));
+            d.push_back(toTlwe(wdata + size_t{j} * (p.n + 1), p.n, 0));
+        }
+        mem::ControlOut o = mem::ramControlUnit(rd, toTlwe(wflag, p.n, 0), d, c->bk.value(),
+                                                threads);
+        for (uint32_t j = 0; j < w; j++) {
+            fromTlwe(o.readOut[j], readout + size_t{j} * (p.n + 1));
+            fromTrlwe(o.controlled[j], controlled + size_t{j} * 2 * p.N1);
+        }
+    });
+}
+
+int ref_ram_write_unit(void* h, uint32_t v, uint32_t w, uint32_t* ram, const uint32_t* sel,
+                       const uint32_t* controlled, unsigned threads)
+{
+    auto* c = static_cast<RefCtx*>(h);
+    return guard([&] {
+        const ParameterSet& p = c->params;
+        std::vector<Trlwe> ctl;
+        for (uint32_t j = 0; j < w; j++)
+            ctl.push_back(toTrlwe(controlled + size_t{j} * 2 * p.N1, p.N1));
+        mem::EncryptedRam r =
+            mem::ramWriteUnit(toRam(ram, v, w, p.N1),
+                              mem::prepareAddress(toAddr(sel, v, p.N1, p.l1), p), ctl,
+                              c->bk.value(), threads);
+        for (size_t i = 0; i < r.cells.size(); i++)
+            fromTrlwe(r.cells[i], ram + i * 2 * p.N1);
+    });
+}
+
+int ref_rom_read_sel(void* h, uint32_t depth_bytes, const uint32_t* luts, uint32_t nluts,
+                     const uint32_t* sel, uint32_t vrom, uint32_t* out, unsigned threads)
+{
+    auto* c = static_cast<RefCtx*>(h);
+    return guard([&] {
+        const ParameterSet& p = c->params;
+        mem::EncryptedRom rom;
+        rom.depthBytes = depth_bytes;
+        for (uint32_t t = 0; t < nluts; t++)
+            rom.luts.push_back(toTrlwe(luts + size_t{t} * 2 * p.N1, p.N1));
+        auto res = mem::romRead(rom, mem::prepareAddress(toAddr(sel, vrom, p.N1, p.l1), p),
+                                c->bk.value(), threads);
+        for (size_t k = 0; k < res.size(); k++)
+            fromTlwe(res[k], out + k * (p.n + 1));
+    });
+}
+
 // Trivial (sk == nullptr) or secret-key encryption of a RAM/ROM image.
 int ref_encrypt_ram(void* h, const uint8_t* image, uint32_t v, uint32_t w,
                     int trivial, uint32_t* out)

@@ -205,6 +205,16 @@ def trlwe_encrypt(params: ParameterSet, lv1: np.ndarray, bit_polys, seed: int) -
     return out
 
 
+def trlwe_phase_at(lv1: np.ndarray, ct: np.ndarray, k: int = 0) -> np.ndarray:
+    """trlwePhaseAt (ops.cpp:494-505) of coefficient k for (count, 2N) TRLWEs (u32)."""
+    ct = np.ascontiguousarray(np.atleast_2d(ct), np.uint32)
+    N = ct.shape[1] // 2
+    ph = np.zeros(ct.shape[0], np.uint32)
+    _ccheck(lib().vsp_client_trlwe_phase_at(_ptr(np.ascontiguousarray(lv1, np.uint32)), N,
+                                            _ptr(ct), ct.shape[0], k, _ptr(ph)))
+    return ph
+
+
 def trlwe_decrypt_at(lv1: np.ndarray, ct: np.ndarray, k: int = 0) -> np.ndarray:
     """trlweDecryptAt (ops.cpp:507-510) for (count, 2N) TRLWEs."""
     ct = np.ascontiguousarray(np.atleast_2d(ct), np.uint32)

@@ -43,3 +43,24 @@ def random_gate_batch(o: CpuTfhe, rng, G, kinds=None):
         for i in range(3):
             ins[g, i] = o.encrypt(int(bits[g, i]))
     return ks, bits, ins
+
+
+@functools.lru_cache(maxsize=None)
+def keys_with_cb(n: int, seed: int) -> dict:
+    """tfhe-80 keys with circuit-bootstrapping material at LWE dimension n (the engine's
+    client keygen: the reference's CSPRNG stream and draw order, bit-identical keys)."""
+    import paper_2010_09410_b200 as vsp
+    return vsp.keygen(vsp.ParameterSet("tfhe-80", n_override=n), seed, True)
+
+
+def phase_error(ph, bits, mu=1 << 29) -> np.ndarray:
+    """phaseError (test_tfhe.cpp:80-86): |phase - (+-mu)| / 2^32 per ciphertext."""
+    ph = np.asarray(ph, np.uint32)
+    want = np.where(np.asarray(bits) != 0, np.uint32(mu), np.uint32((1 << 32) - mu))
+    return np.abs((ph - want).astype(np.uint32).view(np.int32).astype(np.float64)) / 2.0 ** 32
+
+
+def stddev_of_errors(err) -> float:
+    """stddevOfErrors (test_tfhe.cpp:88-94): root mean square of the errors."""
+    err = np.asarray(err, np.float64)
+    return float(np.sqrt(np.mean(err * err)))

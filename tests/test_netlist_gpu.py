@@ -26,9 +26,12 @@ def words_to_image(words, v, w):
 
 
 class RefEval:
-    def __init__(self, r: CpuTfhe, text: str):
+    """The reference's own Evaluator<TfheBackend> (oracle/_ref, ref_shim.cpp)."""
+
+    def __init__(self, r: CpuTfhe, text: str, threads: int = 4):
         self.r, self.L = r, r.L
-        self.h = ctypes.c_void_p(self.L.ref_eval_new(r.h, text.encode(), 4))
+        self.threads = threads
+        self.h = ctypes.c_void_p(self.L.ref_eval_new(r.h, text.encode(), threads))
         assert self.h.value, self.L.ref_last_error()
 
     def set_input(self, port, idx, ct):
@@ -60,7 +63,13 @@ class RefEval:
                                        luts.shape[0], self.r.N1) == 0
 
     def run(self, cycles):
-        assert self.L.ref_eval_run(self.h, cycles, 4, 0, None) == 0, self.L.ref_last_error()
+        assert self.L.ref_eval_run(self.h, cycles, self.threads, 0, None) == 0, \
+            self.L.ref_last_error()
+
+    def set_dff(self, state):
+        state = np.ascontiguousarray(state, np.uint32)
+        assert self.L.ref_eval_set_dff(self.h, state.ctypes.data_as(ctypes.c_void_p),
+                                       ctypes.c_uint32(self.r.n)) == 0
 
 
 @pytest.mark.skipif(not pyoracle.available("ref"), reason="reference not built")
