@@ -273,6 +273,14 @@ int vsp_client_keygen(const vsp_params* params, uint64_t seed, int with_cb, uint
                       uint32_t* lv1, uint32_t* lv2, uint32_t* bk1, uint32_t* ksk,
                       uint64_t* bk2, uint32_t* pks_negs, uint32_t* pks_id);
 
+/* Same keys, bit for bit, with the b = a*s products of every TRLWE-of-zero encryption
+ * (bk1, bk2 and the 2 x 143,430 private key-switching rows: ~3e11 torus adds at tfhe-80)
+ * computed on CUDA device `device`; the CSPRNG draws stay on the host in reference order.
+ * (client key generation, ops.cpp:264-385.) */
+int vsp_client_keygen_dev(const vsp_params* params, uint64_t seed, int with_cb, int device,
+                          uint32_t* lv0, uint32_t* lv1, uint32_t* lv2, uint32_t* bk1,
+                          uint32_t* ksk, uint64_t* bk2, uint32_t* pks_negs, uint32_t* pks_id);
+
 /* tlweEncrypt (ops.cpp:428-440) of count bits, one CSPRNG stream from seed. */
 int vsp_client_tlwe_encrypt(const vsp_params* params, const uint32_t* lv0, uint64_t seed,
                             const uint8_t* bits, size_t count, uint32_t* out);

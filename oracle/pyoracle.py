@@ -23,6 +23,25 @@ LIB_PATHS = {
     "ref": os.path.join(HERE, "_ref", "libhvpref.so"),
 }
 
+
+def _stock_level() -> str:
+    """ISA level of the reference's stock (-march=native) build for THIS host: x86-64-v4
+    when the CPU has AVX-512, else v3 (oracle/Makefile ref-stock)."""
+    try:
+        flags = open("/proc/cpuinfo").read()
+    except OSError:
+        flags = ""
+    return "v4" if " avx512f" in flags and " avx512vl" in flags else "v3"
+
+
+# "ref_stock": the reference built like its own CMake Release (-O3 -DNDEBUG, native ISA):
+# timing only, never a checker (its FP contraction differs from the parity build).
+LIB_PATHS["ref_stock"] = os.path.join(HERE, "_ref", f"stock_{_stock_level()}", "libhvpref.so")
+
+
+def _prefix(kind: str) -> str:
+    return "orc" if kind == "orc" else "ref"
+
 GATE_KINDS = ["AND", "ANDNOT", "MUX", "NAND", "NOR", "NOT", "OR", "ORNOT", "XNOR", "XOR"]
 MU32 = 1 << 29
 
@@ -31,7 +50,7 @@ _libs: dict[str, ctypes.CDLL] = {}
 
 def build(kind: str = "all") -> None:
     target = {"orc": "oracle", "ref": "ref", "all": "all"}[kind]
-    subprocess.run(["make", "-s", "-C", HERE, target], check=True)
+    subprocess.run(["make", "-s", f"-j{os.cpu_count() or 1}", "-C", HERE, target], check=True)
 
 
 def available(kind: str) -> bool:
@@ -44,7 +63,7 @@ def _lib(kind: str) -> ctypes.CDLL:
         if not os.path.exists(path):
             raise FileNotFoundError(f"{path} missing; run `make -C oracle`")
         L = ctypes.CDLL(path)
-        p = kind
+        p = _prefix(kind)
         vp, u32, u64, sz = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_size_t
         getattr(L, f"{p}_ctx_new").restype = vp
         getattr(L, f"{p}_ctx_new").argtypes = [ctypes.c_char_p, u32, u64]
@@ -62,7 +81,7 @@ def _lib(kind: str) -> ctypes.CDLL:
         getattr(L, f"{p}_hom_gate_batch").argtypes = [vp, vp, vp, vp, sz, ctypes.c_uint]
         if kind == "orc":
             L.orc_blind_rotate_lvl2_batch.argtypes = [vp, vp, vp, vp, sz, ctypes.c_uint]
-        if kind == "ref":
+        if p == "ref":
             L.ref_eval_new.restype = vp
             L.ref_eval_new.argtypes = [vp, ctypes.c_char_p, ctypes.c_uint]
             L.ref_eval_run.argtypes = [vp, u64, ctypes.c_uint, u64, vp]
@@ -97,6 +116,7 @@ class CpuTfhe:
     def __init__(self, kind: str, params: str = "test-det", n_override: int = 0,
                  seed: int = 20200729):
         self.kind = kind
+        self.prefix = _prefix(kind)
         self.L = _lib(kind)
         self.h = self._f("ctx_new")(params.encode(), n_override, seed)
         if not self.h:
@@ -110,7 +130,7 @@ class CpuTfhe:
         self.params_name = params
 
     def _f(self, name):
-        return getattr(self.L, f"{self.kind}_{name}")
+        return getattr(self.L, f"{self.prefix}_{name}")
 
     def _check(self, rc):
         if rc != 0:
@@ -320,7 +340,7 @@ class CpuTfhe:
         a = np.ascontiguousarray(addr)
         f = np.ascontiguousarray(wflag)
         d = np.ascontiguousarray(wdata)
-        if self.kind == "ref":
+        if self.prefix == "ref":
             rc = self.L.ref_ram_cycle(self.h, v, w, _ptr(ram), _ptr(a), _ptr(f), _ptr(d),
                                       _ptr(ro), threads)
         else:
@@ -334,7 +354,7 @@ class CpuTfhe:
         out = np.zeros((32, self.n + 1), np.uint32)
         lu = np.ascontiguousarray(luts)
         a = np.ascontiguousarray(addr)
-        if self.kind == "ref":
+        if self.prefix == "ref":
             rc = self.L.ref_rom_read(self.h, depth_bytes, _ptr(lu), lu.shape[0], _ptr(a), vrom,
                                      _ptr(out), threads)
         else:
@@ -345,7 +365,7 @@ class CpuTfhe:
 
     # ---- the units of ramCycle / romRead on given selectors (reference only) ----------
     def _need_ref(self):
-        if self.kind != "ref":
+        if self.prefix != "ref":
             raise NotImplementedError("memory units on selectors: reference checker only")
 
     def ram_read_unit(self, ram, v, w, sel, threads: int = 1) -> np.ndarray:

@@ -81,6 +81,8 @@ def lib() -> ctypes.CDLL:
         L.vsp_sm_count.argtypes = [vp]
         L.vsp_fp64_peak_probe.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
         L.vsp_client_keygen.argtypes = [ctypes.POINTER(VspParams), u64, ctypes.c_int] + [vp] * 8
+        L.vsp_client_keygen_dev.argtypes = [ctypes.POINTER(VspParams), u64, ctypes.c_int,
+                                            ctypes.c_int] + [vp] * 8
         L.vsp_client_tlwe_encrypt.argtypes = [ctypes.POINTER(VspParams), vp, u64, vp, sz, vp]
         L.vsp_client_tlwe_decrypt.argtypes = [vp, u32, vp, sz, vp, vp]
         L.vsp_client_trlwe_encrypt.argtypes = [ctypes.POINTER(VspParams), vp, u64, vp, sz, vp]
@@ -147,9 +149,12 @@ class ParameterSet:
 # ---------------------------------------------------------------------------
 # client side (Alice)
 
-def keygen(params: ParameterSet, seed: int, with_cb: bool | int = False) -> dict:
+def keygen(params: ParameterSet, seed: int, with_cb: bool | int = False,
+           device: int | None = None) -> dict:
     """genSecretKey + BootstrappingKey::generate (ops.cpp:264-385), raw arrays.
-    with_cb=2 draws bk2 but not the private key-switching tables (unit tests)."""
+    with_cb=2 draws bk2 but not the private key-switching tables (unit tests).
+    device: run the b = a*s products on that CUDA device (vsp_client_keygen_dev; the same
+    keys bit for bit), else on host threads."""
     p = params
     full_cb = int(with_cb) == 1
     k = dict(
@@ -161,10 +166,12 @@ def keygen(params: ParameterSet, seed: int, with_cb: bool | int = False) -> dict
         pks_negs=np.zeros(p.pks_words(), np.uint32) if full_cb else None,
         pks_id=np.zeros(p.pks_words(), np.uint32) if full_cb else None,
     )
-    _ccheck(lib().vsp_client_keygen(ctypes.byref(p.c), seed, int(with_cb), _ptr(k["lv0"]),
-                                     _ptr(k["lv1"]), _ptr(k["lv2"]), _ptr(k["bk1"]),
-                                     _ptr(k["ksk"]), _ptr(k["bk2"]), _ptr(k["pks_negs"]),
-                                     _ptr(k["pks_id"])))
+    outs = [_ptr(k[x]) for x in ("lv0", "lv1", "lv2", "bk1", "ksk", "bk2", "pks_negs", "pks_id")]
+    if device is not None:
+        _check(lib().vsp_client_keygen_dev(ctypes.byref(p.c), seed, int(with_cb), int(device),
+                                           *outs))
+    else:
+        _ccheck(lib().vsp_client_keygen(ctypes.byref(p.c), seed, int(with_cb), *outs))
     return k
 
 

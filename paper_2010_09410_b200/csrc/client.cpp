@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "../../include/vsp_b200.h"
+#include "client_internal.h"
 
 namespace {
 
@@ -240,7 +241,22 @@ int vsp_client_keygen(const vsp_params* pp, uint64_t seed, int with_cb, uint32_t
                       uint32_t* pks_negs, uint32_t* pks_id)
 {
     return cguard([&] {
-        const vsp_params& p = *pp;
+        vsp_internal::keygen(*pp, seed, with_cb, lv0, lv1, lv2, bk1, ksk, bk2, pks_negs, pks_id,
+                             {});
+    });
+}
+
+}  // extern "C"
+
+// The sequential CSPRNG draws in reference order; every b = a*s product (the TRLWE-of-
+// zero encryptions of bk1, bk2 and the private key-switching tables) is deferred to
+// `fin` (host threads when empty; the GPU in vsp_client_keygen_dev).
+void vsp_internal::keygen(const vsp_params& p, uint64_t seed, int with_cb, uint32_t* lv0,
+                          uint32_t* lv1, uint32_t* lv2, uint32_t* bk1, uint32_t* ksk,
+                          uint64_t* bk2, uint32_t* pks_negs, uint32_t* pks_id,
+                          const Finalizer& fin)
+{
+    {
         const Alphas al = alphas_for(p);
         Csprng rng(seed);
         for (uint32_t i = 0; i < p.n; i++)
@@ -300,9 +316,21 @@ int vsp_client_keygen(const vsp_params* pp, uint64_t seed, int with_cb, uint32_t
                         }
             }
         }
-        finalize_parallel(j1, lv1);
-        finalize_parallel(j2, lv2);
-        finalize_parallel(jp, lv1);
+        if (fin) {
+            // each group is one contiguous array of (a[N], b[N]) pairs
+            fin(32, bk1, j1.size(), N1, lv1);
+            if (!j2.empty())
+                fin(64, bk2, j2.size(), N2, lv2);
+            if (!jp.empty()) {
+                fin(32, pks_negs, jp.size() / 2, N1, lv1);
+                fin(32, pks_id, jp.size() / 2, N1, lv1);
+            }
+        }
+        else {
+            finalize_parallel(j1, lv1);
+            finalize_parallel(j2, lv2);
+            finalize_parallel(jp, lv1);
+        }
         // gadget offsets of the TRGSWs of lv0[i] (ops.cpp:197-203)
         for (uint32_t i = 0; i < p.n; i++) {
             if (!lv0[i])
@@ -344,8 +372,10 @@ int vsp_client_keygen(const vsp_params* pp, uint64_t seed, int with_cb, uint32_t
                 }
             }
         }
-    });
+    }
 }
+
+extern "C" {
 
 // tlweEncrypt (ops.cpp:428-440) of count bits with one CSPRNG stream; alpha0 noise.
 int vsp_client_tlwe_encrypt(const vsp_params* pp, const uint32_t* lv0, uint64_t seed,

@@ -23,6 +23,7 @@
 #include "exact.cuh"
 #include "level2.cuh"
 #include "vsp_common.cuh"
+#include "client_internal.h"
 
 using namespace vsp;
 
@@ -1271,6 +1272,48 @@ void mem_pair_dev(vsp_ctx* c, const uint32_t* d_luts, int nluts, uint32_t depth_
 #include "snapshot.cuh"
 #include "hvp1.cuh"
 
+// Client keygen on the GPU: b += a * key for `count` consecutive
+// (a[N], b[N]) TRLWE pairs, key binary (polyMulBinary, poly.hpp:61-75).  One CTA per
+// pair: a is staged in smem as the negacyclic extension ext[m] = -a[m] (m < N),
+// a[m - N] (m >= N), so out[k] = sum_{i: key[i]} ext[k - i + N]; thread t owns outputs
+// k = t + 256 r, lanes read consecutive words (no bank conflicts), zero key bits are a
+// block-uniform skip.  Exact mod 2^bits like the reference loop.
+template <class T, int N>
+__global__ void __launch_bounds__(256) keygen_mul_binary_kernel(T* __restrict__ trlwes,
+                                                                const uint32_t* __restrict__ key,
+                                                                size_t count)
+{
+    __shared__ T ext[2 * N];
+    __shared__ uint8_t kb[N];
+    constexpr int R = N / 256;
+    const size_t c = blockIdx.x;
+    if (c >= count)
+        return;
+    T* a = trlwes + c * 2 * N;
+    T* b = a + N;
+    for (int m = threadIdx.x; m < N; m += 256) {
+        const T x = a[m];
+        ext[m] = (T)0 - x;
+        ext[m + N] = x;
+        kb[m] = (uint8_t)(key[m] & 1u);
+    }
+    __syncthreads();
+    T acc[R];
+#pragma unroll
+    for (int r = 0; r < R; r++)
+        acc[r] = 0;
+    for (int i = 0; i < N; i++) {
+        if (!kb[i])
+            continue;
+#pragma unroll
+        for (int r = 0; r < R; r++)
+            acc[r] += ext[threadIdx.x + 256 * r - i + N];
+    }
+#pragma unroll
+    for (int r = 0; r < R; r++)
+        b[threadIdx.x + 256 * r] += acc[r];
+}
+
 // DFMA throughput probe: 16 independent FMA chains per thread.
 __global__ void fp64_probe_kernel(double* out, int iters, double m)
 {
@@ -2386,6 +2429,62 @@ int vsp_profile_reset(vsp_ctx* c)
 }
 
 int vsp_sm_count(vsp_ctx* c) { return c->sms; }
+
+int vsp_client_keygen_dev(const vsp_params* pp, uint64_t seed, int with_cb, int device,
+                          uint32_t* lv0, uint32_t* lv1, uint32_t* lv2, uint32_t* bk1,
+                          uint32_t* ksk, uint64_t* bk2, uint32_t* pks_negs, uint32_t* pks_id)
+{
+    return guard([&] {
+        const vsp_params& p = *pp;
+        if ((p.N1 != 1024 && p.N1 != 64) || (p.N2 != 2048 && p.N2 != 128))
+            throw std::invalid_argument("keygen_dev: ring dimensions not supported");
+        VSP_CUDA_CHECK(cudaSetDevice(device));
+        cudaStream_t st;
+        VSP_CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        DevBuf buf, kbuf;
+        // chunked so the device buffer stays small; copies and kernels on one stream
+        auto fin = [&](int bits, void* trlwes, size_t count, size_t N, const uint32_t* key) {
+            const size_t pair = 2 * N * (bits / 8);
+            const size_t chunk = std::max<size_t>(1, (256u << 20) / pair);
+            uint32_t* d_key = kbuf.as<uint32_t>(N);
+            VSP_CUDA_CHECK(cudaMemcpyAsync(d_key, key, N * 4, cudaMemcpyHostToDevice, st));
+            for (size_t c0 = 0; c0 < count; c0 += chunk) {
+                const size_t cnt = std::min(chunk, count - c0);
+                uint8_t* h = static_cast<uint8_t*>(trlwes) + c0 * pair;
+                void* d = buf.ensure(cnt * pair);
+                VSP_CUDA_CHECK(cudaMemcpyAsync(d, h, cnt * pair, cudaMemcpyHostToDevice, st));
+                const unsigned g = (unsigned)cnt;
+                if (bits == 32 && N == 1024)
+                    keygen_mul_binary_kernel<uint32_t, 1024><<<g, 256, 0, st>>>((uint32_t*)d, d_key, cnt);
+                else if (bits == 64 && N == 2048)
+                    keygen_mul_binary_kernel<uint64_t, 2048><<<g, 256, 0, st>>>((uint64_t*)d, d_key, cnt);
+                else
+                    throw std::invalid_argument("keygen_dev: unsupported ring");
+                VSP_CUDA_CHECK(cudaGetLastError());
+                VSP_CUDA_CHECK(cudaMemcpyAsync(h + N * (bits / 8), (uint8_t*)d + N * (bits / 8),
+                                               cnt * pair - N * (bits / 8),
+                                               cudaMemcpyDeviceToHost, st));
+                VSP_CUDA_CHECK(cudaStreamSynchronize(st));
+            }
+        };
+        vsp_internal::Finalizer f;
+        if (p.N1 == 1024)
+            f = fin;  // test-det rings (N = 64 / 128) stay on the host threads
+        try {
+            vsp_internal::keygen(p, seed, with_cb, lv0, lv1, lv2, bk1, ksk, bk2, pks_negs, pks_id,
+                                 f);
+        }
+        catch (...) {
+            buf.release();
+            kbuf.release();
+            cudaStreamDestroy(st);
+            throw;
+        }
+        buf.release();
+        kbuf.release();
+        VSP_CUDA_CHECK(cudaStreamDestroy(st));
+    });
+}
 
 int vsp_br_plan(vsp_ctx* c, size_t tasks, int32_t out[3])
 {

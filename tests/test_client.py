@@ -2,6 +2,8 @@
 against the reference (golden key hashes)."""
 import hashlib
 
+import pytest
+
 import numpy as np
 
 import paper_2010_09410_b200 as vsp
@@ -54,3 +56,21 @@ def test_client_ram_rom_encryption_layout_matches_reference():
     for t in range(rom.shape[0]):
         for c in range(0, p.N1, 7):
             assert vsp.trlwe_decrypt_at(k["lv1"], rom[t], c)[0] == o.trlwe_decrypt_at(ref[t], c)
+
+
+@pytest.mark.gpu
+def test_client_keygen_on_gpu_equals_host_keygen_with_cb():
+    """vsp_client_keygen_dev (b = a*s products of bk1, bk2 and both private key-switching
+    tables on the GPU) yields the host keygen's keys bit for bit at n = 630 with
+    circuit-bootstrapping material; the host keygen is itself pinned to the reference's
+    BootstrappingKey::generate by the golden key hashes above."""
+    import time
+    from tests.helpers import keys_with_cb
+    p = vsp.ParameterSet("tfhe-80", n_override=630)
+    host = keys_with_cb(630, 630)
+    t0 = time.perf_counter()
+    dev = vsp.keygen(p, 630, True, device=0)
+    dt = time.perf_counter() - t0
+    for name in ["lv0", "lv1", "lv2", "bk1", "ksk", "bk2", "pks_negs", "pks_id"]:
+        assert np.array_equal(dev[name], host[name]), name
+    print(f"GPU keygen with CB at n=630: {dt:.1f} s")
