@@ -219,13 +219,29 @@ int vsp_netlist_set_cycle(vsp_netlist* nl, uint64_t cycle);
 /* ---- multi-GPU --------------------------------------------------------
  * One process per GPU.  Rank 0 creates an NCCL unique id, the host distributes it (e.g.
  * torch.distributed broadcast), every rank attaches its context.  Afterwards the
- * netlist runner shards each level's gates across the ranks (contiguous slices of
- * ceil(G/world)) and all-gathers the output TLWEs over NVLink; keys stay replicated.
+ * netlist runner shards each level's gates across the ranks (contiguous slices of equal
+ * blind-rotation task count) and all-gathers the output TLWEs over NVLink; keys stay
+ * replicated.  A RAM port is sharded by bit-block: rank r owns blocks
+ * [r w/world, (r+1) w/world) (read trees, control bits, write bars) and the read-out TLWEs
+ * are all-gathered; ramCycle / mem_ports on device buffers then update only the owned
+ * blocks of the RAM image (the host ramCycle, the runner's RAM getter and snapshots
+ * gather the whole image).  Circuit bootstraps and the ROM run redundantly on every rank.
  * The reference has no distributed path (parallelFor on host threads only). */
 int vsp_nccl_unique_id(uint8_t out[128]);
 int vsp_attach_comm(vsp_ctx* ctx, const uint8_t id[128], int rank, int world);
-/* The slice [lo, hi) of a G-gate level owned by `rank`; per = ceil(G / world) slots. */
+/* Host-callback exchange instead of NCCL (e.g. torch.distributed over gloo / TCP, or the
+ * tests' two processes on one GPU): allgather(send, recv, bytes, user) must fill
+ * recv[r * bytes ...] with rank r's `bytes` for every rank r (host buffers) and return 0.
+ * The engine stages its slice in pinned host memory around each call. */
+int vsp_attach_exchange(vsp_ctx* ctx, int rank, int world,
+                        int (*allgather)(const void* send, void* recv, size_t bytes, void* user),
+                        void* user);
+/* The slice [lo, hi) of a G-gate level owned by `rank`: slices hold equal numbers of
+ * blind-rotation TASKS (MUX = 2, NOT = 0, others 1); per = the largest slice (the
+ * all-gather's per-rank count).  kinds == NULL: all gates one task each. */
 int vsp_level_partition(size_t G, int world, int rank, size_t* lo, size_t* hi, size_t* per);
+int vsp_level_partition_kinds(const int32_t* kinds, size_t G, int world, int rank, size_t* lo,
+                              size_t* hi, size_t* per);
 /* homGate over one whole level, sharded across the attached ranks: every rank passes
  * all G gates' inputs (device) and receives all G outputs (device) on `stream`. */
 int vsp_hom_gate_level_dev(vsp_ctx* ctx, const int32_t* kinds, const uint32_t* d_in,

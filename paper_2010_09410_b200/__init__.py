@@ -26,6 +26,8 @@ _KIND_ID = {k: i for i, k in enumerate(GATE_KINDS)}
 MU32 = 1 << 29
 
 _lib = None
+_XCHG_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+                            ctypes.c_void_p)
 
 
 class VspParams(ctypes.Structure):
@@ -93,6 +95,10 @@ def lib() -> ctypes.CDLL:
                                           ctypes.POINTER(sz), ctypes.POINTER(sz),
                                           ctypes.POINTER(sz)]
         L.vsp_hom_gate_level_dev.argtypes = [vp, vp, vp, vp, sz, vp]
+        L.vsp_level_partition_kinds.argtypes = [vp, sz, ctypes.c_int, ctypes.c_int,
+                                                ctypes.POINTER(sz), ctypes.POINTER(sz),
+                                                ctypes.POINTER(sz)]
+        L.vsp_attach_exchange.argtypes = [vp, ctypes.c_int, ctypes.c_int, vp, vp]
         L.vsp_upload_keys_hvp1.argtypes = [vp, vp, sz]
         L.vsp_read_hvp1.argtypes = [vp, vp, sz, vp, sz, ctypes.POINTER(sz), vp]
         _lib = L
@@ -600,6 +606,24 @@ class Engine:
         _check(lib().vsp_attach_comm(self.h, _ptr(buf), int(rank), int(world)))
         self.rank, self.world = int(rank), int(world)
 
+    def attach_exchange(self, rank: int, world: int, allgather):
+        """Shard levels / the RAM over `world` ranks with a caller-provided all-gather
+        instead of NCCL: allgather(send: bytes) -> list of `world` bytes objects (one per
+        rank, in rank order), e.g. torch.distributed.all_gather_object over gloo."""
+        def cb(send, recv, nbytes, user):
+            try:
+                parts = allgather(ctypes.string_at(send, nbytes))
+                if len(parts) != world or any(len(x) != nbytes for x in parts):
+                    return 1
+                ctypes.memmove(recv, b"".join(parts), nbytes * world)
+                return 0
+            except Exception:  # an exception must not cross the C boundary
+                return 1
+        self._xchg_cb = _XCHG_FN(cb)  # keep the thunk alive while attached
+        _check(lib().vsp_attach_exchange(self.h, int(rank), int(world),
+                                         ctypes.cast(self._xchg_cb, ctypes.c_void_p), None))
+        self.rank, self.world = int(rank), int(world)
+
     def connect(self, group=None):
         """attach_comm over an initialised torch.distributed group (any backend): rank 0
         creates the NCCL id, a broadcast distributes it."""
@@ -628,12 +652,20 @@ def nccl_unique_id() -> bytes:
     return buf.tobytes()
 
 
-def level_partition(G: int, world: int, rank: int) -> tuple[int, int, int]:
-    """The runner's per-rank slice [lo, hi) of a G-gate level and the padded per-rank
-    slot count ceil(G / world) (multi.cuh level_slice)."""
+def level_partition(G: int, world: int, rank: int, kinds=None) -> tuple[int, int, int]:
+    """The runner's per-rank slice [lo, hi) of a G-gate level (slices of equal blind-
+    rotation task count: MUX 2, NOT 0, others 1; kinds=None: one task per gate) and the
+    all-gather's per-rank slot count (the largest slice; multi.cuh level_slice)."""
     lo, hi, per = ctypes.c_size_t(), ctypes.c_size_t(), ctypes.c_size_t()
-    _check(lib().vsp_level_partition(G, world, rank, ctypes.byref(lo), ctypes.byref(hi),
-                                     ctypes.byref(per)))
+    if kinds is None:
+        _check(lib().vsp_level_partition(G, world, rank, ctypes.byref(lo), ctypes.byref(hi),
+                                         ctypes.byref(per)))
+    else:
+        kid = Engine._kind_ids(kinds)
+        if kid.size != G:
+            raise ValueError(f"level_partition: {kid.size} kinds for {G} gates")
+        _check(lib().vsp_level_partition_kinds(_ptr(kid), G, world, rank, ctypes.byref(lo),
+                                               ctypes.byref(hi), ctypes.byref(per)))
     return int(lo.value), int(hi.value), int(per.value)
 
 

@@ -3,6 +3,8 @@
 // One translation unit: the kernels live in the included .cuh files.  Built for
 // sm_100a only (paper_2010_09410_b200/build.py).
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -80,6 +82,33 @@ struct DevBuf {
     {
         if (p)
             cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+// Pinned host staging buffer (host-callback exchanges).
+struct HostBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    template <class T>
+    T* as(size_t count)
+    {
+        const size_t bytes = count * sizeof(T);
+        if (bytes > cap) {
+            if (p)
+                cudaFreeHost(p);
+            p = nullptr;
+            cap = 0;
+            VSP_CUDA_CHECK(cudaMallocHost(&p, std::max<size_t>(bytes, 256)));
+            cap = std::max<size_t>(bytes, 256);
+        }
+        return static_cast<T*>(p);
+    }
+    void release()
+    {
+        if (p)
+            cudaFreeHost(p);
         p = nullptr;
         cap = 0;
     }
@@ -190,6 +219,10 @@ struct vsp_ctx {
     void* comm = nullptr;  // ncclComm_t
     int rank = 0, world = 1;
     DevBuf mg_send, mg_recv;
+    // host-callback exchange (vsp_attach_exchange) instead of NCCL
+    int (*xchg)(const void*, void*, size_t, void*) = nullptr;
+    void* xchg_user = nullptr;
+    HostBuf xchg_host;
     std::mutex mu;
     // optional per-kernel CUDA-event timing (bench.py's live roofline)
     bool profiling = false;
@@ -851,6 +884,11 @@ void hom_gate_dev(vsp_ctx* c, const int32_t* kinds, const uint32_t* d_in, uint32
     }
 }
 
+}  // namespace
+
+#include "multi.cuh"
+
+namespace {
 
 // ---------------------------------------------------------------------------
 // Circuit bootstrapping, selectors, CMUX chains, CMUX memory (mem.cpp)
@@ -1150,13 +1188,22 @@ void ram_cycle_dev(vsp_ctx* c, uint32_t* d_ram, int v, int w, const uint32_t* d_
         raw = r;
     }
     prepare_selectors(c, raw, v, st);
-    const uint32_t* read = ram_read_unit_dev(c, d_ram, v, w, st);
+    // multi-GPU: this rank runs the read trees, control bits and write bars of its own
+    // bit-blocks [j0, j1) (contiguous cells j * 2^v + A); the read-outs are all-gathered
+    const BlockRange br = ram_blocks(c, w);
+    const int wl = br.j1 - br.j0;
+    const size_t cw = 2 * (size_t)c->p.N1, n1 = c->p.n + 1;
+    uint32_t* ram_l = d_ram + ((size_t)br.j0 << v) * cw;
+    const uint32_t* read = ram_read_unit_dev(c, ram_l, v, wl, st);
     // controlled goes to the layer buffer that does not hold `read`
     uint32_t* A = c->layerA.as<uint32_t>(0);
     uint32_t* B = c->layerB.as<uint32_t>(0);
     uint32_t* controlled = (read == A) ? B : A;
-    ram_control_unit_dev(c, read, w, d_wflag, d_wdata, d_readout, controlled, st);
-    ram_write_unit_dev(c, d_ram, v, w, controlled, st);
+    ram_control_unit_dev(c, read, wl, d_wflag, d_wdata + (size_t)br.j0 * n1,
+                         d_readout + (size_t)br.j0 * n1, controlled, st);
+    if (br.shard)
+        exchange_allgather(c, d_readout + (size_t)br.j0 * n1, d_readout, (size_t)wl * n1 * 4, st);
+    ram_write_unit_dev(c, ram_l, v, wl, controlled, st);
 }
 
 int ctz32(uint32_t x)
@@ -1267,7 +1314,6 @@ void mem_pair_dev(vsp_ctx* c, const uint32_t* d_luts, int nluts, uint32_t depth_
 
 }  // namespace
 
-#include "multi.cuh"
 #include "runner.cuh"
 #include "snapshot.cuh"
 #include "hvp1.cuh"
@@ -1415,6 +1461,7 @@ void vsp_destroy(vsp_ctx* c)
             cudaFree(q);
     c->mg_send.release();
     c->mg_recv.release();
+    c->xchg_host.release();
     if (c->comm)
         nccl().commDestroy((ncclComm_t)c->comm);
     for (size_t k = 0; k < c->ev_in.size(); k++) {
@@ -1774,6 +1821,7 @@ int vsp_ram_cycle(vsp_ctx* c, uint32_t v, uint32_t w, uint32_t* ram, const uint3
         VSP_CUDA_CHECK(cudaMemcpyAsync(d_wflag, wflag, n1 * 4, cudaMemcpyHostToDevice, c->stream));
         VSP_CUDA_CHECK(cudaMemcpyAsync(d_wdata, wdata, w * n1 * 4, cudaMemcpyHostToDevice, c->stream));
         ram_cycle_dev(c, d_ram, (int)v, (int)w, d_addr, d_wflag, d_wdata, d_ro, c->stream);
+        ram_gather_dev(c, d_ram, (int)v, (int)w, c->stream);  // sharded RAM: whole image back
         VSP_CUDA_CHECK(cudaMemcpyAsync(readout, d_ro, w * n1 * 4, cudaMemcpyDeviceToHost, c->stream));
         VSP_CUDA_CHECK(cudaMemcpyAsync(ram, d_ram, cells * cw * 4, cudaMemcpyDeviceToHost, c->stream));
         VSP_CUDA_CHECK(cudaStreamSynchronize(c->stream));
@@ -2159,6 +2207,8 @@ int vsp_netlist_ram(vsp_netlist* nl, uint32_t v, uint32_t w, uint32_t* get, cons
         if (get) {
             if (!nl->has_ram || v != nl->ram_v || w != nl->ram_w)
                 throw std::runtime_error("RAM image not bound");
+            ram_gather_dev(c, nl->ram.as<uint32_t>(0), (int)v, (int)w, c->stream);
+            VSP_CUDA_CHECK(cudaStreamSynchronize(c->stream));
             VSP_CUDA_CHECK(cudaMemcpy(get, nl->ram.as<uint32_t>(0), words * 4, cudaMemcpyDeviceToHost));
         }
     });
@@ -2246,6 +2296,8 @@ int vsp_netlist_snapshot_save(vsp_netlist* nl, const char* param_name, uint8_t* 
     return guard([&] {
         vsp_ctx* c = nl->ctx;
         CallScope cs(c, c->stream);
+        if (nl->has_ram)
+            ram_gather_dev(c, nl->ram.as<uint32_t>(0), (int)nl->ram_v, (int)nl->ram_w, c->stream);
         VSP_CUDA_CHECK(cudaStreamSynchronize(c->stream));
         const std::vector<uint8_t> b = snapshot_save(nl, param_name ? param_name : "");
         *len = b.size();
@@ -2341,6 +2393,7 @@ int vsp_attach_comm(vsp_ctx* c, const uint8_t id[128], int rank, int world)
             nccl().commDestroy((ncclComm_t)c->comm);
             c->comm = nullptr;
         }
+        c->xchg = nullptr;
         c->rank = rank;
         c->world = world;
         // world == 1 normally runs without a communicator; VSP_NCCL_SINGLE=1 attaches a
@@ -2359,13 +2412,37 @@ int vsp_attach_comm(vsp_ctx* c, const uint8_t id[128], int rank, int world)
 
 int vsp_level_partition(size_t G, int world, int rank, size_t* lo, size_t* hi, size_t* per)
 {
+    return vsp_level_partition_kinds(nullptr, G, world, rank, lo, hi, per);
+}
+
+int vsp_level_partition_kinds(const int32_t* kinds, size_t G, int world, int rank, size_t* lo,
+                              size_t* hi, size_t* per)
+{
     return guard([&] {
         if (world < 1 || rank < 0 || rank >= world)
             throw std::invalid_argument("level_partition: bad rank/world");
-        const Slice sl = level_slice(G, world, rank);
+        const Slice sl = level_slice(kinds, G, world, rank);
         *lo = sl.lo;
         *hi = sl.hi;
         *per = sl.per;
+    });
+}
+
+int vsp_attach_exchange(vsp_ctx* c, int rank, int world,
+                        int (*allgather)(const void*, void*, size_t, void*), void* user)
+{
+    return guard([&] {
+        if (world < 1 || rank < 0 || rank >= world)
+            throw std::invalid_argument("attach_exchange: bad rank/world");
+        CallScope cs(c, c->stream);
+        if (c->comm) {
+            nccl().commDestroy((ncclComm_t)c->comm);
+            c->comm = nullptr;
+        }
+        c->rank = rank;
+        c->world = world;
+        c->xchg = allgather;
+        c->xchg_user = user;
     });
 }
 

@@ -542,10 +542,13 @@ class PlainEvaluator:
 class ShardedPlainEvaluator(PlainEvaluator):
     """The multi-GPU runner's schedule on plaintext bits (CPU, any torch.distributed
     backend, e.g. gloo): every ASAP level's gates are split with the runner's own
-    partition (level_partition, multi.cuh) and each rank evaluates only its slice; the
-    slices are all-gathered (the runner's ncclAllGather) before the next level; memory
-    ports and constants are evaluated on every rank, DFFs latch locally.  Must equal
-    PlainEvaluator exactly (tests/test_multi_cpu.py)."""
+    task-balanced partition (level_partition with the level's kinds, multi.cuh) and each
+    rank evaluates only its slice; the padded slices are all-gathered (the runner's
+    all-gather) and repacked before the next level.  The RAM is sharded by bit-block like
+    ram_cycle_dev: rank r reads and writes only bits [r w/world, (r+1) w/world) of each
+    word and the read-out bits are all-gathered.  The ROM and constants are evaluated on
+    every rank, DFFs latch locally.  Must equal PlainEvaluator exactly
+    (tests/test_multi_cpu.py)."""
 
     def __init__(self, nl: Netlist, group=None):
         super().__init__(nl)
@@ -570,7 +573,9 @@ class ShardedPlainEvaluator(PlainEvaluator):
                 vals[self.nl.cells[i].outputs[0]] = v
             for cells in self.levels:
                 gates = [ci for ci in cells if self.nl.cells[ci].kind in GATES]
-                lo, hi, per = self._part(len(gates), self.world, self.rank)
+                kinds = [self.nl.cells[ci].kind for ci in gates]
+                cut = [self._part(len(gates), self.world, r, kinds)[0] for r in range(self.world)]
+                lo, hi, per = self._part(len(gates), self.world, self.rank, kinds)
                 mine = [plain_gate(self.nl.cells[ci].kind,
                                    [vals[b] for b in self.nl.cells[ci].inputs])
                         for ci in gates[lo:hi]]
@@ -578,16 +583,47 @@ class ShardedPlainEvaluator(PlainEvaluator):
                 if gates:
                     box = [None] * self.world
                     dist.all_gather_object(box, mine + [0] * (per - len(mine)), group=self.group)
-                    flat = [x for part in box for x in part][:len(gates)]
+                    cut.append(len(gates))
+                    flat = [x for r in range(self.world) for x in box[r][:cut[r + 1] - cut[r]]]
                     for ci, v in zip(gates, flat):
                         vals[self.nl.cells[ci].outputs[0]] = v
                 for ci in cells:
                     c = self.nl.cells[ci]
                     if c.kind in GATES:
                         continue
-                    self._eval_port(c, vals)
+                    if c.kind == "RAM":
+                        self._eval_ram_sharded(c, vals)
+                    else:
+                        self._eval_port(c, vals)
             for i in self.dff:
                 self.dff[i] = vals[self.nl.cells[i].inputs[0]]
+
+
+    def _eval_ram_sharded(self, c, vals):
+        """ramCycle with the RAM sharded by bit-block (ram_cycle_dev, multi.cuh
+        ram_blocks): this rank owns bits [j0, j1) of every word."""
+        v, w, words = self.ram
+        if w % self.world:
+            return self._eval_port(c, vals)
+        x = [vals[b] for b in c.inputs]
+        j0, j1 = self.rank * w // self.world, (self.rank + 1) * w // self.world
+        a = sum(b << i for i, b in enumerate(x[:v]))
+        mine = [(words[a] >> j) & 1 for j in range(j0, j1)]  # read-before-write
+        if x[v + w]:
+            for j in range(j0, j1):
+                words[a] = (words[a] & ~(1 << j)) | (x[v + j] << j)
+        box = [None] * self.world
+        self._dist.all_gather_object(box, mine, group=self.group)
+        for k, o in enumerate(c.outputs):
+            vals[o] = box[k // (w // self.world)][k % (w // self.world)]
+
+    def owned_ram_bits(self) -> int:
+        """Mask of the word bits this rank keeps current (its bit-blocks)."""
+        v, w, _ = self.ram
+        if w % self.world:
+            return (1 << w) - 1
+        j0, j1 = self.rank * w // self.world, (self.rank + 1) * w // self.world
+        return ((1 << j1) - 1) ^ ((1 << j0) - 1)
 
 
 def plain_gate(kind, x):

@@ -44,12 +44,32 @@ def test_level_partition_covers_each_gate_once(world):
             per0 = per if per0 is None else per0
             assert per == per0 == -(-G // world)
             assert 0 <= hi - lo <= per
-            if hi > lo:
-                assert lo == r * per  # rank r's slice sits at slot r * per of the all-gather
+            if hi > lo and G % world == 0:
+                assert lo == r * per  # equal slices: rank r's slice is slot r * per
             seen.extend(range(lo, hi))
         assert seen == list(range(G))
     with pytest.raises(ValueError):
         vsp.level_partition(4, world, world)
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_level_partition_balances_blind_rotation_tasks(world):
+    """Slices hold equal numbers of blind-rotation tasks (MUX = 2, NOT = 0): every slice
+    is within one MUX of T / world, and together they cover each gate once."""
+    rng = np.random.default_rng(world)
+    for G in [5, 300, 4097]:
+        kinds = [vsp.GATE_KINDS[int(x)] for x in rng.integers(0, 10, G)]
+        if G == 300:
+            kinds = ["MUX"] * 150 + ["AND"] * 150  # heavy front: gate-count slices would skew
+        cost = [2 if k == "MUX" else 0 if k == "NOT" else 1 for k in kinds]
+        T = sum(cost)
+        seen = []
+        for r in range(world):
+            lo, hi, per = vsp.level_partition(G, world, r, kinds)
+            assert hi - lo <= per
+            assert abs(sum(cost[lo:hi]) - T / world) <= 2
+            seen.extend(range(lo, hi))
+        assert seen == list(range(G))
 
 
 def _setup(ev, nl, seed):
@@ -73,7 +93,8 @@ def _sharded_equals_single(rank, world):
     sh.run(3)
     assert sh.dff == ref.dff
     assert sh.values == ref.values
-    assert sh.ram == ref.ram
+    m = sh.owned_ram_bits()  # each rank keeps only its own bit-blocks of the RAM current
+    assert [x & m for x in sh.ram[2]] == [x & m for x in ref.ram[2]]
     n_gates = sum(1 for c in nl.cells if c.kind in N.GATES)
     total = [None] * world
     dist.all_gather_object(total, sh.gate_evals)
