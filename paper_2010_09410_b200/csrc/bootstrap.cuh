@@ -70,16 +70,8 @@ struct Br1024Smem {
     uint32_t tcnt[3];   // TM variant: warps done with a TMEM slot
     uint32_t tstart[3]; // TM variant: warps that started a chunk (the first refills smem)
     uint32_t taddr;     // TM variant: TMEM base (512 columns: three 128-column slots)
+    uint32_t go;        // OFS variant: the upper warp half may start
 };
-
-// (X^k p)[q] mod X^N + 1 (polyRotate, poly.hpp:32-48) = +-p[(q-k) mod 2N]; qk = q - k.
-__device__ __forceinline__ uint32_t rot_coef1024(const uint32_t* src, uint32_t qk)
-{
-    const uint32_t idx = qk & 2047u;
-    const uint32_t x = src[idx & 1023u];
-    const uint32_t neg = idx >> 10;  // 0 or 1
-    return (x ^ (0u - neg)) + neg;
-}
 
 // TM: the bootstrapping-key rows reach the warps through TENSOR MEMORY instead of shared-
 // memory loads: each 16 KiB chunk, staged in smem by the bulk-copy engine (S = 3 slots), is
@@ -89,12 +81,17 @@ __device__ __forceinline__ uint32_t rot_coef1024(const uint32_t* src, uint32_t q
 // port once per warp.  Chunk c lives in smem slot and TMEM slot c % 3: the first warp to
 // start chunk c (its copy is complete) bulk-loads chunk c + 3 into the smem slot, the last
 // warp to finish it copies chunk c + 3 into the TMEM slot.
-template <int WARPS, int S, int BG, bool TM = false>
+// OFS: the upper half of the warps starts half a step (two key chunks) after the lower
+// half, so the two warps sharing a scheduler (w, w + WARPS/2) run out of phase: one in its
+// FP64-bound butterflies while the other is in its shared-memory-bound transposes / key
+// reads.  Needs S >= 3 ring slots for the lead.
+template <int WARPS, int S, int BG, bool TM = false, bool OFS = false>
 __global__ void __launch_bounds__(WARPS * 32, 1)
     br1024_kernel(const uint32_t* __restrict__ tasks, const double2* __restrict__ bkfd,
                   const double2* __restrict__ tw2g, uint32_t* __restrict__ out, int T, int n)
 {
     static_assert(!TM || S == 3, "TM uses a three-slot smem ring");
+    static_assert(!OFS || (S >= 3 && !TM), "OFS needs >= 3 slots");
     extern __shared__ __align__(128) uint8_t smem_raw[];
     auto& sm = *reinterpret_cast<Br1024Smem<WARPS, S>*>(smem_raw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -108,6 +105,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     for (int i = threadIdx.x; i < kTw2Entries * 32; i += blockDim.x)
         sm.tw2[i] = tw2g[i];
     if (threadIdx.x == 0) {
+        sm.go = 0;
         for (int s = 0; s < S; s++) {
             mbar_init(&sm.full[s], 1);
             sm.cnt[s] = 0;
@@ -243,6 +241,14 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
         }
     };
 
+    if constexpr (OFS) {
+        if (warp >= WARPS / 2) {
+            if (lane == 0)
+                while (*reinterpret_cast<volatile uint32_t*>(&sm.go) == 0)
+                    __nanosleep(64);
+            __syncwarp();
+        }
+    }
 #pragma unroll 1
     for (int i = 0; i < n; i++) {
         const uint32_t bara = mod_switch_2n(lwe[i], 11);
@@ -318,6 +324,10 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
                     }
                 }
                 release(c);
+                if constexpr (OFS) {
+                    if (c == 1 && warp == 0 && lane == 0)
+                        atomicExch(&sm.go, 1u);  // lower half is two chunks ahead
+                }
             }
         }
         // inverse transforms, round (llrint, fft.hpp:47-50) and accumulate

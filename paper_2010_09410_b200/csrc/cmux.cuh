@@ -83,20 +83,21 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
             // d = c1' - c0' once per polynomial; level 0 digits straight into z, level 1
             // parked as 16-bit offset-binary pairs (decomposePoly, poly.hpp:79-97)
             double2 z[16];
+            // lane + 32 j from an opaque base so the compiler does not hoist 32 indices
+            // into registers (mode 1 spilled with them)
+            const uint32_t lo = (uint32_t)lane + (uint32_t)opaque_zero();
+            const uint32_t lk = lo - rot;
 #pragma unroll
             for (int j = 0; j < 16; j++) {
-                const uint32_t p0 = lane + 32 * j, p1 = p0 + 512;
+                const uint32_t p0 = lo + 32 * j, p1 = p0 + 512;
                 uint32_t d0, d1;
                 if (mode == 0) {
                     d0 = src[p0] - __ldg(bsrc + p0);
                     d1 = src[p1] - __ldg(bsrc + p1);
                 }
-                else {
-                    const uint32_t i0 = (p0 - rot) & 2047u, i1 = (p1 - rot) & 2047u;
-                    const uint32_t r0 = i0 < 1024 ? src[i0] : 0u - src[i0 - 1024];
-                    const uint32_t r1 = i1 < 1024 ? src[i1] : 0u - src[i1 - 1024];
-                    d0 = r0 - src[p0];
-                    d1 = r1 - src[p1];
+                else {  // (X^rot acc - acc) (polyMulByXkMinusOne, poly.hpp:51-57)
+                    d0 = rot_coef1024(src, lk + 32 * j) - src[p0];
+                    d1 = rot_coef1024(src, lk + 32 * j + 512) - src[p1];
                 }
                 const uint32_t v0 = d0 + offset, v1 = d1 + offset;
                 z[j].x = ob_to_double<15>((v0 >> sh1) + (32768u - half));

@@ -382,9 +382,42 @@ bool br_tmem()
     return on;
 }
 
+// VSP_BR_SLOTS = 3 / 4 (W = 8 only): deeper key ring; VSP_BR_OFS=1 adds the half-step
+// phase offset between the two warps of each scheduler (br1024_kernel OFS).  A/B knobs.
+int br_slots()
+{
+    static const int s = getenv("VSP_BR_SLOTS") ? atoi(getenv("VSP_BR_SLOTS")) : 2;
+    return s;
+}
+bool br_ofs()
+{
+    static const bool on = getenv("VSP_BR_OFS") && atoi(getenv("VSP_BR_OFS")) == 1;
+    return on;
+}
+
+template <int S, bool OFS>
+void launch_br8(vsp_ctx* c, const uint32_t* d_tasks, uint32_t* d_trlwe, int T, cudaStream_t st)
+{
+    br1024_kernel<8, S, kBrBg, false, OFS><<<(T + 7) / 8, 256, sizeof(Br1024Smem<8, S>), st>>>(
+        d_tasks, c->d_bk1fd, c->d_tw2, d_trlwe, T, (int)c->p.n);
+}
+
 template <int W>
 void launch_br_w(vsp_ctx* c, const uint32_t* d_tasks, uint32_t* d_trlwe, int T, cudaStream_t st)
 {
+    if constexpr (W == 8) {
+        const int sl = br_slots();
+        if (sl == 3) {
+            br_ofs() ? launch_br8<3, true>(c, d_tasks, d_trlwe, T, st)
+                     : launch_br8<3, false>(c, d_tasks, d_trlwe, T, st);
+            return;
+        }
+        if (sl == 4) {
+            br_ofs() ? launch_br8<4, true>(c, d_tasks, d_trlwe, T, st)
+                     : launch_br8<4, false>(c, d_tasks, d_trlwe, T, st);
+            return;
+        }
+    }
     if constexpr (W >= 5) {
         if (br_tmem()) {
             br1024_kernel<W, 3, kBrBg, true><<<(T + W - 1) / W, W * 32, sizeof(Br1024Smem<W, 3>),
@@ -408,6 +441,16 @@ void set_br_attr()
     // key-switch CTAs that co-run with the remainder wave
     VSP_CUDA_CHECK(cudaFuncSetAttribute(br1024_kernel<W, kBrSlots, kBrBg>,
                                         cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    if constexpr (W == 8) {
+        auto attr = [](auto k, int bytes) {
+            VSP_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+            VSP_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        };
+        attr(br1024_kernel<8, 3, kBrBg, false, false>, (int)sizeof(Br1024Smem<8, 3>));
+        attr(br1024_kernel<8, 3, kBrBg, false, true>, (int)sizeof(Br1024Smem<8, 3>));
+        attr(br1024_kernel<8, 4, kBrBg, false, false>, (int)sizeof(Br1024Smem<8, 4>));
+        attr(br1024_kernel<8, 4, kBrBg, false, true>, (int)sizeof(Br1024Smem<8, 4>));
+    }
     if constexpr (W >= 5) {
         VSP_CUDA_CHECK(cudaFuncSetAttribute(br1024_kernel<W, 3, kBrBg, true>,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -129,6 +129,15 @@ __device__ __forceinline__ void tmem_ld_x16(uint32_t taddr, uint32_t (&r)[16])
         : "r"(taddr));
 }
 
+// (X^k p)[q] mod X^N + 1 (polyRotate, poly.hpp:32-48) = +-p[(q-k) mod 2N]; qk = q - k.
+__device__ __forceinline__ uint32_t rot_coef1024(const uint32_t* src, uint32_t qk)
+{
+    const uint32_t idx = qk & 2047u;
+    const uint32_t x = src[idx & 1023u];
+    const uint32_t neg = idx >> 10;  // 0 or 1
+    return (x ^ (0u - neg)) + neg;
+}
+
 // modSwitch(2N, phase) (ops.cpp:49-55) for 2N = 2^log2_2N: the reference computes
 // ((phase<<32) + interval/2) / interval with interval = 2^(64-log2_2N), wrapping
 // mod 2^64; that equals (phase + 2^(31-log2_2N)) >> (32-log2_2N) in u32 arithmetic.
