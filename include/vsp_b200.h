@@ -272,6 +272,9 @@ int vsp_profile_reset(vsp_ctx* ctx);
 int vsp_br_plan(vsp_ctx* ctx, size_t tasks, int32_t out[3]);
 /* Streaming multiprocessors of the context's device (sizes every launch plan). */
 int vsp_sm_count(vsp_ctx* ctx);
+/* Engine tuning options (no reference counterpart; results are bit-identical either way):
+ *   "lat_tasks" 1|2: blind-rotation tasks per SM of narrow levels (br_lat / br_lat2). */
+int vsp_set_option(vsp_ctx* ctx, const char* name, int64_t value);
 
 /* Measured dense FP64 FMA throughput of `device` in TFLOP/s (the denominator of the
  * blind-rotation roofline; MEASURED_PEAKS.json carries no FP64 figure). */

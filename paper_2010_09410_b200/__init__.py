@@ -81,6 +81,7 @@ def lib() -> ctypes.CDLL:
         L.vsp_profile_reset.argtypes = [vp]
         L.vsp_br_plan.argtypes = [vp, sz, vp]
         L.vsp_sm_count.argtypes = [vp]
+        L.vsp_set_option.argtypes = [vp, ctypes.c_char_p, ctypes.c_int64]
         L.vsp_fp64_peak_probe.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
         L.vsp_client_keygen.argtypes = [ctypes.POINTER(VspParams), u64, ctypes.c_int] + [vp] * 8
         L.vsp_client_keygen_dev.argtypes = [ctypes.POINTER(VspParams), u64, ctypes.c_int,
@@ -568,6 +569,10 @@ class Engine:
         o = np.zeros(3, np.int32)
         _check(lib().vsp_br_plan(self.h, tasks, _ptr(o)))
         return {"lat": bool(o[0]), "full": int(o[1]), "w_rem": int(o[2])}
+
+    def set_option(self, name: str, value: int):
+        """Engine tuning option (vsp_set_option): "lat_tasks" (1|2)."""
+        _check(lib().vsp_set_option(self.h, name.encode(), int(value)))
 
     def counters(self) -> dict:
         """OpCounters (counters.hpp:11-28)."""

@@ -463,6 +463,16 @@ __global__ void __launch_bounds__(kLatThreads, 1)
         const int o = r & 1, h = r >> 1;
         const int L = 16 * h + (lane & 15), e = lane >> 4;
 
+        // this lane's per-lane twiddles in registers for the whole rotation (the kernel has
+        // the registers to spare; the loads were ~11% of its shared-memory wavefronts):
+        // tangent forms for the forward transform, plain ones at the virtual lane L of the
+        // pair inverse
+        double2 twf[kTw2Plain], twi[kTw2Plain];
+#pragma unroll
+        for (int q = 0; q < kTw2Plain; q++) {
+            twf[q] = sm.tw2[(kTw2Plain + q) * 32 + lane];
+            twi[q] = sm.tw2[q * 32 + L];
+        }
         // a_i is fetched one step ahead (lwe[i + 1] <= lwe[n] is in bounds) so the global
         // load latency hides behind the current external product
         uint32_t a_next = lwe[0];
@@ -487,7 +497,7 @@ __global__ void __launch_bounds__(kLatThreads, 1)
                 }
             }
             mark(0);
-            fft512_fwd(z, sm.xbuf(r), sm.tw2, lane);
+            fft512_fwd_regs(z, sm.xbuf(r), twf, lane);
             mark(1);
             // publish the transformed row: z_r -> bufA[r] (warp r's own transpose buffer,
             // free again after the transform's last __syncwarp)
@@ -524,7 +534,7 @@ __global__ void __launch_bounds__(kLatThreads, 1)
             if (lane == 0)
                 mbar_arrive(&sm.empty[s]);  // this warp is done with slot s
             mark(5);
-            fft512_inv_pair(u, sm.bufB[o], sm.tw2, lane, h, 3 + o);
+            fft512_inv_pair_regs(u, sm.bufB[o], twi, lane, h, 3 + o);
             mark(6);
             // (every warp read acc for its digits before barrier 1)
             uint32_t* dst = sm.acc + o * 1024;
@@ -549,6 +559,168 @@ __global__ void __launch_bounds__(kLatThreads, 1)
     const uint4* s4 = reinterpret_cast<const uint4*>(sm.acc);
     for (int q = threadIdx.x; q < 512; q += blockDim.x)
         dst[q] = s4[q];
+}
+
+// ---------------------------------------------------------------------------
+// br_lat2_kernel: br_lat_kernel's four-warp task, TASKS tasks per CTA (one SM), all on the
+// same key stream.  br_lat's step is bound by the shared-memory crossbar at ~58% of it
+// with one warp per scheduler; two tasks per SM run two warps per scheduler and leave half
+// of the SMs of a narrow level free (the netlist runner puts the RAM write bars there).
+// The key arrives in 16 KiB chunks (one gadget row, both outputs) through an S-slot ring:
+// chunk c = 4 i + q of step i lives in slot c % S; every MAC warp of the CTA releases the
+// four slots of its step on `empty` (count 4 TASKS) and the producer warp refills them.
+constexpr int kLat2Threads(int tasks) { return 128 * tasks + 32; }
+
+template <int TASKS, int S>
+struct BrLat2Smem {
+    double2 ring[S][1024];
+    double2 tw2[kTw2Entries * 32];
+    double2 bufA[TASKS][4][kLatBuf];
+    double2 bufB[TASKS][2][kLatBuf];
+    uint32_t acc[TASKS][2048];
+    uint64_t full[S];
+    uint64_t empty[S];
+};
+
+template <int BG, int TASKS, int S>
+__global__ void __launch_bounds__(128 * TASKS + 32, 1)
+    br_lat2_kernel(const uint32_t* __restrict__ tasks, const double2* __restrict__ bkfd,
+                   const double2* __restrict__ tw2g, uint32_t* __restrict__ out, int T, int n)
+{
+    static_assert(S >= 4, "one whole step of key rows must fit the ring");
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    auto& sm = *reinterpret_cast<BrLat2Smem<TASKS, S>*>(smem_raw);
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tl = w >> 2;  // task slot of this warp (producer: tl == TASKS)
+    const int r = w & 3;
+    int task = blockIdx.x * TASKS + (tl < TASKS ? tl : 0);
+    const bool active = task < T;
+    if (!active)
+        task = T - 1;  // shadow a real task: the ring protocol needs every warp
+    const uint32_t* lwe = tasks + (size_t)task * (n + 1);
+    const int nchunks = 4 * n;
+
+    for (int i = threadIdx.x; i < kTw2Entries * 32; i += blockDim.x)
+        sm.tw2[i] = tw2g[i];
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < S; q++) {
+            mbar_init(&sm.full[q], 1);
+            mbar_init(&sm.empty[q], 4 * TASKS);
+        }
+    }
+    if (tl < TASKS) {
+        const uint32_t rot = (2048u - mod_switch_2n(lwe[n], 11)) & 2047u;
+        uint32_t* a = sm.acc[tl];
+        for (int q = threadIdx.x & 127; q < 1024; q += 128) {
+            a[q] = 0;
+            uint32_t val;
+            if (rot < 1024)
+                val = ((uint32_t)q < rot) ? (0u - kMu32) : kMu32;
+            else
+                val = ((uint32_t)q < rot - 1024) ? kMu32 : (0u - kMu32);
+            a[1024 + q] = val;
+        }
+    }
+    __syncthreads();
+
+    if (tl == TASKS) {
+        // producer warp (see br_lat_kernel: no transform warp issues bulk copies)
+        if (lane == 0) {
+            for (int c = 0; c < nchunks; c++) {
+                const int q = c % S;
+                if (c >= S)
+                    mbar_wait(&sm.empty[q], (uint32_t)(((c / S) - 1) & 1));
+                mbar_arrive_expect_tx(&sm.full[q], 16384);
+                bulk_g2s(sm.ring[q], bkfd + (size_t)c * 1024, 16384, &sm.full[q]);
+            }
+        }
+    }
+    else {
+        constexpr uint32_t kHalf = 1u << (BG - 1);
+        constexpr uint32_t kMask = (1u << BG) - 1;
+        constexpr uint32_t kOffset = (kHalf << (32 - BG)) + (kHalf << (32 - 2 * BG));
+        const int P = r >> 1, lvl = r & 1;
+        uint32_t* accT = sm.acc[tl];
+        const uint32_t* src = accT + P * 1024;
+        const uint32_t sh = (uint32_t)(32 - (lvl + 1) * BG);
+        const int o = r & 1, h = r >> 1;
+        const int L = 16 * h + (lane & 15), e = lane >> 4;
+        const int barA = 1 + 4 * tl, barB = 2 + 4 * tl, barPair = 3 + 4 * tl + o;
+        double2 (&bufA)[4][kLatBuf] = sm.bufA[tl];
+
+        uint32_t a_next = lwe[0];
+#pragma unroll 1
+        for (int i = 0; i < n; i++) {
+            const uint32_t bara = mod_switch_2n(a_next, 11);
+            a_next = lwe[i + 1];
+            double2 z[16];
+            {
+                const uint32_t lo = (uint32_t)lane + (uint32_t)opaque_zero();
+                const uint32_t lk = lo - bara;
+                const uint32_t* srcl = src + lo;
+#pragma unroll
+                for (int j = 0; j < 16; j++) {
+                    const uint32_t v0 = rot_coef1024(src, lk + 32 * j) - srcl[32 * j] + kOffset;
+                    const uint32_t v1 = rot_coef1024(src, lk + 32 * j + 512) - srcl[32 * j + 512] + kOffset;
+                    z[j].x = ob_to_double<31>(((v0 >> sh) & kMask) + (0x80000000u - kHalf));
+                    z[j].y = ob_to_double<31>(((v1 >> sh) & kMask) + (0x80000000u - kHalf));
+                }
+            }
+            fft512_fwd(z, bufA[r], sm.tw2, lane);
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < 16; j++)
+                bufA[r][j * 32 + lane] = z[j];
+            bar_group(barA, 128);  // this task's four rows transformed
+            const int c0 = 4 * i;
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+                mbar_wait(&sm.full[(c0 + q) % S], (uint32_t)(((c0 + q) / S) & 1));
+            const double2* b0p = sm.ring[(c0 + 0) % S] + o * 512;
+            const double2* b1p = sm.ring[(c0 + 1) % S] + o * 512;
+            const double2* b2p = sm.ring[(c0 + 2) % S] + o * 512;
+            const double2* b3p = sm.ring[(c0 + 3) % S] + o * 512;
+            double2 u[8];
+#pragma unroll
+            for (int t = 0; t < 8; t++) {
+                const int q = (2 * t + e) * 32 + L;
+                const double2 z0 = bufA[0][q], z1 = bufA[1][q];
+                const double2 z2 = bufA[2][q], z3 = bufA[3][q];
+                const double2 b0 = b0p[q], b1 = b1p[q], b2 = b2p[q], b3 = b3p[q];
+                double ax = fma(z0.x, b0.x, -z0.y * b0.y);
+                double ay = fma(z0.x, b0.y, z0.y * b0.x);
+                ax = fma(z1.x, b1.x, fma(-z1.y, b1.y, ax));
+                ay = fma(z1.x, b1.y, fma(z1.y, b1.x, ay));
+                ax = fma(z2.x, b2.x, fma(-z2.y, b2.y, ax));
+                ay = fma(z2.x, b2.y, fma(z2.y, b2.x, ay));
+                ax = fma(z3.x, b3.x, fma(-z3.y, b3.y, ax));
+                ay = fma(z3.x, b3.y, fma(z3.y, b3.x, ay));
+                u[t] = make_double2(ax, ay);
+            }
+            __syncwarp();
+            if (lane == 0) {
+#pragma unroll
+                for (int q = 0; q < 4; q++)
+                    mbar_arrive(&sm.empty[(c0 + q) % S]);
+            }
+            fft512_inv_pair(u, sm.bufB[tl][o], sm.tw2, lane, h, barPair);
+            uint32_t* dst = accT + o * 1024;
+#pragma unroll
+            for (int t = 0; t < 8; t++) {
+                const int p = L + 32 * (t + 8 * e);
+                dst[p] += (uint32_t)__double2ll_rn(u[t].x);
+                dst[p + 512] += (uint32_t)__double2ll_rn(u[t].y);
+            }
+            bar_group(barB, 128);  // acc updated before the next step's digits
+        }
+    }
+    __syncthreads();
+    if (tl < TASKS && active) {
+        uint4* dst = reinterpret_cast<uint4*>(out + (size_t)task * 2048);
+        const uint4* s4 = reinterpret_cast<const uint4*>(sm.acc[tl]);
+        for (int q = threadIdx.x & 127; q < 512; q += 128)
+            dst[q] = s4[q];
+    }
 }
 
 // ---------------------------------------------------------------------------

@@ -277,13 +277,13 @@ __device__ __forceinline__ void xpose_inv(double2 (&v)[16], void* buf, int lane)
 }
 
 // Forward transform in place.  xbuf: per-warp smem, kFftXbufStride double2 (HALF:
-// kFftXbufStride doubles).  tw2: smem table [kTw2Entries][32] double2 (plain, then tangent).
-template <int ROOT = 0, bool HALF = false>
-__device__ __forceinline__ void fft512_fwd(double2 (&v)[16], void* xbuf,
-                                           const double2* tw2, int lane)
+// kFftXbufStride doubles).  twt(e): this lane's tangent-form per-lane twiddle of entry
+// e < kTw2Plain (a shared-memory load, or a register when the kernel has room to keep
+// all twelve: fft512_fwd_regs).
+template <int ROOT, bool HALF, class TWT>
+__device__ __forceinline__ void fft512_fwd_g(double2 (&v)[16], void* xbuf, const TWT& twt, int lane)
 {
     const double2* tw1t = &c_tw1t[ROOT][0] + opaque_zero();
-    const double2* tw2t = tw2 + kTw2Plain * 32;
 #pragma unroll
     for (int d = 0; d < 4; d++) {
         const int h = 8 >> d;
@@ -306,7 +306,7 @@ __device__ __forceinline__ void fft512_fwd(double2 (&v)[16], void* xbuf,
         for (int j = 0; j < 16; j++)
             if ((j & h) == 0) {
                 const int k = tw_k(d, j >> (8 - d));
-                const double2 w = tw2t[tw_entry(d, k & 3) * 32 + lane];
+                const double2 w = twt(tw_entry(d, k & 3));
                 if (k >> 2)
                     bf_fwd_tq<1>(v[j], v[j + h], w);
                 else
@@ -321,7 +321,7 @@ __device__ __forceinline__ void fft512_fwd(double2 (&v)[16], void* xbuf,
         double2 u = odd ? recv : v[k];
         double2 w = odd ? v[k + 8] : recv;
         const int br = bitrev_const(k, 3);
-        const double2 t = tw2t[tw_entry(8, br & 3) * 32 + lane];
+        const double2 t = twt(tw_entry(8, br & 3));
         if (br >> 2)
             bf_fwd_tq<1>(u, w, t);
         else
@@ -329,6 +329,23 @@ __device__ __forceinline__ void fft512_fwd(double2 (&v)[16], void* xbuf,
         v[k] = u;
         v[k + 8] = w;
     }
+}
+
+// tw2: smem table [kTw2Entries][32] double2 (plain, then tangent).
+template <int ROOT = 0, bool HALF = false>
+__device__ __forceinline__ void fft512_fwd(double2 (&v)[16], void* xbuf,
+                                           const double2* tw2, int lane)
+{
+    const double2* tw2t = tw2 + kTw2Plain * 32;
+    fft512_fwd_g<ROOT, HALF>(v, xbuf, [&](int e) { return tw2t[e * 32 + lane]; }, lane);
+}
+
+// Same with the twelve tangent twiddles of this lane held in registers (twr[e]).
+template <int ROOT = 0>
+__device__ __forceinline__ void fft512_fwd_regs(double2 (&v)[16], void* xbuf,
+                                                const double2 (&twr)[kTw2Plain], int lane)
+{
+    fft512_fwd_g<ROOT, false>(v, xbuf, [&](int e) { return twr[e]; }, lane);
 }
 
 // Exact inverse of fft512_fwd up to the factor 512 (folded into the key).
@@ -454,9 +471,9 @@ __device__ __forceinline__ double2 cmul(const double2 a, const double2 b)
     return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
 }
 
-template <int ROOT = 0>
-__device__ __forceinline__ void fft512_inv_pair(double2 (&u)[8], double2* xbuf,
-                                                const double2* tw2, int lane, int h, int bar_id)
+template <int ROOT, class TWP>
+__device__ __forceinline__ void fft512_inv_pair_g(double2 (&u)[8], double2* xbuf, const TWP& twp,
+                                                  int lane, int h, int bar_id)
 {
     const int L = 16 * h + (lane & 15);
     const int e = lane >> 4;
@@ -465,7 +482,7 @@ __device__ __forceinline__ void fft512_inv_pair(double2 (&u)[8], double2* xbuf,
     // stage 8: butterflies (k, k + 8), k = 2 tp + e; bitrev3(k) = (e << 2) | bitrev2(tp)
 #pragma unroll
     for (int tp = 0; tp < 4; tp++) {
-        double2 w = tw2[tw_entry(8, bitrev_const(tp, 2)) * 32 + L];
+        double2 w = twp(tw_entry(8, bitrev_const(tp, 2)));
         if (e)
             w = make_double2(-w.y, w.x);  // i^Q with Q = e
         double2 a = u[tp], b = u[tp + 4];
@@ -478,7 +495,7 @@ __device__ __forceinline__ void fft512_inv_pair(double2 (&u)[8], double2* xbuf,
 #pragma unroll
     for (int t = 0; t < 8; t++) {
         const int k = tw_k(7, t);
-        double2 w = tw2[tw_entry(7, k & 3) * 32 + L];
+        double2 w = twp(tw_entry(7, k & 3));
         if (k >> 2)
             w = make_double2(-w.y, w.x);
         const double2 c = e ? make_double2(w.x, -w.y) : make_double2(1.0, 0.0);
@@ -494,7 +511,7 @@ __device__ __forceinline__ void fft512_inv_pair(double2 (&u)[8], double2* xbuf,
         for (int t = 0; t < 8; t++)
             if ((t & hh) == 0) {
                 const int k = tw_k(d, t >> (7 - d));
-                const double2 w = tw2[tw_entry(d, k & 3) * 32 + L];
+                const double2 w = twp(tw_entry(d, k & 3));
                 if (k >> 2)
                     bf_inv_q<1>(u[t], u[t + hh], w);
                 else
@@ -534,6 +551,23 @@ __device__ __forceinline__ void fft512_inv_pair(double2 (&u)[8], double2* xbuf,
             u[t] = cmul(d, c);
         }
     }
+}
+
+// twp(e): plain per-lane twiddle of entry e at virtual lane L = 16 h + (lane & 15).
+template <int ROOT = 0>
+__device__ __forceinline__ void fft512_inv_pair(double2 (&u)[8], double2* xbuf,
+                                                const double2* tw2, int lane, int h, int bar_id)
+{
+    const int L = 16 * h + (lane & 15);
+    fft512_inv_pair_g<ROOT>(u, xbuf, [&](int e) { return tw2[e * 32 + L]; }, lane, h, bar_id);
+}
+
+template <int ROOT = 0>
+__device__ __forceinline__ void fft512_inv_pair_regs(double2 (&u)[8], double2* xbuf,
+                                                     const double2 (&twr)[kTw2Plain], int lane,
+                                                     int h, int bar_id)
+{
+    fft512_inv_pair_g<ROOT>(u, xbuf, [&](int e) { return twr[e]; }, lane, h, bar_id);
 }
 
 // Forward transform of one block split over a warp pair (the mirror of fft512_inv_pair).

@@ -70,6 +70,8 @@ struct vsp_netlist {
     std::vector<int> dff_q, dff_d;   // per DFF: output net (Q), input net (D)
     bool table_valid = false;
     uint64_t cycle = 0;
+    // the largest narrow level's CTAs with two tasks per SM (ram_overlap partition)
+    int max_level_ctas = 0;
     // memory ports
     DevBuf ram, rom;
     uint32_t ram_v = 0, ram_w = 0, rom_depth = 0, rom_nluts = 0;
@@ -244,6 +246,15 @@ void build_dag(vsp_netlist* nl)
         else
             nl->const_cells.push_back(c);
     }
+    const int sms = nl->ctx->sms;
+    nl->max_level_ctas = 0;
+    for (const auto& lg : nl->level_gates) {
+        int tasks = 0;
+        for (int cell : lg)
+            tasks += nl->kind[cell] == cMux ? 2 : nl->kind[cell] == cNot ? 0 : 1;
+        const int ctas = tasks <= 2 * sms ? (tasks > 64 ? (tasks + 1) / 2 : tasks) : sms;
+        nl->max_level_ctas = std::max(nl->max_level_ctas, ctas);
+    }
 }
 
 // tlweTrivial (ops.cpp:212-217): a = 0, b = +-mu
@@ -299,7 +310,44 @@ void run_mem_pair(vsp_netlist* nl, const std::vector<int>& cells, uint32_t* vals
     VSP_CUDA_CHECK(cudaGetLastError());
 }
 
+// ram_overlap: SMs left to the deferred write bars beside the widest narrow level (two
+// tasks per SM) and a margin for the levels' key-switch / gather kernels; 0 = no overlap.
+int write_ctas(const vsp_netlist* nl)
+{
+    const vsp_ctx* c = nl->ctx;
+    if (!c->ram_overlap || nl->ram_cell < 0 || !c->p.fft || sharded(c))
+        return 0;
+    const int k = c->sms - nl->max_level_ctas - 2;
+    return k >= 16 ? k : 0;
+}
+
+void run_cycle_body(vsp_netlist* nl, cudaStream_t st);
+
 void run_cycle(vsp_netlist* nl, cudaStream_t st)
+{
+    vsp_ctx* c = nl->ctx;
+    const int k = write_ctas(nl);
+    if (!k) {
+        run_cycle_body(nl, st);
+        return;
+    }
+    struct Restore {  // options hold for this cycle only, also on an exception
+        vsp_ctx* c;
+        int lat;
+        ~Restore()
+        {
+            c->lat_tasks = lat;
+            c->defer_write_now = false;
+            c->w_ctas = 0;
+        }
+    } restore{c, c->lat_tasks};
+    c->lat_tasks = 2;
+    c->w_ctas = k;
+    c->defer_write_now = true;
+    run_cycle_body(nl, st);
+}
+
+void run_cycle_body(vsp_netlist* nl, cudaStream_t st)
 {
     vsp_ctx* c = nl->ctx;
     const uint32_t n = c->p.n;

@@ -265,6 +265,39 @@ struct vsp_ctx {
             VSP_CUDA_CHECK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     }
 
+    // narrow-level tasks per SM (1 or 2, see br_lat2_kernel); VSP_LAT_TASKS overrides
+    int lat_tasks = 1;
+
+    // RAM write bars off the cycle's critical path (option "ram_overlap", netlist runner):
+    // the write unit's key switch + noise-refresh blind rotations run on a low-priority
+    // stream, capped at w_ctas SMs per launch, beside the later narrow levels (which then
+    // run two tasks per SM); joined before the next access to the RAM image.
+    bool ram_overlap = false;
+    bool defer_write_now = false;  // set by the runner around a cycle
+    int w_ctas = 0;
+    cudaStream_t wstream = nullptr;
+    cudaEvent_t ev_wfork = nullptr, ev_wdone = nullptr;
+    bool w_pending = false;
+    DevBuf wlw, wgt, wgl;
+    void ensure_wstream()
+    {
+        if (wstream)
+            return;
+        int least = 0, greatest = 0;
+        VSP_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        VSP_CUDA_CHECK(cudaStreamCreateWithPriority(&wstream, cudaStreamNonBlocking, least));
+        VSP_CUDA_CHECK(cudaEventCreateWithFlags(&ev_wfork, cudaEventDisableTiming));
+        VSP_CUDA_CHECK(cudaEventCreateWithFlags(&ev_wdone, cudaEventDisableTiming));
+    }
+    // order `st` after a deferred write unit (the RAM image it updates)
+    void ram_join(cudaStream_t st)
+    {
+        if (!w_pending)
+            return;
+        VSP_CUDA_CHECK(cudaStreamWaitEvent(st, ev_wdone, 0));
+        w_pending = false;
+    }
+
     // The context's scratch buffers are shared by all calls: a call on a different stream
     // than the previous one first waits for the previous call's work (ev_last).
     cudaEvent_t ev_last = nullptr;
@@ -320,6 +353,12 @@ struct CallScope {
     }
 };
 
+int lat_tasks(const vsp_ctx* c)
+{
+    static const int forced = getenv("VSP_LAT_TASKS") ? atoi(getenv("VSP_LAT_TASKS")) : 0;
+    return forced ? forced : c->lat_tasks;
+}
+
 template <class F>
 void timed(vsp_ctx* c, const char* name, cudaStream_t st, F&& launch)
 {
@@ -352,6 +391,10 @@ void validate(const Params& p)  // ParameterSet::validate (params.cpp:17-29)
 // Kernel configuration of the level-1 FFT blind rotation.
 constexpr int kBrSlots = 2;
 constexpr int kBrBg = 10;  // the FFT path is specialised for Bg1 = 2^10 (tfhe-80)
+
+// Narrow levels: tasks per SM of the latency kernel (1: br_lat_kernel, 2: br_lat2_kernel,
+// which leaves half of the SMs free for the RAM write bars; vsp_ctx::lat_tasks).
+constexpr int kLat2Slots = 6;
 
 // Warps (= tasks) per CTA of the blind-rotation kernel.  Every task costs the same, so
 // time ~ waves(W) x t(W), t(W) = duration of one wave with W tasks per SM, measured on
@@ -573,8 +616,13 @@ void launch_br(vsp_ctx* c, const uint32_t* d_tasks, uint32_t* d_trlwe, int T, cu
                 }
             }
             timed(c, "br_lat", st, [&] {
-                br_lat_kernel<kBrBg><<<T, kLatThreads, sizeof(BrLatSmem), st>>>(d_tasks, c->d_bk1fd,
-                                                                      c->d_tw2, d_trlwe, (int)p.n);
+                if (lat_tasks(c) == 2 && T > 64)
+                    br_lat2_kernel<kBrBg, 2, kLat2Slots>
+                        <<<(T + 1) / 2, kLat2Threads(2), sizeof(BrLat2Smem<2, kLat2Slots>), st>>>(
+                            d_tasks, c->d_bk1fd, c->d_tw2, d_trlwe, T, (int)p.n);
+                else
+                    br_lat_kernel<kBrBg><<<T, kLatThreads, sizeof(BrLatSmem), st>>>(
+                        d_tasks, c->d_bk1fd, c->d_tw2, d_trlwe, (int)p.n);
             });
             VSP_CUDA_CHECK(cudaGetLastError());
             c->launches++;
@@ -726,6 +774,9 @@ void configure_kernels()
     VSP_CUDA_CHECK(cudaFuncSetAttribute(br_lat_kernel<kBrBg, true>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)sizeof(BrLatSmem)));
+    VSP_CUDA_CHECK(cudaFuncSetAttribute(br_lat2_kernel<kBrBg, 2, kLat2Slots>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)sizeof(BrLat2Smem<2, kLat2Slots>)));
     set_br_attr<8>();
     set_br_attr<7>();
     set_br_attr<6>();
@@ -1170,12 +1221,50 @@ void ram_write_unit_dev(vsp_ctx* c, uint32_t* d_ram, int v, int w, const uint32_
         tasks.push_back(t);
     }
     run_chains(c, tasks, st);
+    const int T = (int)cells;
+    if (c->defer_write_now && p.fft && c->w_ctas > 0) {
+        // noise refresh on the low-priority write stream, private scratch: key switch of all
+        // cells, then blind-rotation launches of at most w_ctas CTAs (8 cells each), so the
+        // later narrow levels keep their SMs; joined before the next access of this RAM
+        c->ensure_wstream();
+        cudaStream_t ws = c->wstream;
+        VSP_CUDA_CHECK(cudaEventRecord(c->ev_wfork, st));
+        VSP_CUDA_CHECK(cudaStreamWaitEvent(ws, c->ev_wfork, 0));
+        uint32_t* wl = c->wlw.as<uint32_t>(cells * n1);
+        std::vector<int2> gt(T);
+        std::vector<int> gl(T);
+        for (int i = 0; i < T; i++) {
+            gt[i] = make_int2(i, -1);
+            gl[i] = i;
+        }
+        int2* d_gt = c->wgt.as<int2>(T);
+        int* d_gl = c->wgl.as<int>(T);
+        VSP_CUDA_CHECK(cudaMemcpyAsync(d_gt, gt.data(), T * sizeof(int2), cudaMemcpyHostToDevice, ws));
+        VSP_CUDA_CHECK(cudaMemcpyAsync(d_gl, gl.data(), T * sizeof(int), cudaMemcpyHostToDevice, ws));
+        launch_iks(c, chain_out, d_gt, d_gl, T, wl, ws);
+        const int per_launch = 8 * c->w_ctas;
+        const int launches = (T + per_launch - 1) / per_launch;
+        const int per = ((T + launches - 1) / launches + 7) / 8 * 8;  // balanced, whole CTAs
+        timed(c, "br1024", ws, [&] {
+            for (int lo = 0; lo < T; lo += per) {
+                const int cnt = std::min(per, T - lo);
+                br1024_kernel<8, kBrSlots, kBrBg><<<(cnt + 7) / 8, 256, sizeof(Br1024Smem<8, kBrSlots>),
+                                                    ws>>>(wl + (size_t)lo * n1, c->d_bk1fd, c->d_tw2,
+                                                          d_ram + (size_t)lo * cw, cnt, (int)p.n);
+                VSP_CUDA_CHECK(cudaGetLastError());
+                c->launches++;
+            }
+        });
+        c->counters[1] += (uint64_t)T;
+        VSP_CUDA_CHECK(cudaEventRecord(c->ev_wdone, ws));
+        c->w_pending = true;
+        return;
+    }
     uint32_t* lw = c->tasks.as<uint32_t>(cells * n1);
     // noise refresh: cell = BR(IKS(SE(t, 0))).  Arranged so the key switch of the
     // whole-wave cells runs UNDER the remainder wave (which holds half of each SM): key
     // switch the remainder cells, then their blind rotations (high-priority stream) beside
     // the whole-wave cells' key switch (low-priority stream), then the whole waves.
-    const int T = (int)cells;
     const int full = p.fft ? br_plan(T, c->sms).full : 0;
     const int rem = T - full;
     if (full && rem) {
@@ -1224,6 +1313,7 @@ void ram_cycle_dev(vsp_ctx* c, uint32_t* d_ram, int v, int w, const uint32_t* d_
 {
     require_cb(c);
     check_ram_geometry(v, w);
+    c->ram_join(st);  // a deferred write unit of the previous access updates this image
     const uint32_t* raw = pre_raw;
     if (!raw) {
         uint32_t* r = c->cbraw.as<uint32_t>(v * trgsw_words(c->p));
@@ -1458,7 +1548,12 @@ vsp_ctx* vsp_create(const vsp_params* params, int device)
         c->device = device;
         c->set_device();
         VSP_CUDA_CHECK(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device));
-        VSP_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        {
+            // the context stream outranks the deferred write-bar stream (ram_overlap)
+            int least = 0, greatest = 0;
+            VSP_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+            VSP_CUDA_CHECK(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, greatest));
+        }
         // twiddles of the 512-point negacyclic transform
         double2 tw1[3][15], tw1t[3][15], tw1a[3][15];
         std::vector<double2> tw2all;
@@ -1521,6 +1616,14 @@ void vsp_destroy(vsp_ctx* c)
     }
     if (c->ev_last)
         cudaEventDestroy(c->ev_last);
+    if (c->wstream) {
+        cudaStreamSynchronize(c->wstream);
+        cudaStreamDestroy(c->wstream);
+        cudaEventDestroy(c->ev_wfork);
+        cudaEventDestroy(c->ev_wdone);
+    }
+    for (DevBuf* b : {&c->wlw, &c->wgt, &c->wgl})
+        b->release();
     for (auto& kv : c->timers)  // profiling events never read back
         for (auto& e : kv.second.pending) {
             cudaEventDestroy(e.first);
@@ -2238,6 +2341,7 @@ int vsp_netlist_ram(vsp_netlist* nl, uint32_t v, uint32_t w, uint32_t* get, cons
         CallScope cs(c, c->stream);
         if (nl->ram_cell < 0)
             throw std::runtime_error("netlist has no RAM port");
+        c->ram_join(c->stream);  // a deferred write unit may still update the image
         VSP_CUDA_CHECK(cudaStreamSynchronize(c->stream));  // in-flight cycles use the image
         const size_t words = ((size_t)w << v) * 2 * c->p.N1;
         if (set) {
@@ -2270,6 +2374,8 @@ int vsp_netlist_run(vsp_netlist* nl, uint64_t cycles, double* stats)
         for (uint64_t i = 0; i < cycles; i++) {
             VSP_CUDA_CHECK(cudaEventRecord(a, c->stream));
             run_cycle(nl, c->stream);
+            if (i + 1 == cycles)  // a deferred write unit finishes inside the last cycle
+                c->ram_join(c->stream);
             VSP_CUDA_CHECK(cudaEventRecord(b, c->stream));
             VSP_CUDA_CHECK(cudaEventSynchronize(b));
             float ms = 0;
@@ -2339,6 +2445,7 @@ int vsp_netlist_snapshot_save(vsp_netlist* nl, const char* param_name, uint8_t* 
     return guard([&] {
         vsp_ctx* c = nl->ctx;
         CallScope cs(c, c->stream);
+        c->ram_join(c->stream);
         if (nl->has_ram)
             ram_gather_dev(c, nl->ram.as<uint32_t>(0), (int)nl->ram_v, (int)nl->ram_w, c->stream);
         VSP_CUDA_CHECK(cudaStreamSynchronize(c->stream));
@@ -2358,6 +2465,7 @@ int vsp_netlist_snapshot_load(vsp_netlist* nl, const char* param_name, const uin
     return guard([&] {
         vsp_ctx* c = nl->ctx;
         CallScope cs(c, c->stream);
+        c->ram_join(c->stream);
         VSP_CUDA_CHECK(cudaStreamSynchronize(c->stream));
         snapshot_load(nl, param_name ? param_name : "", in, len);
     });
@@ -2549,6 +2657,25 @@ int vsp_profile_reset(vsp_ctx* c)
 }
 
 int vsp_sm_count(vsp_ctx* c) { return c->sms; }
+
+int vsp_set_option(vsp_ctx* c, const char* name, int64_t value)
+{
+    return guard([&] {
+        CallScope cs(c, c->stream);
+        const std::string k = name ? name : "";
+        if (k == "lat_tasks") {
+            if (value != 1 && value != 2)
+                throw std::invalid_argument("lat_tasks must be 1 or 2");
+            c->lat_tasks = (int)value;
+        }
+        else if (k == "ram_overlap") {
+            c->ram_overlap = value != 0;
+        }
+        else {
+            throw std::invalid_argument("unknown option: " + k);
+        }
+    });
+}
 
 int vsp_client_keygen_dev(const vsp_params* pp, uint64_t seed, int with_cb, int device,
                           uint32_t* lv0, uint32_t* lv1, uint32_t* lv2, uint32_t* bk1,

@@ -299,3 +299,29 @@ def test_back_to_back_calls_on_different_streams(prod):
     torch.cuda.synchronize()
     for d_out, want in zip(outs, wants):
         assert np.array_equal(vsp.decrypt(k["lv0"], d_out.cpu().numpy().view(np.uint32)), want)
+
+
+@pytest.mark.parametrize("G", [1, 2, 77, 141, 148])
+def test_two_tasks_per_sm_latency_kernel_equals_one(prod, G):
+    """br_lat2_kernel (two narrow-level tasks per SM, chunked key ring) gives the same
+    words as br_lat_kernel on ragged narrow levels (odd task counts shadow the last task),
+    all gate kinds; sampled against the oracle."""
+    e, o = prod
+    rng = np.random.default_rng(500 + G)
+    kid = rng.integers(0, len(GATE_KINDS), G).astype(np.int32)
+    k = oracle_keys("tfhe-80", 20200729, False)
+    p = vsp.ParameterSet("tfhe-80")
+    bits = rng.integers(0, 2, size=(G, 3)).astype(np.uint8)
+    ins = vsp.encrypt(p, k["lv0"], bits.reshape(-1), 600 + G).reshape(G, 3, p.n + 1)
+    tasks = int(sum(2 if x == 2 else 0 if x == 5 else 1 for x in kid))
+    if e.sms == 148 and tasks:
+        assert e.br_plan(tasks)["lat"]
+    one = e.hom_gate_batch(kid, ins)
+    e.set_option("lat_tasks", 2)
+    try:
+        two = e.hom_gate_batch(kid, ins)
+    finally:
+        e.set_option("lat_tasks", 1)
+    assert np.array_equal(one, two)
+    idx = np.arange(0, G, max(1, G // 5))
+    assert np.array_equal(two[idx], o.hom_gate_batch(kid[idx], ins[idx], threads=8))

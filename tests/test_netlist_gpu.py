@@ -174,3 +174,41 @@ def test_flat_netlist_validated_by_c_abi(bad, match):
     bad(nl)
     with pytest.raises(RuntimeError, match=match):
         N.Evaluator(nl, e)
+
+
+def test_runner_ram_overlap_equals_inline():
+    """ram_overlap (write bars deferred to a low-priority stream beside the later levels,
+    narrow levels at two tasks per SM, joined before the next RAM access) gives the same
+    words as the inline schedule: DFF state, outputs and RAM image over 3 cycles, and the
+    RAM getter joins the deferred write."""
+    p = vsp.ParameterSet("tfhe-80")
+    k = vsp.keygen(p, 2207, True, device=0)
+    nl = N.synthetic_netlist(seed=9, scale=0.05, levels=6, dffs=48, ram=(4, 8))
+    rng = np.random.default_rng(9)
+    v, w = 4, 8
+    ram = vsp.encrypt_ram(p, k, rng.integers(0, 256, (w << v) // 8).astype(np.uint8), v, w, 1)
+    luts = vsp.encrypt_rom(p, k, rng.integers(0, 256, 512).astype(np.uint8), 2)
+    dff0 = vsp.encrypt(p, k["lv0"], rng.integers(0, 2, 48).astype(np.uint8), 3)
+    ins = vsp.encrypt(p, k["lv0"], rng.integers(0, 2, len(nl.inputs[0].bits)).astype(np.uint8), 4)
+    res = []
+    for overlap in (0, 1):
+        e = vsp.Engine(p)
+        e.upload_keys(k)
+        e.set_option("ram_overlap", overlap)
+        ev = N.Evaluator(nl, e)
+        ev.set_ram(ram, v, w)
+        ev.set_rom(luts, 512)
+        ev.set_dff_state_raw(dff0)
+        for i, ct in enumerate(ins):
+            ev.set_input("in", i, ct)
+        trace = []
+        for _ in range(3):
+            ev.run(1)
+            trace.append((ev.dff_state(), np.stack([ev.output("out", j) for j in range(16)])))
+        res.append((trace, ev.ram()))
+        ev.close()
+        e.close()
+    (t0, r0), (t1, r1) = res
+    for (d0, o0), (d1, o1) in zip(t0, t1):
+        assert np.array_equal(d0, d1) and np.array_equal(o0, o1)
+    assert np.array_equal(r0, r1)
