@@ -1574,6 +1574,8 @@ vsp_ctx* vsp_create(const vsp_params* params, int device)
         VSP_CUDA_CHECK(cudaMalloc(&c->d_tv1, tv.size() * 4));
         VSP_CUDA_CHECK(cudaMemcpy(c->d_tv1, tv.data(), tv.size() * 4, cudaMemcpyHostToDevice));
         configure_kernels();
+        if (const char* e = getenv("VSP_RAM_OVERLAP"))  // A/B knob for the option
+            c->ram_overlap = atoi(e) != 0;
         out = c.release();
     });
     return out;
