@@ -622,6 +622,7 @@ def measure_cycle(cx: Ctx, steps: int) -> dict | None:
     eng.profile_enable(False)
     kernels = {k: round(eng.profile_read(k)[0] / steps, 3) for k in KERNEL_TIMERS}
     secs = cx.max_over_ranks(float(np.mean([s.seconds for s in stats])))
+    cpc = {k: v_ // max(steps, 1) for k, v_ in eng.counters().items()}  # timed cycles only
     # e2e through the Evaluator API: every cycle sets the 8 input TLWEs from host memory
     # and reads the 16 output TLWEs back
     e2e = None
@@ -644,7 +645,6 @@ def measure_cycle(cx: Ctx, steps: int) -> dict | None:
         eng.close()
         return None
     st = N.netlist_stats(nl)
-    cpc = {k: v_ // max(steps, 1) for k, v_ in eng.counters().items()}
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         cpu = cycle_cpu_baseline(p, keys, nl, ram, v, w, luts, dff0, ins, dff1, outs1)
