@@ -53,7 +53,7 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> str:
                   "-c", s, "-o", o])
         objs.append(o)
     if force or _stale(OUT, objs):
-        _run([NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-Xcompiler", "-pthread"])
+        _run([NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-Xcompiler", "-pthread", "-lcublasLt"])
     return OUT
 
 

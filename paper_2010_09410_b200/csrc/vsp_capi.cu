@@ -21,6 +21,7 @@
 
 #include "../../include/vsp_b200.h"
 #include "bootstrap.cuh"
+#include "iks_gemm.cuh"
 #include "cmux.cuh"
 #include "exact.cuh"
 #include "level2.cuh"
@@ -267,6 +268,15 @@ struct vsp_ctx {
 
     // narrow-level tasks per SM (1 or 2, see br_lat2_kernel); VSP_LAT_TASKS overrides
     int lat_tasks = 1;
+
+    // key switching as an INT8 tensor-core GEMM (iks_gemm.cuh): the key in signed-byte
+    // planes, cuBLASLt handle, selector / product scratch; option "iks_gemm"
+    bool iks_gemm = true;
+    int8_t* d_k4t = nullptr;
+    int k4_npad = 0;
+    cublasLtHandle_t lt = nullptr;
+    DevBuf iks_S, iks_C, lt_ws;
+    std::map<int, cublasLtMatmulAlgo_t> lt_algo;  // per padded batch
 
     // RAM write bars off the cycle's critical path (option "ram_overlap", netlist runner):
     // the write unit's key switch + noise-refresh blind rotations run on a low-priority
@@ -689,6 +699,74 @@ int iks_split(int tiles, int N, int sms)
     return s;
 }
 
+void lt_check(cublasStatus_t r, const char* what)
+{
+    if (r != CUBLAS_STATUS_SUCCESS)
+        throw std::runtime_error(std::string("cuBLASLt ") + what + " failed (status " +
+                                 std::to_string((int)r) + ")");
+}
+
+// Batches from this many key switches up take the INT8-GEMM key switch (below it the
+// GEMM's fixed cost -- streaming the 62 MB byte-plane key once -- loses to iks_b2).
+constexpr int kIksGemmMin = 64;
+
+bool iks_gemm_on(const vsp_ctx* c, int Gl)
+{
+    return c->iks_gemm && c->d_k4t && Gl >= kIksGemmMin;
+}
+
+// C (Mpad x npad, int32, row-major) = S (Mpad x K_, int8, row-major) x K4 (K_ x npad):
+// in cuBLASLt's column-major terms C^T = (K4t)^T S^T, a "TN" int8 GEMM with K contiguous
+// in both operands (the tensor-core IMMA layout).
+void iks_gemm_run(vsp_ctx* c, const int8_t* S, int Mpad, int32_t* C, cudaStream_t st)
+{
+    if (!c->lt)
+        lt_check(cublasLtCreate(&c->lt), "create");
+    const int K = kIksGemmK, Np = c->k4_npad;
+    cublasLtMatmulDesc_t desc = nullptr;
+    cublasLtMatrixLayout_t la = nullptr, lb = nullptr, lc = nullptr;
+    cublasLtMatmulPreference_t pref = nullptr;
+    const size_t ws_bytes = 32u << 20;
+    void* ws = c->lt_ws.ensure(ws_bytes);
+    auto cleanup = [&] {
+        if (pref) cublasLtMatmulPreferenceDestroy(pref);
+        if (la) cublasLtMatrixLayoutDestroy(la);
+        if (lb) cublasLtMatrixLayoutDestroy(lb);
+        if (lc) cublasLtMatrixLayoutDestroy(lc);
+        if (desc) cublasLtMatmulDescDestroy(desc);
+    };
+    try {
+        lt_check(cublasLtMatmulDescCreate(&desc, CUBLAS_COMPUTE_32I, CUDA_R_32I), "desc");
+        const cublasOperation_t opT = CUBLAS_OP_T, opN = CUBLAS_OP_N;
+        lt_check(cublasLtMatmulDescSetAttribute(desc, CUBLASLT_MATMUL_DESC_TRANSA, &opT, sizeof opT), "transa");
+        lt_check(cublasLtMatmulDescSetAttribute(desc, CUBLASLT_MATMUL_DESC_TRANSB, &opN, sizeof opN), "transb");
+        lt_check(cublasLtMatrixLayoutCreate(&la, CUDA_R_8I, K, Np, K), "layout A");
+        lt_check(cublasLtMatrixLayoutCreate(&lb, CUDA_R_8I, K, Mpad, K), "layout B");
+        lt_check(cublasLtMatrixLayoutCreate(&lc, CUDA_R_32I, Np, Mpad, Np), "layout C");
+        auto it = c->lt_algo.find(Mpad);
+        if (it == c->lt_algo.end()) {
+            lt_check(cublasLtMatmulPreferenceCreate(&pref), "preference");
+            lt_check(cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES,
+                                                          &ws_bytes, sizeof ws_bytes), "workspace");
+            cublasLtMatmulHeuristicResult_t h{};
+            int found = 0;
+            lt_check(cublasLtMatmulAlgoGetHeuristic(c->lt, desc, la, lb, lc, lc, pref, 1, &h, &found),
+                     "heuristic");
+            if (found < 1)
+                throw std::runtime_error("cuBLASLt: no int8 GEMM algorithm for the key switch");
+            it = c->lt_algo.emplace(Mpad, h.algo).first;
+        }
+        const int32_t one = 1, zero = 0;
+        lt_check(cublasLtMatmul(c->lt, desc, &one, c->d_k4t, la, S, lb, &zero, C, lc, C, lc,
+                                &it->second, ws, ws_bytes, st), "matmul");
+    }
+    catch (...) {
+        cleanup();
+        throw;
+    }
+    cleanup();
+}
+
 // gt8: 8 gates per CTA instead of 16 (fewer registers, so more CTAs fit beside a running
 // blind-rotation wave; the key is streamed twice as often).
 void launch_iks(vsp_ctx* c, const uint32_t* d_trlwe, const int2* d_gtask, const int* d_glist,
@@ -698,6 +776,23 @@ void launch_iks(vsp_ctx* c, const uint32_t* d_trlwe, const int2* d_gtask, const 
     if (Gl == 0)
         return;
     const Params& p = c->p;
+    if (iks_gemm_on(c, Gl)) {
+        const int Mpad = (Gl + 15) / 16 * 16;
+        int8_t* S = c->iks_S.as<int8_t>((size_t)Mpad * kIksGemmK);
+        int32_t* C = c->iks_C.as<int32_t>((size_t)Mpad * c->k4_npad);
+        timed(c, "iks", st, [&] {
+            iks_gemm_selectors_kernel<<<Gl, 256, 0, st>>>(d_trlwe, d_gtask, d_glist, d_seidx, S,
+                                                          (int)p.N1);
+            VSP_CUDA_CHECK(cudaGetLastError());
+            iks_gemm_run(c, S, Mpad, C, st);
+            iks_gemm_epilogue_kernel<<<Gl, 128, 0, st>>>(C, c->k4_npad, d_trlwe, d_gtask, d_glist,
+                                                         d_seidx, d_out, (int)p.n, (int)p.N1);
+            VSP_CUDA_CHECK(cudaGetLastError());
+        });
+        c->launches += 3;
+        c->counters[2] += (uint64_t)Gl;
+        return;
+    }
     const int kpt = (int)((p.n + 1 + 255) / 256);
     timed(c, "iks", st, [&] {
         iks_init_kernel<<<Gl, 128, 0, st>>>(d_trlwe, d_gtask, d_glist, d_seidx, Gl, d_out, p.n,
@@ -959,7 +1054,11 @@ void hom_gate_dev(vsp_ctx* c, const int32_t* kinds, const uint32_t* d_in, uint32
         if (io)  // gates below the first remainder task are final once this key switch is
             gdone = first_gate_ending_after(full);
     };
-    launch_br(c, d_tasks, d_trlwe, pl.T, st, fork_iks, before_part);
+    // the INT8-GEMM key switch of the whole batch after the last wave is cheaper than the
+    // tensor-free one forked under the remainder wave (which then has the SMs to itself)
+    const bool fork = !iks_gemm_on(c, Gl);
+    launch_br(c, d_tasks, d_trlwe, pl.T, st, fork ? std::function<void(int)>(fork_iks)
+                                                  : std::function<void(int)>(), before_part);
     launch_iks(c, d_trlwe, d_gtask, d_glist + k1, Gl - k1, d_out, st);
     if (forked)
         VSP_CUDA_CHECK(cudaStreamWaitEvent(st, c->ev_join, 0));
@@ -1267,7 +1366,7 @@ void ram_write_unit_dev(vsp_ctx* c, uint32_t* d_ram, int v, int w, const uint32_
     // the whole-wave cells' key switch (low-priority stream), then the whole waves.
     const int full = p.fft ? br_plan(T, c->sms).full : 0;
     const int rem = T - full;
-    if (full && rem) {
+    if (full && rem && !iks_gemm_on(c, T)) {
         std::vector<int2> gt(full);
         std::vector<int> gl(full);
         for (int i = 0; i < full; i++) {
@@ -1574,8 +1673,10 @@ vsp_ctx* vsp_create(const vsp_params* params, int device)
         VSP_CUDA_CHECK(cudaMalloc(&c->d_tv1, tv.size() * 4));
         VSP_CUDA_CHECK(cudaMemcpy(c->d_tv1, tv.data(), tv.size() * 4, cudaMemcpyHostToDevice));
         configure_kernels();
-        if (const char* e = getenv("VSP_RAM_OVERLAP"))  // A/B knob for the option
+        if (const char* e = getenv("VSP_RAM_OVERLAP"))  // A/B knobs for the options
             c->ram_overlap = atoi(e) != 0;
+        if (const char* e = getenv("VSP_IKS_GEMM"))
+            c->iks_gemm = atoi(e) != 0;
         out = c.release();
     });
     return out;
@@ -1624,8 +1725,12 @@ void vsp_destroy(vsp_ctx* c)
         cudaEventDestroy(c->ev_wfork);
         cudaEventDestroy(c->ev_wdone);
     }
-    for (DevBuf* b : {&c->wlw, &c->wgt, &c->wgl})
+    for (DevBuf* b : {&c->wlw, &c->wgt, &c->wgl, &c->iks_S, &c->iks_C, &c->lt_ws})
         b->release();
+    if (c->d_k4t)
+        cudaFree(c->d_k4t);
+    if (c->lt)
+        cublasLtDestroy(c->lt);
     for (auto& kv : c->timers)  // profiling events never read back
         for (auto& e : kv.second.pending) {
             cudaEventDestroy(e.first);
@@ -1676,6 +1781,18 @@ int vsp_upload_keys(vsp_ctx* c, const uint32_t* bk1, const uint32_t* ksk, const 
         VSP_CUDA_CHECK(cudaMalloc(&c->d_ksk, (c->ksk_words() + kKskPad) * 4));
         VSP_CUDA_CHECK(cudaMemcpy(c->d_ksk, ksk, c->ksk_words() * 4, cudaMemcpyHostToDevice));
         VSP_CUDA_CHECK(cudaMemset(c->d_ksk + c->ksk_words(), 0, kKskPad * 4));
+        if (c->d_k4t)
+            cudaFree(c->d_k4t);
+        c->d_k4t = nullptr;
+        if (p.fft && p.N1 == 1024 && p.ksBaseBits == 2 && p.ksLen == 8) {
+            // the key-switching key as four signed-byte planes for the INT8-GEMM key switch
+            c->k4_npad = (int)((4 * (p.n + 1) + 15) / 16 * 16);
+            VSP_CUDA_CHECK(cudaMalloc(&c->d_k4t, (size_t)c->k4_npad * kIksGemmK));
+            iks_gemm_prep_key_kernel<<<kIksGemmK, 256, 0, c->stream>>>(c->d_ksk, c->d_k4t, (int)p.n,
+                                                                       c->k4_npad);
+            VSP_CUDA_CHECK(cudaGetLastError());
+            VSP_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+        }
         c->has_cb = false;
         if (has_cb) {
             const size_t bk2_words = (size_t)p.n * 2 * p.l2 * 2 * p.N2;
@@ -2672,6 +2789,9 @@ int vsp_set_option(vsp_ctx* c, const char* name, int64_t value)
         }
         else if (k == "ram_overlap") {
             c->ram_overlap = value != 0;
+        }
+        else if (k == "iks_gemm") {
+            c->iks_gemm = value != 0;
         }
         else {
             throw std::invalid_argument("unknown option: " + k);

@@ -325,3 +325,31 @@ def test_two_tasks_per_sm_latency_kernel_equals_one(prod, G):
     assert np.array_equal(one, two)
     idx = np.arange(0, G, max(1, G // 5))
     assert np.array_equal(two[idx], o.hom_gate_batch(kid[idx], ins[idx], threads=8))
+
+
+@pytest.mark.parametrize("G", [64, 141, 1500])
+def test_int8_gemm_key_switch_equals_tensor_free(prod, G):
+    """The key switch as an INT8 tensor-core GEMM (one-hot digit selectors x the key in
+    signed-byte planes, iks_gemm.cuh) gives the same words as iks_b2_kernel and the oracle:
+    identity key switches, and whole gate batches (MUX sums, NOT) with and without it."""
+    e, o = prod
+    rng = np.random.default_rng(900 + G)
+    k = oracle_keys("tfhe-80", 20200729, False)
+    p = vsp.ParameterSet("tfhe-80")
+    kid = rng.integers(0, len(GATE_KINDS), G).astype(np.int32)
+    bits = rng.integers(0, 2, size=(G, 3)).astype(np.uint8)
+    ins = vsp.encrypt(p, k["lv0"], bits.reshape(-1), 901 + G).reshape(G, 3, p.n + 1)
+    e.set_option("iks_gemm", 1)
+    with_gemm = e.hom_gate_batch(kid, ins)
+    e.set_option("iks_gemm", 0)
+    try:
+        without = e.hom_gate_batch(kid, ins)
+    finally:
+        e.set_option("iks_gemm", 1)
+    assert np.array_equal(with_gemm, without)
+    idx = np.arange(0, G, max(1, G // 6))
+    assert np.array_equal(with_gemm[idx], o.hom_gate_batch(kid[idx], ins[idx], threads=8))
+    lvl1 = np.stack([o.sample_extract(t, 0) for t in e.bootstrap_to_trlwe(ins[:G, 0])])
+    ks = e.identity_key_switch(lvl1)
+    for i in range(0, G, max(1, G // 4)):
+        assert np.array_equal(ks[i], o.identity_key_switch(lvl1[i]))
