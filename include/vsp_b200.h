@@ -267,13 +267,17 @@ int vsp_profile_reset(vsp_ctx* ctx);
 
 /* Launch plan the engine picks for a level-1 blind rotation of `tasks` tasks (FFT path;
  * test-det runs the exact kernel): out = {narrow-level latency kernel (1/0), tasks in
- * whole 8-task-per-SM waves, tasks per CTA of the remainder launch (0 = none)}.  Lets the
- * tests assert which wave boundaries a batch really crosses.  No reference counterpart. */
-int vsp_br_plan(vsp_ctx* ctx, size_t tasks, int32_t out[3]);
+ * whole 8-task-per-SM waves, tasks per SM of the remainder / single launch (0 = none),
+ * its kernel (0 none, 1 br1024, 2 br1024p two warps per task, 3 br_lat)}.  Lets the tests
+ * assert which wave boundaries a batch really crosses.  No reference counterpart. */
+int vsp_br_plan(vsp_ctx* ctx, size_t tasks, int32_t out[4]);
 /* Streaming multiprocessors of the context's device (sizes every launch plan). */
 int vsp_sm_count(vsp_ctx* ctx);
 /* Engine tuning options (no reference counterpart; results are bit-identical either way):
- *   "lat_tasks" 1|2: blind-rotation tasks per SM of narrow levels (br_lat / br_lat2). */
+ *   "lat_tasks" 1|2: blind-rotation tasks per SM of narrow levels (br_lat / br_lat2);
+ *   "ram_overlap" 0|1: the netlist runner's deferred RAM write unit;
+ *   "iks_gemm" 0|1: identity key switching as an INT8 tensor-core GEMM (default 1);
+ *   "br_pair" 0|1: partial blind-rotation waves with two warps per task (default 1). */
 int vsp_set_option(vsp_ctx* ctx, const char* name, int64_t value);
 
 /* Measured dense FP64 FMA throughput of `device` in TFLOP/s (the denominator of the

@@ -565,10 +565,12 @@ class Engine:
 
     def br_plan(self, tasks: int) -> dict:
         """The blind-rotation launch plan for `tasks` tasks: narrow-level latency kernel,
-        tasks in whole W=8 waves, tasks per CTA of the remainder wave."""
-        o = np.zeros(3, np.int32)
+        tasks in whole W=8 waves, tasks per SM of the remainder / single launch and its
+        kernel."""
+        o = np.zeros(4, np.int32)
         _check(lib().vsp_br_plan(self.h, tasks, _ptr(o)))
-        return {"lat": bool(o[0]), "full": int(o[1]), "w_rem": int(o[2])}
+        return {"lat": bool(o[0]), "full": int(o[1]), "w_rem": int(o[2]),
+                "rem_kernel": ("none", "br1024", "br1024p", "br_lat")[int(o[3])]}
 
     def set_option(self, name: str, value: int):
         """Engine tuning option (vsp_set_option): "lat_tasks" (1|2)."""

@@ -362,6 +362,186 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
 }
 
 // ---------------------------------------------------------------------------
+// br1024p_kernel: the throughput kernel with TWO warps per task, for partial waves (the
+// remainder of a split batch, mid-size batches).  A wave of W <= 4 tasks per SM leaves a
+// single warp per scheduler and runs at the latency of one task's 630-step chain; here
+// warp P of a task owns accumulator polynomial P: its digits (both levels), its two
+// forward transforms, the MAC of its two rows into both outputs, then the partners swap
+// the partial sums of each other's output through shared memory, and each warp inverts,
+// rounds and accumulates its own polynomial -- the next step's digits of polynomial P only
+// read polynomial P, so the pair needs no other synchronisation.  The four key rows of a
+// step sit in four 16 KiB slots (chunk 4 i + 2P + lvl in slot 2P + lvl, used by the TASKS
+// warps of parity P; the last of them refills it).
+template <int TASKS>
+struct BrPairSmem {
+    double2 ring[4][1024];
+    double2 tw2[kTw2Entries * 32];
+    double2 xbuf[2 * TASKS][kFftXbufStride];  // transposes, then the partial-sum exchange
+    uint32_t acc[TASKS][2048];
+    uint32_t dig[2 * TASKS][16 * 32];
+    uint64_t full[4];
+    uint32_t cnt[4];
+};
+
+template <int TASKS, int BG>
+__global__ void __launch_bounds__(64 * TASKS, 1)
+    br1024p_kernel(const uint32_t* __restrict__ tasks, const double2* __restrict__ bkfd,
+                   const double2* __restrict__ tw2g, uint32_t* __restrict__ out, int T, int n)
+{
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    auto& sm = *reinterpret_cast<BrPairSmem<TASKS>*>(smem_raw);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tl = warp >> 1, P = warp & 1;
+    int task = blockIdx.x * TASKS + tl;
+    const bool active = task < T;
+    if (!active)
+        task = T - 1;  // shadow a real task to keep the slot protocol
+    const uint32_t* lwe = tasks + (size_t)task * (n + 1);
+    const int nchunks = 4 * n;
+
+    for (int i = threadIdx.x; i < kTw2Entries * 32; i += blockDim.x)
+        sm.tw2[i] = tw2g[i];
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < 4; s++) {
+            mbar_init(&sm.full[s], 1);
+            sm.cnt[s] = 0;
+        }
+    }
+    uint32_t* acc = sm.acc[tl];
+    {
+        // acc = X^{-round(2N b)} * (0, mu...mu); warp P writes polynomial P
+        const uint32_t rot = (2048u - mod_switch_2n(lwe[n], 11)) & 2047u;
+        for (int q = lane; q < 1024; q += 32) {
+            uint32_t val = 0;
+            if (P == 1) {
+                if (rot < 1024)
+                    val = ((uint32_t)q < rot) ? (0u - kMu32) : kMu32;
+                else
+                    val = ((uint32_t)q < rot - 1024) ? kMu32 : (0u - kMu32);
+            }
+            acc[P * 1024 + q] = val;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < 4 && s < nchunks; s++) {
+            mbar_arrive_expect_tx(&sm.full[s], 16384);
+            bulk_g2s(sm.ring[s], bkfd + (size_t)s * 1024, 16384, &sm.full[s]);
+        }
+    }
+
+    constexpr uint32_t kHalf = 1u << (BG - 1);
+    constexpr uint32_t kMask = (1u << BG) - 1;
+    constexpr uint32_t kOffset = (kHalf << (32 - BG)) + (kHalf << (32 - 2 * BG));
+    double2* xbuf = sm.xbuf[warp];
+    const double2* xpeer = sm.xbuf[warp ^ 1];
+    const uint32_t* src = acc + P * 1024;
+    double2 accOwn[16], accOth[16];
+
+    auto release = [&](int c) {
+        __syncwarp();
+        if (lane == 0) {
+            const int s = c & 3;
+            const uint32_t old = atomicAdd(&sm.cnt[s], 1u);
+            if (old == TASKS - 1) {
+                sm.cnt[s] = 0;
+                const int cn = c + 4;
+                if (cn < nchunks) {
+                    fence_proxy_async();
+                    mbar_arrive_expect_tx(&sm.full[s], 16384);
+                    bulk_g2s(sm.ring[s], bkfd + (size_t)cn * 1024, 16384, &sm.full[s]);
+                }
+            }
+        }
+    };
+
+#pragma unroll 1
+    for (int i = 0; i < n; i++) {
+        const uint32_t bara = mod_switch_2n(lwe[i], 11);
+#pragma unroll
+        for (int j = 0; j < 16; j++) {
+            accOwn[j] = make_double2(0.0, 0.0);
+            accOth[j] = make_double2(0.0, 0.0);
+        }
+        double2 z[16];
+        {
+            // (X^bara - 1) acc_P; level-0 digits to z, level-1 parked (see br1024_kernel)
+            const uint32_t lo = (uint32_t)lane + (uint32_t)opaque_zero();
+            const uint32_t lk = lo - bara;
+            const uint32_t* srcl = src + lo;
+#pragma unroll
+            for (int j = 0; j < 16; j++) {
+                const uint32_t v0 = rot_coef1024(src, lk + 32 * j) - srcl[32 * j] + kOffset;
+                const uint32_t v1 = rot_coef1024(src, lk + 32 * j + 512) - srcl[32 * j + 512] + kOffset;
+                const uint32_t d0 = (v0 >> (32 - BG)) + (32768u - kHalf);
+                const uint32_t d1 = (v1 >> (32 - BG)) + (32768u - kHalf);
+                const uint32_t e0 = ((v0 >> (32 - 2 * BG)) & kMask) + (32768u - kHalf);
+                const uint32_t e1 = ((v1 >> (32 - 2 * BG)) & kMask) + (32768u - kHalf);
+                z[j].x = ob_to_double<15>(d0);
+                z[j].y = ob_to_double<15>(d1);
+                sm.dig[warp][j * 32 + lane] = e0 | (e1 << 16);
+            }
+        }
+#pragma unroll 1
+        for (int lvl = 0; lvl < 2; lvl++) {
+            if (lvl) {
+                __syncwarp();
+#pragma unroll
+                for (int j = 0; j < 16; j++) {
+                    const uint32_t w = sm.dig[warp][j * 32 + lane];
+                    z[j].x = ob_to_double<15>(w & 0xffffu);
+                    z[j].y = ob_to_double<15>(w >> 16);
+                }
+            }
+            fft512_fwd(z, xbuf, sm.tw2, lane);
+            const int c = 4 * i + 2 * P + lvl;
+            mbar_wait(&sm.full[c & 3], (uint32_t)(i & 1));
+            const double2* bo = sm.ring[c & 3] + P * 512;
+            const double2* bt = sm.ring[c & 3] + (1 - P) * 512;
+#pragma unroll
+            for (int j = 0; j < 16; j++) {
+                const double2 ba = bo[j * 32 + lane];
+                const double2 bb = bt[j * 32 + lane];
+                accOwn[j].x = fma(z[j].x, ba.x, fma(-z[j].y, ba.y, accOwn[j].x));
+                accOwn[j].y = fma(z[j].x, ba.y, fma(z[j].y, ba.x, accOwn[j].y));
+                accOth[j].x = fma(z[j].x, bb.x, fma(-z[j].y, bb.y, accOth[j].x));
+                accOth[j].y = fma(z[j].x, bb.y, fma(z[j].y, bb.x, accOth[j].y));
+            }
+            release(c);
+        }
+        // swap the partial sums of the partner's output, then invert my own output
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 16; j++)
+            xbuf[j * 32 + lane] = accOth[j];
+        bar_group(1 + tl, 64);
+#pragma unroll
+        for (int j = 0; j < 16; j++) {
+            const double2 q = xpeer[j * 32 + lane];
+            accOwn[j].x += q.x;
+            accOwn[j].y += q.y;
+        }
+        bar_group(1 + tl, 64);  // the partner has read my buffer before I transpose in it
+        fft512_inv(accOwn, xbuf, sm.tw2, lane);
+        uint32_t* dst = acc + P * 1024;
+#pragma unroll
+        for (int j = 0; j < 16; j++) {
+            const int p = lane + 32 * j;
+            dst[p] += (uint32_t)__double2ll_rn(accOwn[j].x);
+            dst[p + 512] += (uint32_t)__double2ll_rn(accOwn[j].y);
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+    if (active) {
+        uint4* d4 = reinterpret_cast<uint4*>(out + (size_t)task * 2048 + P * 1024);
+        const uint4* s4 = reinterpret_cast<const uint4*>(acc + P * 1024);
+        for (int q = lane; q < 256; q += 32)
+            d4[q] = s4[q];
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Latency-optimised blind rotation for narrow netlist levels (T <= ~2 x SMs), where
 // br1024_kernel runs one dependent chain of n external products per warp and per-level
 // latency is the chain length (630 x ~9 us).  Here FOUR warps share one task: warp r
@@ -390,10 +570,6 @@ struct BrLatSmem {
     __device__ double2* xbuf(int r) { return bufA[r]; }
 };
 
-__device__ __forceinline__ void bar_group(int id, int nthreads)
-{
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
 
 // PROBE: per-warp clock64 totals of the step phases -> probe[task][warp][16] (tuning).
 template <int BG, bool PROBE = false>

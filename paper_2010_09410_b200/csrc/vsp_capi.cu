@@ -272,6 +272,8 @@ struct vsp_ctx {
     // key switching as an INT8 tensor-core GEMM (iks_gemm.cuh): the key in signed-byte
     // planes, cuBLASLt handle, selector / product scratch; option "iks_gemm"
     bool iks_gemm = true;
+    // partial blind-rotation waves on br1024p_kernel (two warps per task); option "br_pair"
+    bool br_pair = true;
     int8_t* d_k4t = nullptr;
     int k4_npad = 0;
     cublasLtHandle_t lt = nullptr;
@@ -406,27 +408,6 @@ constexpr int kBrBg = 10;  // the FFT path is specialised for Bg1 = 2^10 (tfhe-8
 // which leaves half of the SMs free for the RAM write bars; vsp_ctx::lat_tasks).
 constexpr int kLat2Slots = 6;
 
-// Warps (= tasks) per CTA of the blind-rotation kernel.  Every task costs the same, so
-// time ~ waves(W) x t(W), t(W) = duration of one wave with W tasks per SM, measured on
-// B200 at n = 630 (scripts/br_occupancy.py -> profiles/r01_br_occupancy.json):
-// 1-3 tasks/SM are latency-bound (~5.7 ms: 630 dependent steps), 8 tasks/SM 8.7 ms.
-// Narrow netlist levels therefore get one task per SM, wide batches 7-8.
-int br_warps_for(int T, int sms)
-{
-    static const double t[9] = {0, 5.7, 5.7, 5.9, 6.5, 8.3, 8.7, 8.8, 8.7};
-    int best = 1;
-    double best_cost = 1e30;
-    for (int w = 1; w <= 8; w++) {
-        const long waves = (T + (long)sms * w - 1) / ((long)sms * w);
-        const double cost = (double)waves * t[w];
-        if (cost < best_cost - 1e-9) {
-            best_cost = cost;
-            best = w;
-        }
-    }
-    return best;
-}
-
 // VSP_BR_TMEM=1: the bootstrapping key reaches the warps through tensor memory (br1024
 // TM variant, W >= 5: one CTA per SM, all 512 TMEM columns).
 bool br_tmem()
@@ -452,6 +433,21 @@ template <int S, bool OFS>
 void launch_br8(vsp_ctx* c, const uint32_t* d_tasks, uint32_t* d_trlwe, int T, cudaStream_t st)
 {
     br1024_kernel<8, S, kBrBg, false, OFS><<<(T + 7) / 8, 256, sizeof(Br1024Smem<8, S>), st>>>(
+        d_tasks, c->d_bk1fd, c->d_tw2, d_trlwe, T, (int)c->p.n);
+}
+
+// Partial waves (W <= 4 tasks per SM) on the two-warps-per-task kernel; option "br_pair",
+// VSP_BR_PAIR overrides.
+bool br_pair(const vsp_ctx* c)
+{
+    static const int forced = getenv("VSP_BR_PAIR") ? atoi(getenv("VSP_BR_PAIR")) : -1;
+    return forced >= 0 ? forced != 0 : c->br_pair;
+}
+
+template <int TASKS>
+void launch_brp(vsp_ctx* c, const uint32_t* d_tasks, uint32_t* d_trlwe, int T, cudaStream_t st)
+{
+    br1024p_kernel<TASKS, kBrBg><<<(T + TASKS - 1) / TASKS, 64 * TASKS, sizeof(BrPairSmem<TASKS>), st>>>(
         d_tasks, c->d_bk1fd, c->d_tw2, d_trlwe, T, (int)c->p.n);
 }
 
@@ -543,19 +539,46 @@ void launch_br2(vsp_ctx* c, const uint32_t* d_lwe, int ninputs, const uint64_t* 
 // before_part(lo, hi): called (host side) before the launch that consumes tasks [lo, hi);
 // when set, whole waves are launched one wave per launch so the host pipeline can upload
 // the inputs of wave k + 1 while wave k runs.
-// Launch plan of a level-1 blind rotation of T tasks (FFT path):
-//  - lat: T <= 2 x SMs -> the narrow-level latency kernel (br_lat, one task per CTA);
-//  - else whole waves of W = 8 tasks per SM over the first `full` tasks, and the remainder
-//    as one wave of W_rem = br_warps_for(rem) tasks per SM.  Every task costs the same and
-//    one CTA runs per SM, so a partial last wave of W = 8 would cost a full wave.
+// Launch plan of a level-1 blind rotation of T tasks (FFT path), from a cost model of
+// measured wave times at n = 630 (ms per wave; scripts/br_occupancy.py, scripts/br_ab.py):
+//   br1024, W tasks per SM (one warp per task):  5.7 5.7 5.9 6.5 8.3 8.7 8.8 8.7
+//   br1024p, W <= 4 tasks per SM (two warps per task): 4.3 4.3 4.32 4.59
+//   br_lat, one task per SM (four warps):       1.96
+// Every task costs the same and one CTA runs per SM, so a partial wave costs a whole one.
+// Candidates: one launch of W tasks per SM (ceil(T / (SMs W)) waves), or k whole W = 8
+// waves + the remainder at its own best (latency kernel when it fits two of its waves);
+// the cheapest wins (whole waves on a tie).  T <= 2 SMs: the latency kernel.
 struct BrPlan {
     bool lat = false;
-    int full = 0;      // tasks in whole W = 8 waves
-    int w_rem = 0;     // tasks per CTA of the remainder launch (0: none)
-    int forced = 0;    // VSP_BR_WARPS override
+    int full = 0;       // tasks in whole W = 8 waves
+    int w_rem = 0;      // tasks per SM of the remainder / single launch (0: none)
+    bool rem_lat = false;  // the remainder runs on the latency kernel
+    int forced = 0;     // VSP_BR_WARPS override
 };
 
-BrPlan br_plan(int T, int sms)
+double br_wave_ms(int W, bool pair)
+{
+    static const double t[9] = {0, 5.7, 5.7, 5.9, 6.5, 8.3, 8.7, 8.8, 8.7};
+    static const double tp[5] = {0, 4.3, 4.3, 4.32, 4.59};
+    return (pair && W <= 4) ? tp[W] : t[W];
+}
+
+constexpr double kLatWaveMs = 1.96;
+
+// best single launch for T tasks: (cost, W)
+std::pair<double, int> br_best_single(long T, int sms, bool pair)
+{
+    std::pair<double, int> best{1e30, 1};
+    for (int w = 1; w <= 8; w++) {
+        const long waves = (T + (long)sms * w - 1) / ((long)sms * w);
+        const double cost = (double)waves * br_wave_ms(w, pair);
+        if (cost < best.first - 1e-9)
+            best = {cost, w};
+    }
+    return best;
+}
+
+BrPlan br_plan(int T, int sms, bool pair)
 {
     BrPlan pl;
     if (const char* e = getenv("VSP_BR_WARPS"))  // tuning knob (scripts/br_occupancy.py)
@@ -568,12 +591,42 @@ BrPlan br_plan(int T, int sms)
         pl.lat = T > 0;
         return pl;
     }
+    const auto single = br_best_single(T, sms, pair);
     const long wave8 = 8L * sms;
-    pl.full = (br_warps_for(T, sms) == 8 && T > wave8) ? (int)(T / wave8 * wave8) : 0;
-    const int rem = T - pl.full;
-    pl.w_rem = rem ? br_warps_for(rem, sms) : 0;
+    const long k = T / wave8;
+    if (k > 0) {
+        const long rem = T - k * wave8;
+        double rem_cost = 0;
+        int rem_w = 0;
+        bool rem_lat = false;
+        if (rem > 0) {
+            const auto r = br_best_single(rem, sms, pair);
+            rem_cost = r.first;
+            rem_w = r.second;
+            if (rem <= 2L * sms) {
+                const double lat = (double)((rem + sms - 1) / sms) * kLatWaveMs;
+                if (lat < rem_cost) {
+                    rem_cost = lat;
+                    rem_lat = true;
+                    rem_w = 0;
+                }
+            }
+        }
+        const double split = (double)k * br_wave_ms(8, pair) + rem_cost;
+        if (split <= single.first + 1e-9) {
+            pl.full = (int)(k * wave8);
+            pl.w_rem = rem_w;
+            pl.rem_lat = rem_lat;
+            return pl;
+        }
+    }
+    pl.w_rem = single.second;
     return pl;
 }
+
+bool br_pair(const vsp_ctx* c);
+
+BrPlan br_plan(const vsp_ctx* c, int T) { return br_plan(T, c->sms, br_pair(c)); }
 
 void launch_br(vsp_ctx* c, const uint32_t* d_tasks, uint32_t* d_trlwe, int T, cudaStream_t st,
                const std::function<void(int)>& after_full = {},
@@ -583,13 +636,25 @@ void launch_br(vsp_ctx* c, const uint32_t* d_tasks, uint32_t* d_trlwe, int T, cu
         return;
     const Params& p = c->p;
     const long wave8 = 8L * c->sms;
-    const BrPlan plan = br_plan(T, c->sms);
+    const BrPlan plan = br_plan(c, T);
     if (before_part && !(p.fft && plan.full > 0))
         before_part(0, T);
     if (p.fft) {
         const int full = plan.full;
         const int forced = plan.forced;
         auto launch_part_on = [&](const uint32_t* tk, uint32_t* tr, int cnt, int W, cudaStream_t s) {
+            if (W <= 4 && br_pair(c) && !forced) {
+                // partial wave: two warps per task (br1024p_kernel), W tasks per CTA
+                switch (W) {
+                case 4: launch_brp<4>(c, tk, tr, cnt, s); break;
+                case 3: launch_brp<3>(c, tk, tr, cnt, s); break;
+                case 2: launch_brp<2>(c, tk, tr, cnt, s); break;
+                default: launch_brp<1>(c, tk, tr, cnt, s); break;
+                }
+                VSP_CUDA_CHECK(cudaGetLastError());
+                c->launches++;
+                return;
+            }
             switch (W) {
             case 8: launch_br_w<8>(c, tk, tr, cnt, s); break;
             case 7: launch_br_w<7>(c, tk, tr, cnt, s); break;
@@ -605,6 +670,17 @@ void launch_br(vsp_ctx* c, const uint32_t* d_tasks, uint32_t* d_trlwe, int T, cu
         };
         auto launch_part = [&](const uint32_t* tk, uint32_t* tr, int cnt, int W) {
             launch_part_on(tk, tr, cnt, W, st);
+        };
+        // the remainder after the whole waves: its own best kernel (plan.rem_lat: br_lat)
+        auto launch_rem_on = [&](const uint32_t* tk, uint32_t* tr, int cnt, cudaStream_t s) {
+            if (plan.rem_lat) {
+                br_lat_kernel<kBrBg><<<cnt, kLatThreads, sizeof(BrLatSmem), s>>>(
+                    tk, c->d_bk1fd, c->d_tw2, tr, (int)p.n);
+                VSP_CUDA_CHECK(cudaGetLastError());
+                c->launches++;
+                return;
+            }
+            launch_part_on(tk, tr, cnt, plan.w_rem, s);
         };
         if (plan.lat) {
             // narrow level: latency kernel, 4 warps per task (bootstrap.cuh br_lat_kernel)
@@ -662,16 +738,16 @@ void launch_br(vsp_ctx* c, const uint32_t* d_tasks, uint32_t* d_trlwe, int T, cu
                 c->ensure_aux_stream();
                 VSP_CUDA_CHECK(cudaEventRecord(c->ev_full, st));
                 VSP_CUDA_CHECK(cudaStreamWaitEvent(c->hstream, c->ev_full, 0));
-                launch_part_on(d_tasks + (size_t)full * (p.n + 1), d_trlwe + (size_t)full * 2 * p.N1,
-                               rem, plan.w_rem, c->hstream);
+                launch_rem_on(d_tasks + (size_t)full * (p.n + 1), d_trlwe + (size_t)full * 2 * p.N1,
+                              rem, c->hstream);
                 VSP_CUDA_CHECK(cudaEventRecord(c->ev_rem, c->hstream));
                 after_full(full);
                 VSP_CUDA_CHECK(cudaStreamWaitEvent(st, c->ev_rem, 0));
                 return;
             }
             if (rem)
-                launch_part(d_tasks + (size_t)full * (p.n + 1), d_trlwe + (size_t)full * 2 * p.N1,
-                            rem, plan.w_rem);
+                launch_rem_on(d_tasks + (size_t)full * (p.n + 1), d_trlwe + (size_t)full * 2 * p.N1,
+                              rem, st);
         });
         c->counters[1] += (uint64_t)T;
         return;
@@ -872,6 +948,13 @@ void configure_kernels()
     VSP_CUDA_CHECK(cudaFuncSetAttribute(br_lat2_kernel<kBrBg, 2, kLat2Slots>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)sizeof(BrLat2Smem<2, kLat2Slots>)));
+    auto pair_attr = [](auto k, int bytes) {
+        VSP_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    };
+    pair_attr(br1024p_kernel<4, kBrBg>, (int)sizeof(BrPairSmem<4>));
+    pair_attr(br1024p_kernel<3, kBrBg>, (int)sizeof(BrPairSmem<3>));
+    pair_attr(br1024p_kernel<2, kBrBg>, (int)sizeof(BrPairSmem<2>));
+    pair_attr(br1024p_kernel<1, kBrBg>, (int)sizeof(BrPairSmem<1>));
     set_br_attr<8>();
     set_br_attr<7>();
     set_br_attr<6>();
@@ -1364,7 +1447,7 @@ void ram_write_unit_dev(vsp_ctx* c, uint32_t* d_ram, int v, int w, const uint32_
     // whole-wave cells runs UNDER the remainder wave (which holds half of each SM): key
     // switch the remainder cells, then their blind rotations (high-priority stream) beside
     // the whole-wave cells' key switch (low-priority stream), then the whole waves.
-    const int full = p.fft ? br_plan(T, c->sms).full : 0;
+    const int full = p.fft ? br_plan(c, T).full : 0;
     const int rem = T - full;
     if (full && rem && !iks_gemm_on(c, T)) {
         std::vector<int2> gt(full);
@@ -2793,6 +2876,9 @@ int vsp_set_option(vsp_ctx* c, const char* name, int64_t value)
         else if (k == "iks_gemm") {
             c->iks_gemm = value != 0;
         }
+        else if (k == "br_pair") {
+            c->br_pair = value != 0;
+        }
         else {
             throw std::invalid_argument("unknown option: " + k);
         }
@@ -2855,16 +2941,18 @@ int vsp_client_keygen_dev(const vsp_params* pp, uint64_t seed, int with_cb, int 
     });
 }
 
-int vsp_br_plan(vsp_ctx* c, size_t tasks, int32_t out[3])
+int vsp_br_plan(vsp_ctx* c, size_t tasks, int32_t out[4])
 {
     return guard([&] {
         std::lock_guard<std::mutex> lk(c->mu);
         if (tasks > (size_t)INT32_MAX)
             throw std::invalid_argument("br_plan: too many tasks");
-        const BrPlan pl = br_plan((int)tasks, c->sms);
+        const BrPlan pl = br_plan(c, (int)tasks);
         out[0] = pl.lat ? 1 : 0;
         out[1] = pl.full;
         out[2] = pl.w_rem;
+        // kernel of the remainder (or single) launch: 0 none, 1 br1024, 2 br1024p, 3 br_lat
+        out[3] = pl.rem_lat ? 3 : pl.w_rem == 0 ? 0 : (pl.w_rem <= 4 && br_pair(c)) ? 2 : 1;
     });
 }
 

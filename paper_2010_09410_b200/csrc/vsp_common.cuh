@@ -129,6 +129,12 @@ __device__ __forceinline__ void tmem_ld_x16(uint32_t taddr, uint32_t (&r)[16])
         : "r"(taddr));
 }
 
+// Named barrier over `nthreads` threads (a warp group of the CTA).
+__device__ __forceinline__ void bar_group(int id, int nthreads)
+{
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
 // (X^k p)[q] mod X^N + 1 (polyRotate, poly.hpp:32-48) = +-p[(q-k) mod 2N]; qk = q - k.
 __device__ __forceinline__ uint32_t rot_coef1024(const uint32_t* src, uint32_t qk)
 {

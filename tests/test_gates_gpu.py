@@ -183,13 +183,14 @@ def test_pipelined_host_batch_equals_single_device_call(prod):
     assert np.array_equal(dec, want)
 
 
-# (tasks) -> launch plan the engine must pick on a 148-SM B200 (vsp_br_plan)
+# (tasks) -> launch plan the engine must pick on a 148-SM B200 (vsp_br_plan, cost model)
 WAVE_PLANS = {
-    1: {"lat": True, "full": 0, "w_rem": 0},        # latency kernel, one task
-    150: {"lat": True, "full": 0, "w_rem": 0},      # latency kernel, 150 CTAs
-    2368: {"lat": False, "full": 2368, "w_rem": 0},  # exactly two whole W=8 waves
-    2400: {"lat": False, "full": 0, "w_rem": 6},    # one W=6 launch (3 waves), no split
-    2995: {"lat": False, "full": 2368, "w_rem": 5},  # two whole waves + a W=5 remainder
+    1: {"lat": True, "full": 0, "w_rem": 0, "rem_kernel": "none"},        # latency kernel
+    150: {"lat": True, "full": 0, "w_rem": 0, "rem_kernel": "none"},      # 150 CTAs
+    2368: {"lat": False, "full": 2368, "w_rem": 0, "rem_kernel": "none"},  # two whole waves
+    2400: {"lat": False, "full": 2368, "w_rem": 0, "rem_kernel": "br_lat"},  # + 32 on br_lat
+    2995: {"lat": False, "full": 2368, "w_rem": 5, "rem_kernel": "br1024"},  # + W=5 wave
+    300: {"lat": False, "full": 0, "w_rem": 3, "rem_kernel": "br1024p"},  # two warps/task
 }
 
 
@@ -231,7 +232,7 @@ def test_mux_straddling_wave_boundaries_host_pipeline(prod):
     G = 1601
     kid = np.array([GATE_KINDS.index("AND")] + [GATE_KINDS.index("MUX")] * 1600, np.int32)
     if e.sms == 148:
-        assert e.br_plan(3201) == {"lat": False, "full": 2368, "w_rem": 6}
+        assert e.br_plan(3201) == {"lat": False, "full": 2368, "w_rem": 3, "rem_kernel": "br1024p"}
     rng = np.random.default_rng(1601)
     k = oracle_keys("tfhe-80", 20200729, False)
     p = vsp.ParameterSet("tfhe-80")
@@ -261,9 +262,9 @@ def test_not_only_and_mux_heavy_batches_tfhe80(prod):
         x[i, 0] = o.encrypt(int(b))
     out = e.hom_gate_batch(["NOT"] * 40, x)
     assert [o.decrypt(c) for c in out] == [1 - int(b) for b in bits]
-    G = 700  # 1,400 blind-rotation tasks: one W=5 launch (two waves)
+    G = 700  # 1,400 blind-rotation tasks: one whole W=8 wave + 216 on the latency kernel
     if e.sms == 148:
-        assert e.br_plan(2 * G) == {"lat": False, "full": 0, "w_rem": 5}
+        assert e.br_plan(2 * G) == {"lat": False, "full": 1184, "w_rem": 0, "rem_kernel": "br_lat"}
     k = oracle_keys("tfhe-80", 20200729, False)
     p = vsp.ParameterSet("tfhe-80")
     mb = rng.integers(0, 2, size=(G, 3)).astype(np.uint8)
@@ -353,3 +354,27 @@ def test_int8_gemm_key_switch_equals_tensor_free(prod, G):
     ks = e.identity_key_switch(lvl1)
     for i in range(0, G, max(1, G // 4)):
         assert np.array_equal(ks[i], o.identity_key_switch(lvl1[i]))
+
+
+@pytest.mark.parametrize("G", [300, 4096])
+def test_two_warps_per_task_partial_wave_equals_one(prod, G):
+    """br1024p_kernel (partial waves with two warps per task: a single W=3 launch for 300
+    tasks, the 544-task W=4 remainder of 4,096) gives the same words as br1024_kernel."""
+    e, o = prod
+    rng = np.random.default_rng(1200 + G)
+    k = oracle_keys("tfhe-80", 20200729, False)
+    p = vsp.ParameterSet("tfhe-80")
+    kid = rng.choice([GATE_KINDS.index("NAND"), GATE_KINDS.index("XOR")], G).astype(np.int32)
+    bits = rng.integers(0, 2, size=(G, 3)).astype(np.uint8)
+    ins = vsp.encrypt(p, k["lv0"], bits.reshape(-1), 1201 + G).reshape(G, 3, p.n + 1)
+    if e.sms == 148:
+        assert e.br_plan(G)["rem_kernel"] == "br1024p"
+    two = e.hom_gate_batch(kid, ins)
+    e.set_option("br_pair", 0)
+    try:
+        one = e.hom_gate_batch(kid, ins)
+    finally:
+        e.set_option("br_pair", 1)
+    assert np.array_equal(one, two)
+    want = np.array([TRUTH[GATE_KINDS[kk]](*(int(x) for x in b)) for kk, b in zip(kid, bits)])
+    assert np.array_equal(vsp.decrypt(k["lv0"], two), want)
