@@ -682,12 +682,14 @@ __global__ void __launch_bounds__(kLatThreads, 1)
             for (int j = 0; j < 16; j++)
                 sm.bufA[r][j * 32 + lane] = z[j];
             const int s = i & 1;
+            // the key rows of this step: waited for before the barrier, so the wait overlaps
+            // the slowest warp's transform instead of following it
+            mbar_wait(&sm.full[s], (uint32_t)((i >> 1) & 1));
+            mark(3);
             bar_group(1, 128);  // all four rows transformed
             mark(2);
             // output o at this lane's 8 slots: acc_o = sum_q z_q . bk[q][o], rows in order
             // 0..3 as in br1024_kernel
-            mbar_wait(&sm.full[s], (uint32_t)((i >> 1) & 1));
-            mark(3);
             const double2* bk = sm.ring[s] + o * 512;
             double2 u[8];
 #pragma unroll
