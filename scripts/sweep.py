@@ -5,7 +5,7 @@ res = []
 for G in [1024, 4096, 16384, 65536, 262144, 1048576]:
     steps = 2 if G >= 262144 else 5
     r = subprocess.run([sys.executable, "bench.py", "--gates", str(G), "--steps", str(steps),
-                        "--warmup", "3", "--no-cpu-baseline", "--no-e2e"],
+                        "--warmup", "3", "--no-cpu-baseline", "--no-e2e", "--headline-only"],
                        capture_output=True, text=True, timeout=1800)
     try:
         d = json.loads(r.stdout.strip().splitlines()[-1])
