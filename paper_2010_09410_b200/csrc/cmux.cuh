@@ -55,8 +55,19 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
         return;
     const ChainTask& task = tasks[t];
     uint32_t* acc = sm.acc[warp];
-    for (int q = lane; q < 2048; q += 32)
-        acc[q] = task.c1[q];
+    {
+        // one round trip: 16 independent 16-byte loads per lane (a rolled word loop
+        // serialised 64 global-load latencies per chain, ~30 us per single-step layer)
+        const uint4* c1 = reinterpret_cast<const uint4*>(task.c1);
+        uint4* a4 = reinterpret_cast<uint4*>(acc);
+        uint4 v[16];
+#pragma unroll
+        for (int k = 0; k < 16; k++)
+            v[k] = __ldg(c1 + lane + 32 * k);
+#pragma unroll
+        for (int k = 0; k < 16; k++)
+            a4[lane + 32 * k] = v[k];
+    }
     __syncwarp();
     const uint32_t half = 1u << (bgbits - 1);
     const uint32_t mask = (1u << bgbits) - 1;
@@ -152,8 +163,13 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
         }
         __syncwarp();
     }
-    for (int q = lane; q < 2048; q += 32)
-        task.out[q] = acc[q];
+    {
+        uint4* o4 = reinterpret_cast<uint4*>(task.out);
+        const uint4* a4 = reinterpret_cast<const uint4*>(acc);
+#pragma unroll
+        for (int k = 0; k < 16; k++)
+            o4[lane + 32 * k] = a4[lane + 32 * k];
+    }
 }
 
 // Exact-path chain (test-det): one CTA of N threads per task; selectors raw TRGSW words.
