@@ -524,6 +524,13 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(256, 1)
     for (int i = 0; i < n; i++) {
         const uint32_t bara = mod_switch_2n(a_next, 12);
         a_next = lwe[i + 1];
+        if (tid < 16 && i + 1 < n) {
+            // next step's quarter of bk2 (16 segments of 8 KiB: row u, this CTA's polynomial
+            // half and branch) into L2 while this step runs, as br2c_kernel does
+            const double2* nk = bk2fd + (size_t)(i + 1) * 8 * 4 * 1024 + (size_t)(4 * P) * 4 * 1024 +
+                                (size_t)br * 512 + (size_t)tid * 1024;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nk), "r"(8192) : "memory");
+        }
         // ---- A: row L on the warp pair (L, L + 4), branch br
         {
             const int L = warp & 3, h = warp >> 2;
