@@ -87,6 +87,10 @@ def parse():
     ap.add_argument("--levels", type=int, default=32, help="cycle config: logic depth")
     ap.add_argument("--sub-steps", type=int, default=0,
                     help="timed steps of the memory / cycle sub-objects (0 = --steps)")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "gloo"],
+                    help="multi-GPU exchange: NCCL over NVLink (default) or the engine's "
+                         "host-callback exchange over gloo (flow check on a 1-GPU box; "
+                         "timings are not a scaling result)")
     return ap.parse_args()
 
 
@@ -165,11 +169,18 @@ class Ctx:
     def __init__(self, args, world, rank, local):
         import torch
         self.args, self.world, self.rank, self.local = args, world, rank, local
+        # one GPU per rank; on a box with fewer GPUs than ranks (--exchange gloo smoke runs)
+        # ranks share devices round robin
+        self.local = local = local % max(torch.cuda.device_count(), 1)
         torch.cuda.set_device(local)
         self.dist = None
+        self.gloo = args.exchange == "gloo"
         if world > 1:
             import torch.distributed as dist
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            if self.gloo:
+                dist.init_process_group("gloo")
+            else:
+                dist.init_process_group("nccl", device_id=torch.device("cuda", local))
             self.dist = dist
         self.dev = f"cuda:{local}"
         self._peak = None
@@ -181,11 +192,27 @@ class Ctx:
             self._peak = vsp.fp64_peak_tflops(self.local)
         return self._peak
 
+    def connect(self, eng):
+        """Attach an engine to the ranks: NCCL over NVLink (default), or the host-callback
+        exchange over gloo (--exchange gloo: exercises the multi-rank flow on any box)."""
+        if self.world == 1:
+            return
+        if self.gloo:
+            dist = self.dist
+
+            def ag(b: bytes):
+                box = [None] * self.world
+                dist.all_gather_object(box, b)
+                return box
+            eng.attach_exchange(self.rank, self.world, ag)
+        else:
+            eng.connect()
+
     def max_over_ranks(self, x: float) -> float:
         if not self.dist:
             return x
         import torch
-        t = torch.tensor([x], dtype=torch.float64, device=self.dev)
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if self.gloo else self.dev)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -269,8 +296,7 @@ def measure_gates(cx: Ctx) -> dict | None:
     keys, kinds, ins, truth = make_workload(vsp, p, GA, 1000)
     eng = vsp.Engine(p, device=local)
     eng.upload_keys(keys)
-    if world > 1:
-        eng.connect()
+    cx.connect(eng)
 
     d_in = torch.from_numpy(ins.view(np.int32)).to(cx.dev)
     d_out = torch.empty((GA, p.n + 1), dtype=torch.int32, device=cx.dev)
@@ -452,8 +478,7 @@ def measure_memory(cx: Ctx, steps: int) -> dict | None:
     rng = np.random.default_rng(77)
     eng = vsp.Engine(p, device=local)
     eng.upload_keys(keys)
-    if world > 1:
-        eng.connect()
+    cx.connect(eng)
     v, w = 8, 16
     words = [int(x) for x in rng.integers(0, 1 << w, 1 << v)]
     ram = vsp.encrypt_ram(p, keys, words_to_image(words, v, w), v, w, 5)
@@ -589,8 +614,7 @@ def measure_cycle(cx: Ctx, steps: int) -> dict | None:
     rng = np.random.default_rng(99)
     eng = vsp.Engine(p, device=local)
     eng.upload_keys(keys)
-    if world > 1:
-        eng.connect()  # every level's gates sharded across the ranks + all-gathered
+    cx.connect(eng)  # every level's gates sharded across the ranks + all-gathered
     nl = N.synthetic_netlist(seed=1, levels=args.levels)
     ev = N.Evaluator(nl, eng)
     v, w = 8, 16
