@@ -564,7 +564,11 @@ struct BrLatSmem {
     double2 tw2[kTw2Entries * 32];
     double2 bufA[4][kLatBuf];  // transformed row z_r (also warp r's forward transposes)
     double2 bufB[2][kLatBuf];  // inverse-transform transposes of warps 0 / 1
-    uint32_t acc[2048];
+    // accumulator polynomial P at acc[P * stride]: EXT = 1 keeps its negacyclic extension
+    // (acc, -acc, acc: 3072 words), so a coefficient of X^-bara acc is one load at a lane
+    // base plus an immediate offset (no index wrap / sign select in the digit pass); EXT = 2
+    // keeps (acc, -acc) and applies one per-lane sign instead of the third copy
+    uint32_t acc[2 * 3072];
     uint64_t full[2];
     uint64_t empty[2];  // slot consumed by the four transform warps (count 4)
     __device__ double2* xbuf(int r) { return bufA[r]; }
@@ -572,7 +576,10 @@ struct BrLatSmem {
 
 
 // PROBE: per-warp clock64 totals of the step phases -> probe[task][warp][16] (tuning).
-template <int BG, bool PROBE = false>
+// EXT: negacyclic-extension accumulator (see BrLatSmem).  Measured per 140-task level:
+// 1.889 ms (EXT 0, the round-1 layout: 1024 words per polynomial, rot_coef1024), 1.679 ms
+// (EXT 1), 1.672 ms (EXT 2, default); the others stay for A/B (VSP_LAT_EXT=0 / 1).
+template <int BG, bool PROBE = false, int EXT = 2>
 __global__ void __launch_bounds__(kLatThreads, 1)
     br_lat_kernel(const uint32_t* __restrict__ tasks, const double2* __restrict__ bkfd,
                   const double2* __restrict__ tw2g, uint32_t* __restrict__ out, int n,
@@ -601,6 +608,7 @@ __global__ void __launch_bounds__(kLatThreads, 1)
             mbar_init(&sm.empty[q], 4);
         }
     }
+    constexpr int kStride = EXT == 1 ? 3072 : EXT == 2 ? 2048 : 1024;  // words per polynomial
     {
         const uint32_t rot = (2048u - mod_switch_2n(lwe[n], 11)) & 2047u;
         for (int q = threadIdx.x; q < 1024; q += blockDim.x) {
@@ -610,7 +618,15 @@ __global__ void __launch_bounds__(kLatThreads, 1)
                 val = ((uint32_t)q < rot) ? (0u - kMu32) : kMu32;
             else
                 val = ((uint32_t)q < rot - 1024) ? kMu32 : (0u - kMu32);
-            sm.acc[1024 + q] = val;
+            sm.acc[kStride + q] = val;
+            if constexpr (EXT) {
+                sm.acc[1024 + q] = 0;
+                sm.acc[kStride + 1024 + q] = 0u - val;
+            }
+            if constexpr (EXT == 1) {
+                sm.acc[2048 + q] = 0;
+                sm.acc[kStride + 2048 + q] = val;
+            }
         }
     }
     __syncthreads();
@@ -633,7 +649,7 @@ __global__ void __launch_bounds__(kLatThreads, 1)
         constexpr uint32_t kMask = (1u << BG) - 1;
         constexpr uint32_t kOffset = (kHalf << (32 - BG)) + (kHalf << (32 - 2 * BG));
         const int P = r >> 1, lvl = r & 1;
-        const uint32_t* src = sm.acc + P * 1024;
+        const uint32_t* src = sm.acc + P * kStride;
         const uint32_t sh = (uint32_t)(32 - (lvl + 1) * BG);
         // MAC / inverse role: output o (0: a, 1: b) on the warp pair (o, o + 2), half h
         const int o = r & 1, h = r >> 1;
@@ -662,10 +678,16 @@ __global__ void __launch_bounds__(kLatThreads, 1)
                 const uint32_t lo = (uint32_t)lane + (uint32_t)opaque_zero();
                 const uint32_t lk = lo - bara;
                 const uint32_t* srcl = src + lo;
+                // EXT: X^-bara acc at lane + 32 j is srcr[32 j] (EXT 2: times (-1)^sg)
+                const uint32_t* srcr = src + (lk & (EXT == 1 ? 2047u : 1023u));
+                const uint32_t sg = EXT == 2 ? (lk >> 10) & 1u : 0u;
+                const uint32_t sm_ = 0u - sg, ko = kOffset + sg;
 #pragma unroll
                 for (int j = 0; j < 16; j++) {
-                    const uint32_t v0 = rot_coef1024(src, lk + 32 * j) - srcl[32 * j] + kOffset;
-                    const uint32_t v1 = rot_coef1024(src, lk + 32 * j + 512) - srcl[32 * j + 512] + kOffset;
+                    const uint32_t r0 = EXT ? srcr[32 * j] ^ sm_ : rot_coef1024(src, lk + 32 * j);
+                    const uint32_t r1 = EXT ? srcr[32 * j + 512] ^ sm_ : rot_coef1024(src, lk + 32 * j + 512);
+                    const uint32_t v0 = r0 - srcl[32 * j] + ko;
+                    const uint32_t v1 = r1 - srcl[32 * j + 512] + ko;
                     // level-lvl digit = bits [32 - (lvl+1) BG, 32 - lvl BG) of v, recentred
                     // (the mask is a no-op for level 0); offset binary for ob_to_double
                     z[j].x = ob_to_double<31>(((v0 >> sh) & kMask) + (0x80000000u - kHalf));
@@ -715,12 +737,22 @@ __global__ void __launch_bounds__(kLatThreads, 1)
             fft512_inv_pair_regs(u, sm.bufB[o], twi, lane, h, 3 + o);
             mark(6);
             // (every warp read acc for its digits before barrier 1)
-            uint32_t* dst = sm.acc + o * 1024;
+            uint32_t* dst = sm.acc + o * kStride;
 #pragma unroll
             for (int t = 0; t < 8; t++) {
                 const int p = L + 32 * (t + 8 * e);
-                dst[p] += (uint32_t)__double2ll_rn(u[t].x);
-                dst[p + 512] += (uint32_t)__double2ll_rn(u[t].y);
+                const uint32_t n0 = dst[p] + (uint32_t)__double2ll_rn(u[t].x);
+                const uint32_t n1 = dst[p + 512] + (uint32_t)__double2ll_rn(u[t].y);
+                dst[p] = n0;
+                dst[p + 512] = n1;
+                if constexpr (EXT) {
+                    dst[p + 1024] = 0u - n0;
+                    dst[p + 1536] = 0u - n1;
+                }
+                if constexpr (EXT == 1) {
+                    dst[p + 2048] = n0;
+                    dst[p + 2560] = n1;
+                }
             }
             mark(7);
             bar_group(2, 128);  // acc updated before the next step's digits
@@ -734,9 +766,8 @@ __global__ void __launch_bounds__(kLatThreads, 1)
     }
     __syncthreads();
     uint4* dst = reinterpret_cast<uint4*>(out + (size_t)task * 2048);
-    const uint4* s4 = reinterpret_cast<const uint4*>(sm.acc);
     for (int q = threadIdx.x; q < 512; q += blockDim.x)
-        dst[q] = s4[q];
+        dst[q] = reinterpret_cast<const uint4*>(sm.acc + (q >> 8) * kStride)[q & 255];
 }
 
 // ---------------------------------------------------------------------------

@@ -473,18 +473,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
 // Two cluster barriers per step; each exchange buffer is written and read between the
 // same pair of barriers, so single buffers suffice.
 struct Br2qSmem {
-    uint64_t acc[2048];                 // polynomial P (identical on both branch CTAs)
+    uint64_t acc[4096];                 // polynomial P (identical on both branch CTAs); EXT:
+                                        // its negacyclic extension (acc, -acc)
     double2 reg[4][kBr2cRegion];        // row L (forward), then own outputs k (2 x)
     double2 part[2][512];               // MAC partials from (1-P, b), by output k
     double2 xin[2][512];                // branch 1-b inverse outputs from (P, 1-b)
     double2 tw2[kTw2Entries * 32];      // this branch's root (1 + b)
 };
 
+// PROBE: clock64 totals per phase -> probe[cta rank][warp][8] of task 0 (tuning).
+// EXT: digits read X^-bara acc at a per-lane base plus immediate offsets from the
+// (acc, -acc) extension with one per-lane sign, and convert by the offset-binary DADD
+// (EXT = false: the round-1 index wrap / select per coefficient and I2F; A/B only).
+template <bool PROBE = false, bool EXT = true>
 __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(256, 1)
     br2q_kernel(const uint32_t* __restrict__ tasks, int ninputs, const uint64_t* __restrict__ hv,
                 const double2* __restrict__ bk2fd, const double2* __restrict__ tw2g,
-                uint64_t* __restrict__ out, int n, int bgbits)
+                uint64_t* __restrict__ out, int n, int bgbits,
+                unsigned long long* __restrict__ probe = nullptr)
 {
+    unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long tprev = 0;
+    auto mark = [&](int k) {
+        if constexpr (PROBE) {
+            const long long t = clock64();
+            ph[k] += (unsigned long long)(t - tprev);
+            tprev = t;
+        }
+    };
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
     extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -510,6 +526,8 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(256, 1)
                     val = ((uint32_t)q < rot - 2048) ? h2 : (0ull - h2);
             }
             sm.acc[q] = val;
+            if constexpr (EXT)
+                sm.acc[2048 + q] = 0ull - val;
         }
     }
     cluster.sync();
@@ -520,6 +538,8 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(256, 1)
         offset += half << (64 - i * bgbits);
 
     uint32_t a_next = lwe[0];
+    if constexpr (PROBE)
+        tprev = clock64();
 #pragma unroll 1
     for (int i = 0; i < n; i++) {
         const uint32_t bara = mod_switch_2n(a_next, 12);
@@ -542,13 +562,31 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(256, 1)
                 const uint64_t v = r - sm.acc[q] + offset;
                 return (double)(int32_t)(int64_t)(((v >> sh) & mask) - half);
             };
+            // EXT: coefficient q = Lv + 256 e + o of X^-bara acc is (-1)^sg srcr[o]
+            const uint32_t lk = (uint32_t)(Lv + 256 * e) - bara;
+            const uint64_t* srcr = sm.acc + (lk & 2047u);
+            const uint64_t* srcl = sm.acc + Lv + 256 * e;
+            const uint32_t sg = (lk >> 11) & 1u;
+            const uint64_t sgm = 0ull - (uint64_t)sg, off2 = offset + sg;
+            const double obc = 4503599627370496.0 + (double)half;  // 2^52 + half
+            auto digit_ext = [&](int o) -> double {
+                const uint64_t v = (srcr[o] ^ sgm) - srcl[o] + off2;
+                return __hiloint2double(0x43300000, (int)(uint32_t)((v >> sh) & mask)) - obc;
+            };
             double2 z[8];
 #pragma unroll
             for (int t = 0; t < 8; t++) {
-                const uint32_t p = (uint32_t)(Lv + 32 * (t + 8 * e));
-                const double2 u = make_double2(digit(p), digit(p + 1024));
-                const double2 v = make_double2(digit(p + 512), digit(p + 1536));
-                z[t] = split_fwd(u, v, br);
+                if constexpr (EXT) {
+                    const double2 u = make_double2(digit_ext(32 * t), digit_ext(32 * t + 1024));
+                    const double2 v = make_double2(digit_ext(32 * t + 512), digit_ext(32 * t + 1536));
+                    z[t] = split_fwd(u, v, br);
+                }
+                else {
+                    const uint32_t p = (uint32_t)(Lv + 32 * (t + 8 * e));
+                    const double2 u = make_double2(digit(p), digit(p + 1024));
+                    const double2 v = make_double2(digit(p + 512), digit(p + 1536));
+                    z[t] = split_fwd(u, v, br);
+                }
             }
             double2* rg = sm.reg[L];
             if (br == 0)
@@ -560,7 +598,9 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(256, 1)
             for (int t = 0; t < 8; t++)
                 rg[(2 * t + e) * 32 + Lv] = z[t];
         }
+        mark(0);
         __syncthreads();
+        mark(1);
         // ---- B: partial MAC at this branch's 512 points, 2 per thread
         {
             const double2* K = bk2fd + (size_t)i * 8 * 4 * 1024 + (size_t)(4 * P) * 4 * 1024 +
@@ -606,7 +646,9 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(256, 1)
                 }
             }
         }
+        mark(2);
         cluster.sync();  // partials exchanged
+        mark(3);
         // ---- C: own outputs k = 0, 1 (lo, hi) on warp pairs (k, k + 4); warps 2, 3, 6, 7
         // idle here
         {
@@ -636,7 +678,9 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(256, 1)
                 }
             }
         }
+        mark(4);
         cluster.sync();  // both branches' inverse outputs in place
+        mark(5);
         // ---- D: inverse split stage, exact rounding, lo/hi recombination into acc[P]
         {
             const double c = 0.70710678118654752440;
@@ -657,11 +701,23 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(256, 1)
                     part[hh][3] = __double2ll_rn(vv.y);  // p + 1536
                 }
 #pragma unroll
-                for (int e4 = 0; e4 < 4; e4++)
-                    sm.acc[p + 512 * e4] += (uint64_t)part[0][e4] + ((uint64_t)part[1][e4] << 32);
+                for (int e4 = 0; e4 < 4; e4++) {
+                    const uint64_t nv = sm.acc[p + 512 * e4] + (uint64_t)part[0][e4] +
+                                        ((uint64_t)part[1][e4] << 32);
+                    sm.acc[p + 512 * e4] = nv;
+                    if constexpr (EXT)
+                        sm.acc[2048 + p + 512 * e4] = 0ull - nv;
+                }
             }
         }
+        mark(6);
         __syncthreads();
+        mark(7);
+    }
+    if constexpr (PROBE) {
+        if (lane == 0 && task == 0)
+            for (int k = 0; k < 8; k++)
+                probe[((size_t)cr * 8 + warp) * 8 + k] = ph[k];
     }
     if (br == 0) {
         uint64_t* dst = out + (size_t)task * 4096 + (size_t)P * 2048;

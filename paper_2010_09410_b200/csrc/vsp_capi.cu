@@ -371,6 +371,13 @@ int lat_tasks(const vsp_ctx* c)
     return forced ? forced : c->lat_tasks;
 }
 
+// VSP_LAT_EXT=0 / 1: br_lat_kernel's accumulator layout (A/B only; default 2)
+int lat_ext()
+{
+    static const int e = getenv("VSP_LAT_EXT") ? atoi(getenv("VSP_LAT_EXT")) : 2;
+    return e;
+}
+
 template <class F>
 void timed(vsp_ctx* c, const char* name, cudaStream_t st, F&& launch)
 {
@@ -525,6 +532,27 @@ void launch_br2(vsp_ctx* c, const uint32_t* d_lwe, int ninputs, const uint64_t* 
         br2c_kernel<<<2 * T, 256, sizeof(Br2cSmem), st>>>(d_lwe, ninputs, d_hv, c->d_bk2fd,
                                                             c->d_tw2, d_acc, (int)c->p.n,
                                                             (int)c->p.Bg2Bits);
+    else if (getenv("VSP_BR2_PROBE")) {  // tuning only: per-phase clock64 of task 0
+        unsigned long long* d_pr = nullptr;
+        VSP_CUDA_CHECK(cudaMalloc(&d_pr, 4 * 8 * 8 * 8));
+        br2q_kernel<true><<<4 * T, 256, sizeof(Br2qSmem), st>>>(d_lwe, ninputs, d_hv, c->d_bk2fd,
+                                                                c->d_tw2, d_acc, (int)c->p.n,
+                                                                (int)c->p.Bg2Bits, d_pr);
+        std::vector<unsigned long long> h(256);
+        VSP_CUDA_CHECK(cudaMemcpyAsync(h.data(), d_pr, 256 * 8, cudaMemcpyDeviceToHost, st));
+        VSP_CUDA_CHECK(cudaStreamSynchronize(st));
+        cudaFree(d_pr);
+        for (int r = 0; r < 4; r += 3)
+            for (int w = 0; w < 8; w += 2) {
+                fprintf(stderr, "br2q probe cta %d warp %d cycles/step:", r, w);
+                for (int k = 0; k < 8; k++)
+                    fprintf(stderr, " %.0f", (double)h[(r * 8 + w) * 8 + k] / c->p.n);
+                fprintf(stderr, "\n");
+            }
+    }
+    else if (getenv("VSP_BR2_EXT") && atoi(getenv("VSP_BR2_EXT")) == 0)  // A/B only
+        br2q_kernel<false, false><<<4 * T, 256, sizeof(Br2qSmem), st>>>(
+            d_lwe, ninputs, d_hv, c->d_bk2fd, c->d_tw2, d_acc, (int)c->p.n, (int)c->p.Bg2Bits);
     else
         br2q_kernel<<<4 * T, 256, sizeof(Br2qSmem), st>>>(d_lwe, ninputs, d_hv, c->d_bk2fd,
                                                             c->d_tw2, d_acc, (int)c->p.n,
@@ -706,6 +734,12 @@ void launch_br(vsp_ctx* c, const uint32_t* d_tasks, uint32_t* d_trlwe, int T, cu
                     br_lat2_kernel<kBrBg, 2, kLat2Slots>
                         <<<(T + 1) / 2, kLat2Threads(2), sizeof(BrLat2Smem<2, kLat2Slots>), st>>>(
                             d_tasks, c->d_bk1fd, c->d_tw2, d_trlwe, T, (int)p.n);
+                else if (lat_ext() == 0)  // A/B: round-1 accumulator layout
+                    br_lat_kernel<kBrBg, false, 0><<<T, kLatThreads, sizeof(BrLatSmem), st>>>(
+                        d_tasks, c->d_bk1fd, c->d_tw2, d_trlwe, (int)p.n);
+                else if (lat_ext() == 1)  // A/B: three-copy accumulator
+                    br_lat_kernel<kBrBg, false, 1><<<T, kLatThreads, sizeof(BrLatSmem), st>>>(
+                        d_tasks, c->d_bk1fd, c->d_tw2, d_trlwe, (int)p.n);
                 else
                     br_lat_kernel<kBrBg><<<T, kLatThreads, sizeof(BrLatSmem), st>>>(
                         d_tasks, c->d_bk1fd, c->d_tw2, d_trlwe, (int)p.n);
@@ -945,6 +979,12 @@ void configure_kernels()
     VSP_CUDA_CHECK(cudaFuncSetAttribute(br_lat_kernel<kBrBg, true>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)sizeof(BrLatSmem)));
+    VSP_CUDA_CHECK(cudaFuncSetAttribute(br_lat_kernel<kBrBg, false, 0>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)sizeof(BrLatSmem)));
+    VSP_CUDA_CHECK(cudaFuncSetAttribute(br_lat_kernel<kBrBg, false, 1>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)sizeof(BrLatSmem)));
     VSP_CUDA_CHECK(cudaFuncSetAttribute(br_lat2_kernel<kBrBg, 2, kLat2Slots>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)sizeof(BrLat2Smem<2, kLat2Slots>)));
@@ -967,7 +1007,12 @@ void configure_kernels()
                                         (int)sizeof(Br2Smem)));
     VSP_CUDA_CHECK(cudaFuncSetAttribute(br2c_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)sizeof(Br2cSmem)));
-    VSP_CUDA_CHECK(cudaFuncSetAttribute(br2q_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    VSP_CUDA_CHECK(cudaFuncSetAttribute(br2q_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)sizeof(Br2qSmem)));
+    VSP_CUDA_CHECK(cudaFuncSetAttribute(br2q_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)sizeof(Br2qSmem)));
+    VSP_CUDA_CHECK(cudaFuncSetAttribute(br2q_kernel<false, false>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)sizeof(Br2qSmem)));
     VSP_CUDA_CHECK(cudaFuncSetAttribute(cmux_chain1024_kernel<kChainWarps, 0>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2338,7 +2383,9 @@ int vsp_blind_rotate_lvl2_batch(vsp_ctx* c, const uint32_t* in, const uint64_t* 
         VSP_CUDA_CHECK(cudaMemcpyAsync(d_in, in, T * n1 * 4, cudaMemcpyHostToDevice, c->stream));
         VSP_CUDA_CHECK(cudaMemcpyAsync(d_h, h, T * 8, cudaMemcpyHostToDevice, c->stream));
         if (p.fft) {
-            launch_br2(c, d_in, (int)T, d_h, (int)T, d_acc, c->stream);
+            timed(c, "br2", c->stream, [&] {
+                launch_br2(c, d_in, (int)T, d_h, (int)T, d_acc, c->stream);
+            });
         }
         else {
             const int N = (int)N2;

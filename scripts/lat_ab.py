@@ -18,4 +18,5 @@ for _ in range(5):
     e.hom_gate_batch(kid, ins)
 e.profile_enable(False)
 ms, n = e.profile_read("br_lat")
-print(f"T={T} br_lat {ms / max(n, 1):.3f} ms/level correct={ok}")
+import hashlib
+print(f"T={T} br_lat {ms / max(n, 1):.3f} ms/level correct={ok} out={hashlib.sha1(out.tobytes()).hexdigest()[:12]}")
