@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
                         z[j].y = ob_to_double<15>(w >> 16);
                     }
                 }
-                fft512_fwd(z, xbuf, sm.tw2, lane);
+                fft512_fwd<0, false, false>(z, xbuf, sm.tw2, lane);
                 const double2* row = S + (size_t)(P * 2 + lvl) * 1024;
 #pragma unroll
                 for (int j = 0; j < 16; j++) {
@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
             __syncwarp();
         }
         // acc <- c0' + round(inverse): mode 0 c0' = base, mode 1 c0' = acc
-        fft512_inv(accA, xbuf, sm.tw2, lane);
+        fft512_inv<0, false, false>(accA, xbuf, sm.tw2, lane);
         __syncwarp();
 #pragma unroll
         for (int j = 0; j < 16; j++) {
@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
             acc[p] = b0 + (uint32_t)__double2ll_rn(accA[j].x);
             acc[p + 512] = b1 + (uint32_t)__double2ll_rn(accA[j].y);
         }
-        fft512_inv(accB, xbuf, sm.tw2, lane);
+        fft512_inv<0, false, false>(accB, xbuf, sm.tw2, lane);
 #pragma unroll
         for (int j = 0; j < 16; j++) {
             const int p = lane + 32 * j;

@@ -200,6 +200,35 @@ __device__ __forceinline__ double2 shfl_xor_d2(double2 v, int m)
     return v;
 }
 
+// Per-lane select as ONE LOP3 per 32-bit word: m = 0 -> a, m = ~0 -> b.  Written as the
+// ternary, the compiler emits a move plus a predicated move per word -- in the lane-pair
+// exchanges of the last forward / first inverse stage that was ~1,000 of the ~6,600
+// instructions of an external product.
+__device__ __forceinline__ uint32_t lop_sel(uint32_t m, uint32_t a, uint32_t b)
+{
+    uint32_t r;
+    asm("lop3.b32 %0, %1, %2, %3, 0xD8;" : "=r"(r) : "r"(a), "r"(b), "r"(m));  // (a & ~m) | (b & m)
+    return r;
+}
+__device__ __forceinline__ double dsel(uint32_t m, double a, double b)
+{
+    return __hiloint2double((int)lop_sel(m, (uint32_t)__double2hiint(a), (uint32_t)__double2hiint(b)),
+                            (int)lop_sel(m, (uint32_t)__double2loint(a), (uint32_t)__double2loint(b)));
+}
+__device__ __forceinline__ double2 d2sel(uint32_t m, double2 a, double2 b)
+{
+    return make_double2(dsel(m, a.x, b.x), dsel(m, a.y, b.y));
+}
+// LS = false: the plain ternary (kernels whose register allocation prefers it).
+template <bool LS>
+__device__ __forceinline__ double2 sel2(uint32_t m, double2 a, double2 b)
+{
+    if constexpr (LS)
+        return d2sel(m, a, b);
+    else
+        return m ? b : a;
+}
+
 // The one data exchange of the transform: lane L's value j sits at position L + 32 j
 // before it and at (L & 1) + 2 j + 32 (L >> 1) after it (stride-34 padding keeps both
 // phases bank-conflict free).  HALF moves the real parts, then the imaginary parts,
@@ -280,7 +309,7 @@ __device__ __forceinline__ void xpose_inv(double2 (&v)[16], void* buf, int lane)
 // kFftXbufStride doubles).  twt(e): this lane's tangent-form per-lane twiddle of entry
 // e < kTw2Plain (a shared-memory load, or a register when the kernel has room to keep
 // all twelve: fft512_fwd_regs).
-template <int ROOT, bool HALF, class TWT>
+template <int ROOT, bool HALF, class TWT, bool LS = true>
 __device__ __forceinline__ void fft512_fwd_g(double2 (&v)[16], void* xbuf, const TWT& twt, int lane)
 {
     const double2* tw1t = &c_tw1t[ROOT][0] + opaque_zero();
@@ -313,13 +342,13 @@ __device__ __forceinline__ void fft512_fwd_g(double2 (&v)[16], void* xbuf, const
                     bf_fwd_tq<0>(v[j], v[j + h], w);
             }
     }
-    const bool odd = lane & 1;
+    const uint32_t odd = 0u - (uint32_t)(lane & 1);  // select mask
 #pragma unroll
     for (int k = 0; k < 8; k++) {
-        const double2 send = odd ? v[k] : v[k + 8];
+        const double2 send = sel2<LS>(odd, v[k + 8], v[k]);
         const double2 recv = shfl_xor_d2(send, 1);
-        double2 u = odd ? recv : v[k];
-        double2 w = odd ? v[k + 8] : recv;
+        double2 u = sel2<LS>(odd, v[k], recv);
+        double2 w = sel2<LS>(odd, recv, v[k + 8]);
         const int br = bitrev_const(k, 3);
         const double2 t = twt(tw_entry(8, br & 3));
         if (br >> 2)
@@ -332,12 +361,13 @@ __device__ __forceinline__ void fft512_fwd_g(double2 (&v)[16], void* xbuf, const
 }
 
 // tw2: smem table [kTw2Entries][32] double2 (plain, then tangent).
-template <int ROOT = 0, bool HALF = false>
+template <int ROOT = 0, bool HALF = false, bool LS = true>
 __device__ __forceinline__ void fft512_fwd(double2 (&v)[16], void* xbuf,
                                            const double2* tw2, int lane)
 {
     const double2* tw2t = tw2 + kTw2Plain * 32;
-    fft512_fwd_g<ROOT, HALF>(v, xbuf, [&](int e) { return tw2t[e * 32 + lane]; }, lane);
+    auto twt = [&](int e) { return tw2t[e * 32 + lane]; };
+    fft512_fwd_g<ROOT, HALF, decltype(twt), LS>(v, xbuf, twt, lane);
 }
 
 // Same with the twelve tangent twiddles of this lane held in registers (twr[e]).
@@ -349,11 +379,11 @@ __device__ __forceinline__ void fft512_fwd_regs(double2 (&v)[16], void* xbuf,
 }
 
 // Exact inverse of fft512_fwd up to the factor 512 (folded into the key).
-template <int ROOT = 0, bool HALF = false>
+template <int ROOT = 0, bool HALF = false, bool LS = true>
 __device__ __forceinline__ void fft512_inv(double2 (&v)[16], void* xbuf,
                                            const double2* tw2, int lane)
 {
-    const bool odd = lane & 1;
+    const uint32_t odd = 0u - (uint32_t)(lane & 1);  // select mask
 #pragma unroll
     for (int k = 0; k < 8; k++) {
         double2 a = v[k], b = v[k + 8];
@@ -363,10 +393,10 @@ __device__ __forceinline__ void fft512_inv(double2 (&v)[16], void* xbuf,
             bf_inv_q<1>(a, b, t);
         else
             bf_inv_q<0>(a, b, t);
-        const double2 send = odd ? a : b;
+        const double2 send = sel2<LS>(odd, b, a);
         const double2 recv = shfl_xor_d2(send, 1);
-        v[k] = odd ? recv : a;
-        v[k + 8] = odd ? b : recv;
+        v[k] = sel2<LS>(odd, a, recv);
+        v[k + 8] = sel2<LS>(odd, recv, b);
     }
 #pragma unroll
     for (int d = 7; d >= 4; d--) {
@@ -401,7 +431,7 @@ template <int ROOT = 0>
 __device__ __forceinline__ void fft512_inv2(double2 (&va)[16], double2 (&vb)[16], void* xbuf,
                                             const double2* tw2, int lane)
 {
-    const bool odd = lane & 1;
+    const uint32_t odd = 0u - (uint32_t)(lane & 1);  // select mask
 #pragma unroll
     for (int k = 0; k < 8; k++) {
         const int br = bitrev_const(k, 3);
@@ -416,12 +446,12 @@ __device__ __forceinline__ void fft512_inv2(double2 (&va)[16], double2 (&vb)[16]
             bf_inv_q<0>(a, b, t);
             bf_inv_q<0>(c, d, t);
         }
-        const double2 ra = shfl_xor_d2(odd ? a : b, 1);
-        const double2 rb = shfl_xor_d2(odd ? c : d, 1);
-        va[k] = odd ? ra : a;
-        va[k + 8] = odd ? b : ra;
-        vb[k] = odd ? rb : c;
-        vb[k + 8] = odd ? d : rb;
+        const double2 ra = shfl_xor_d2(d2sel(odd, b, a), 1);
+        const double2 rb = shfl_xor_d2(d2sel(odd, d, c), 1);
+        va[k] = d2sel(odd, a, ra);
+        va[k + 8] = d2sel(odd, ra, b);
+        vb[k] = d2sel(odd, c, rb);
+        vb[k + 8] = d2sel(odd, rb, d);
     }
 #pragma unroll
     for (int d = 7; d >= 4; d--) {
