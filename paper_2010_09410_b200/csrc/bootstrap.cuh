@@ -558,6 +558,7 @@ __global__ void __launch_bounds__(64 * TASKS, 1)
 // have released it (mbarrier `empty`).
 constexpr int kLatBuf = kFftXbufStride;  // double2 per exchange / transpose buffer
 constexpr int kLatThreads = 160;          // 4 transform warps + 1 producer warp
+constexpr int kLatProducerSleepNs = 1024;  // producer back-off between empty-slot probes
 
 struct BrLatSmem {
     double2 ring[2][4 * 1024];
@@ -638,7 +639,7 @@ __global__ void __launch_bounds__(kLatThreads, 1)
             for (int i = 0; i < n; i++) {
                 const int s = i & 1;
                 if (i >= 2)
-                    mbar_wait(&sm.empty[s], (uint32_t)(((i - 2) >> 1) & 1));
+                    mbar_wait_sleep(&sm.empty[s], (uint32_t)(((i - 2) >> 1) & 1), kLatProducerSleepNs);
                 mbar_arrive_expect_tx(&sm.full[s], 65536);
                 bulk_g2s(sm.ring[s], bkfd + (size_t)i * 4096, 65536, &sm.full[s]);
             }
