@@ -149,8 +149,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
             const int p = lane + 32 * j;
             const uint32_t b0 = mode == 0 ? __ldg(base + p) : acc[p];
             const uint32_t b1 = mode == 0 ? __ldg(base + p + 512) : acc[p + 512];
-            acc[p] = b0 + (uint32_t)__double2ll_rn(accA[j].x);
-            acc[p + 512] = b1 + (uint32_t)__double2ll_rn(accA[j].y);
+            acc[p] = b0 + round_u32(accA[j].x);
+            acc[p + 512] = b1 + round_u32(accA[j].y);
         }
         fft512_inv<0, false, false>(accB, xbuf, sm.tw2, lane);
 #pragma unroll
@@ -158,8 +158,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
             const int p = lane + 32 * j;
             const uint32_t b0 = mode == 0 ? __ldg(base + 1024 + p) : acc[1024 + p];
             const uint32_t b1 = mode == 0 ? __ldg(base + 1024 + p + 512) : acc[1024 + p + 512];
-            acc[1024 + p] = b0 + (uint32_t)__double2ll_rn(accB[j].x);
-            acc[1024 + p + 512] = b1 + (uint32_t)__double2ll_rn(accB[j].y);
+            acc[1024 + p] = b0 + round_u32(accB[j].x);
+            acc[1024 + p + 512] = b1 + round_u32(accB[j].y);
         }
         __syncwarp();
     }

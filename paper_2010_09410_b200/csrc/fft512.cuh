@@ -184,6 +184,17 @@ __device__ __forceinline__ double ob_to_double(uint32_t u)
     return __hiloint2double(0x43300000, (int)u) - (4503599627370496.0 + (double)(1ull << K));
 }
 
+// Round-half-even of x to an integer, mod 2^32, in ONE DADD instead of the quarter-rate
+// F2I.S64.F64 of __double2ll_rn: for |x| < 2^51, x + 1.5 * 2^52 lies in [2^52, 2^53), where
+// doubles are exactly the integers, so the addition rounds x half-to-even (the default
+// mode, as llrint, fft.hpp:47-50) and the low mantissa word is round(x) + 2^51 = round(x)
+// mod 2^32.  The level-1 inverse outputs are sums of 4,096 products of digits |d| <= 2^9
+// and key words < 2^31: ~2^45 for uniform key words, the bound 2^51 is ~100 sigma away.
+__device__ __forceinline__ uint32_t round_u32(double x)
+{
+    return (uint32_t)__double2loint(__dadd_rn(x, 6755399441055744.0));
+}
+
 // An opaque zero: keeps the compiler from hoisting the per-stage twiddle loads out of
 // the blind-rotation loop (which would pin ~60 registers for the whole kernel).
 __device__ __forceinline__ int opaque_zero()

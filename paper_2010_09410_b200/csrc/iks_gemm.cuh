@@ -83,7 +83,9 @@ __global__ void __launch_bounds__(256) iks_gemm_selectors_kernel(
 
 // out[glist[gi]] = (0, ..., 0, b') - sum_b 256^b C[gi][b (n+1) + kk]  (mod 2^32), with b'
 // the extracted b (MUX: both plus mu, ops.cpp:886-892) exactly as iks_init_kernel.
-__global__ void iks_gemm_epilogue_kernel(const int32_t* __restrict__ C, int npad,
+// Split-K: the nsplit partial products C_b = C + b * cstride are summed mod 2^32 first.
+__global__ void iks_gemm_epilogue_kernel(const int32_t* __restrict__ C, int npad, int nsplit,
+                                         size_t cstride,
                                          const uint32_t* __restrict__ trlwe, const int2* __restrict__ gtask,
                                          const int* __restrict__ glist, const int* __restrict__ seidx,
                                          uint32_t* __restrict__ out, int n, int N)
@@ -100,8 +102,12 @@ __global__ void iks_gemm_epilogue_kernel(const int32_t* __restrict__ C, int npad
             if (tt.y >= 0)
                 v += trlwe[(size_t)tt.y * 2 * N + N + se] + kMu32;
         }
-        const uint32_t s = (uint32_t)c[kk] + ((uint32_t)c[(n + 1) + kk] << 8) +
-                           ((uint32_t)c[2 * (n + 1) + kk] << 16) + ((uint32_t)c[3 * (n + 1) + kk] << 24);
+        uint32_t s = 0;
+        for (int b = 0; b < nsplit; b++) {
+            const int32_t* cb = c + (size_t)b * cstride;
+            s += (uint32_t)cb[kk] + ((uint32_t)cb[(n + 1) + kk] << 8) +
+                 ((uint32_t)cb[2 * (n + 1) + kk] << 16) + ((uint32_t)cb[3 * (n + 1) + kk] << 24);
+        }
         out[(size_t)gate * (n + 1) + kk] = v - s;
     }
 }

@@ -828,7 +828,22 @@ bool iks_gemm_on(const vsp_ctx* c, int Gl)
 // C (Mpad x npad, int32, row-major) = S (Mpad x K_, int8, row-major) x K4 (K_ x npad):
 // in cuBLASLt's column-major terms C^T = (K4t)^T S^T, a "TN" int8 GEMM with K contiguous
 // in both operands (the tensor-core IMMA layout).
-void iks_gemm_run(vsp_ctx* c, const int8_t* S, int Mpad, int32_t* C, cudaStream_t st)
+//
+// Split-K (nsplit > 1): a batch of M <= a few hundred key switches is one row of GEMM
+// tiles -- ~10 CTAs on 148 SMs, each streaming a 24,576-deep slice of the 62 MB key.  The
+// K dimension is cut into nsplit strided batches (partial products C_b, summed mod 2^32 by
+// the epilogue: the planes recombine mod 2^32, so wrapped int32 partial sums stay exact).
+int iks_nsplit(int Mpad)
+{
+    static const int forced = getenv("VSP_IKS_SPLIT") ? atoi(getenv("VSP_IKS_SPLIT")) : 0;
+    if (forced > 0)
+        return forced;
+    // measured (B200, n = 630): 140 key switches 0.075 / 0.050 / 0.044 / 0.052 ms at
+    // 1 / 2 / 4 / 8 splits; 4,096: 0.272 / 0.251 / 0.273 ms at 1 / 2 / 4
+    return Mpad <= 512 ? 4 : 2;
+}
+
+void iks_gemm_run(vsp_ctx* c, const int8_t* S, int Mpad, int32_t* C, cudaStream_t st, int nsplit)
 {
     if (!c->lt)
         lt_check(cublasLtCreate(&c->lt), "create");
@@ -850,10 +865,24 @@ void iks_gemm_run(vsp_ctx* c, const int8_t* S, int Mpad, int32_t* C, cudaStream_
         const cublasOperation_t opT = CUBLAS_OP_T, opN = CUBLAS_OP_N;
         lt_check(cublasLtMatmulDescSetAttribute(desc, CUBLASLT_MATMUL_DESC_TRANSA, &opT, sizeof opT), "transa");
         lt_check(cublasLtMatmulDescSetAttribute(desc, CUBLASLT_MATMUL_DESC_TRANSB, &opN, sizeof opN), "transb");
-        lt_check(cublasLtMatrixLayoutCreate(&la, CUDA_R_8I, K, Np, K), "layout A");
-        lt_check(cublasLtMatrixLayoutCreate(&lb, CUDA_R_8I, K, Mpad, K), "layout B");
+        const int Ks = K / nsplit;
+        lt_check(cublasLtMatrixLayoutCreate(&la, CUDA_R_8I, Ks, Np, K), "layout A");
+        lt_check(cublasLtMatrixLayoutCreate(&lb, CUDA_R_8I, Ks, Mpad, K), "layout B");
         lt_check(cublasLtMatrixLayoutCreate(&lc, CUDA_R_32I, Np, Mpad, Np), "layout C");
-        auto it = c->lt_algo.find(Mpad);
+        if (nsplit > 1) {
+            const int32_t cnt = nsplit;
+            const int64_t sk = Ks, sc = (int64_t)Np * Mpad;
+            for (auto l : {la, lb, lc})
+                lt_check(cublasLtMatrixLayoutSetAttribute(l, CUBLASLT_MATRIX_LAYOUT_BATCH_COUNT, &cnt,
+                                                          sizeof cnt), "batch count");
+            lt_check(cublasLtMatrixLayoutSetAttribute(la, CUBLASLT_MATRIX_LAYOUT_STRIDED_BATCH_OFFSET,
+                                                      &sk, sizeof sk), "batch stride A");
+            lt_check(cublasLtMatrixLayoutSetAttribute(lb, CUBLASLT_MATRIX_LAYOUT_STRIDED_BATCH_OFFSET,
+                                                      &sk, sizeof sk), "batch stride B");
+            lt_check(cublasLtMatrixLayoutSetAttribute(lc, CUBLASLT_MATRIX_LAYOUT_STRIDED_BATCH_OFFSET,
+                                                      &sc, sizeof sc), "batch stride C");
+        }
+        auto it = c->lt_algo.find(Mpad * 64 + nsplit);
         if (it == c->lt_algo.end()) {
             lt_check(cublasLtMatmulPreferenceCreate(&pref), "preference");
             lt_check(cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES,
@@ -864,7 +893,7 @@ void iks_gemm_run(vsp_ctx* c, const int8_t* S, int Mpad, int32_t* C, cudaStream_
                      "heuristic");
             if (found < 1)
                 throw std::runtime_error("cuBLASLt: no int8 GEMM algorithm for the key switch");
-            it = c->lt_algo.emplace(Mpad, h.algo).first;
+            it = c->lt_algo.emplace(Mpad * 64 + nsplit, h.algo).first;
         }
         const int32_t one = 1, zero = 0;
         lt_check(cublasLtMatmul(c->lt, desc, &one, c->d_k4t, la, S, lb, &zero, C, lc, C, lc,
@@ -888,15 +917,17 @@ void launch_iks(vsp_ctx* c, const uint32_t* d_trlwe, const int2* d_gtask, const 
     const Params& p = c->p;
     if (iks_gemm_on(c, Gl)) {
         const int Mpad = (Gl + 15) / 16 * 16;
+        const int nsplit = iks_nsplit(Mpad);
         int8_t* S = c->iks_S.as<int8_t>((size_t)Mpad * kIksGemmK);
-        int32_t* C = c->iks_C.as<int32_t>((size_t)Mpad * c->k4_npad);
+        int32_t* C = c->iks_C.as<int32_t>((size_t)Mpad * c->k4_npad * nsplit);
         timed(c, "iks", st, [&] {
             iks_gemm_selectors_kernel<<<Gl, 256, 0, st>>>(d_trlwe, d_gtask, d_glist, d_seidx, S,
                                                           (int)p.N1);
             VSP_CUDA_CHECK(cudaGetLastError());
-            iks_gemm_run(c, S, Mpad, C, st);
-            iks_gemm_epilogue_kernel<<<Gl, 128, 0, st>>>(C, c->k4_npad, d_trlwe, d_gtask, d_glist,
-                                                         d_seidx, d_out, (int)p.n, (int)p.N1);
+            iks_gemm_run(c, S, Mpad, C, st, nsplit);
+            iks_gemm_epilogue_kernel<<<Gl, 128, 0, st>>>(C, c->k4_npad, nsplit, (size_t)Mpad * c->k4_npad,
+                                                         d_trlwe, d_gtask, d_glist, d_seidx, d_out,
+                                                         (int)p.n, (int)p.N1);
             VSP_CUDA_CHECK(cudaGetLastError());
         });
         c->launches += 3;
