@@ -277,7 +277,9 @@ int vsp_sm_count(vsp_ctx* ctx);
  *   "lat_tasks" 1|2: blind-rotation tasks per SM of narrow levels (br_lat / br_lat2);
  *   "ram_overlap" 0|1: the netlist runner's deferred RAM write unit;
  *   "iks_gemm" 0|1: identity key switching as an INT8 tensor-core GEMM (default 1);
- *   "br_pair" 0|1: partial blind-rotation waves with two warps per task (default 1). */
+ *   "br_pair" 0|1: partial blind-rotation waves with two warps per task (default 1);
+ *   "iks_split" k: split-K factor of the key-switch GEMM, k divides 24,576 into multiples
+ *      of 16 (0 = automatic: 4 up to 512 key switches, else 2). */
 int vsp_set_option(vsp_ctx* ctx, const char* name, int64_t value);
 
 /* Measured dense FP64 FMA throughput of `device` in TFLOP/s (the denominator of the

@@ -573,7 +573,8 @@ class Engine:
                 "rem_kernel": ("none", "br1024", "br1024p", "br_lat")[int(o[3])]}
 
     def set_option(self, name: str, value: int):
-        """Engine tuning option (vsp_set_option): "lat_tasks" (1|2)."""
+        """Engine tuning option (vsp_set_option): "lat_tasks" (1|2), "ram_overlap",
+        "iks_gemm", "br_pair" (0|1), "iks_split" (split-K factor, 0 = automatic)."""
         _check(lib().vsp_set_option(self.h, name.encode(), int(value)))
 
     def counters(self) -> dict:

@@ -272,6 +272,7 @@ struct vsp_ctx {
     // key switching as an INT8 tensor-core GEMM (iks_gemm.cuh): the key in signed-byte
     // planes, cuBLASLt handle, selector / product scratch; option "iks_gemm"
     bool iks_gemm = true;
+    int iks_split = 0;  // option "iks_split": split-K factor of the key-switch GEMM (0: auto)
     // partial blind-rotation waves on br1024p_kernel (two warps per task); option "br_pair"
     bool br_pair = true;
     int8_t* d_k4t = nullptr;
@@ -833,11 +834,17 @@ bool iks_gemm_on(const vsp_ctx* c, int Gl)
 // tiles -- ~10 CTAs on 148 SMs, each streaming a 24,576-deep slice of the 62 MB key.  The
 // K dimension is cut into nsplit strided batches (partial products C_b, summed mod 2^32 by
 // the epilogue: the planes recombine mod 2^32, so wrapped int32 partial sums stay exact).
-int iks_nsplit(int Mpad)
+// A split must divide K_ = 24,576 into slices that keep the IMMA operand alignment
+// (multiples of 16 bytes).
+bool iks_split_valid(int s) { return s >= 1 && s <= 64 && kIksGemmK % s == 0 && (kIksGemmK / s) % 16 == 0; }
+
+int iks_nsplit(const vsp_ctx* c, int Mpad)
 {
     static const int forced = getenv("VSP_IKS_SPLIT") ? atoi(getenv("VSP_IKS_SPLIT")) : 0;
-    if (forced > 0)
+    if (forced > 0 && iks_split_valid(forced))
         return forced;
+    if (c->iks_split > 0)
+        return c->iks_split;
     // measured (B200, n = 630): 140 key switches 0.075 / 0.050 / 0.044 / 0.052 ms at
     // 1 / 2 / 4 / 8 splits; 4,096: 0.272 / 0.251 / 0.273 ms at 1 / 2 / 4
     return Mpad <= 512 ? 4 : 2;
@@ -917,7 +924,7 @@ void launch_iks(vsp_ctx* c, const uint32_t* d_trlwe, const int2* d_gtask, const 
     const Params& p = c->p;
     if (iks_gemm_on(c, Gl)) {
         const int Mpad = (Gl + 15) / 16 * 16;
-        const int nsplit = iks_nsplit(Mpad);
+        const int nsplit = iks_nsplit(c, Mpad);
         int8_t* S = c->iks_S.as<int8_t>((size_t)Mpad * kIksGemmK);
         int32_t* C = c->iks_C.as<int32_t>((size_t)Mpad * c->k4_npad * nsplit);
         timed(c, "iks", st, [&] {
@@ -2956,6 +2963,11 @@ int vsp_set_option(vsp_ctx* c, const char* name, int64_t value)
         }
         else if (k == "br_pair") {
             c->br_pair = value != 0;
+        }
+        else if (k == "iks_split") {
+            if (value != 0 && !iks_split_valid((int)value))
+                throw std::invalid_argument("iks_split must divide 24576 into multiples of 16");
+            c->iks_split = (int)value;
         }
         else {
             throw std::invalid_argument("unknown option: " + k);

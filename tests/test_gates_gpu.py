@@ -356,6 +356,31 @@ def test_int8_gemm_key_switch_equals_tensor_free(prod, G):
         assert np.array_equal(ks[i], o.identity_key_switch(lvl1[i]))
 
 
+@pytest.mark.parametrize("G", [70, 1200])
+def test_int8_gemm_split_k_equals_unsplit(prod, G):
+    """Split-K key-switch GEMM (K_ = 24,576 cut into strided batches whose int32 partial
+    products the epilogue sums mod 2^32): every split factor gives the same words,
+    including a non-power-of-two split and the automatic choice."""
+    e, _ = prod
+    rng = np.random.default_rng(950 + G)
+    k = oracle_keys("tfhe-80", 20200729, False)
+    p = vsp.ParameterSet("tfhe-80")
+    kid = rng.integers(0, len(GATE_KINDS), G).astype(np.int32)
+    bits = rng.integers(0, 2, size=(G, 3)).astype(np.uint8)
+    ins = vsp.encrypt(p, k["lv0"], bits.reshape(-1), 951 + G).reshape(G, 3, p.n + 1)
+    outs = []
+    try:
+        for s in (1, 3, 4, 8, 0):
+            e.set_option("iks_split", s)
+            outs.append(e.hom_gate_batch(kid, ins))
+    finally:
+        e.set_option("iks_split", 0)
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+    with pytest.raises(ValueError):
+        e.set_option("iks_split", 5)  # 24,576 / 5 is not an integer
+
+
 @pytest.mark.parametrize("G", [300, 4096])
 def test_two_warps_per_task_partial_wave_equals_one(prod, G):
     """br1024p_kernel (partial waves with two warps per task: a single W=3 launch for 300
