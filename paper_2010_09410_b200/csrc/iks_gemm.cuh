@@ -84,32 +84,49 @@ __global__ void __launch_bounds__(256) iks_gemm_selectors_kernel(
 // out[glist[gi]] = (0, ..., 0, b') - sum_b 256^b C[gi][b (n+1) + kk]  (mod 2^32), with b'
 // the extracted b (MUX: both plus mu, ops.cpp:886-892) exactly as iks_init_kernel.
 // Split-K: the nsplit partial products C_b = C + b * cstride are summed mod 2^32 first.
-__global__ void iks_gemm_epilogue_kernel(const int32_t* __restrict__ C, int npad, int nsplit,
-                                         size_t cstride,
-                                         const uint32_t* __restrict__ trlwe, const int2* __restrict__ gtask,
-                                         const int* __restrict__ glist, const int* __restrict__ seidx,
-                                         uint32_t* __restrict__ out, int n, int N)
+// Grid (key switches, coordinate chunks of 128): one coordinate per thread, its 4 x nsplit
+// partial words loaded together (one round trip; a per-gate loop over the coordinates
+// serialised ~5 of them).
+__global__ void __launch_bounds__(128) iks_gemm_epilogue_kernel(
+    const int32_t* __restrict__ C, int npad, int nsplit, size_t cstride,
+    const uint32_t* __restrict__ trlwe, const int2* __restrict__ gtask,
+    const int* __restrict__ glist, const int* __restrict__ seidx, uint32_t* __restrict__ out,
+    int n, int N)
 {
     const int gi = blockIdx.x;
+    const int kk = blockIdx.y * 128 + threadIdx.x;
+    if (kk > n)
+        return;
     const int gate = glist[gi];
-    const int2 tt = gtask[gate];
-    const int se = seidx ? seidx[gate] : 0;
     const int32_t* c = C + (size_t)gi * npad;
-    for (int kk = threadIdx.x; kk <= n; kk += blockDim.x) {
-        uint32_t v = 0;
-        if (kk == n) {
-            v = trlwe[(size_t)tt.x * 2 * N + N + se];
-            if (tt.y >= 0)
-                v += trlwe[(size_t)tt.y * 2 * N + N + se] + kMu32;
-        }
-        uint32_t s = 0;
+    uint32_t v = 0;
+    if (kk == n) {
+        const int2 tt = gtask[gate];
+        const int se = seidx ? seidx[gate] : 0;
+        v = trlwe[(size_t)tt.x * 2 * N + N + se];
+        if (tt.y >= 0)
+            v += trlwe[(size_t)tt.y * 2 * N + N + se] + kMu32;
+    }
+    uint32_t s = 0;
+    if (nsplit == 4) {
+        uint32_t w[4][4];
+#pragma unroll
+        for (int b = 0; b < 4; b++)
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+                w[b][q] = (uint32_t)__ldg(c + (size_t)b * cstride + (size_t)q * (n + 1) + kk);
+#pragma unroll
+        for (int b = 0; b < 4; b++)
+            s += w[b][0] + (w[b][1] << 8) + (w[b][2] << 16) + (w[b][3] << 24);
+    }
+    else {
         for (int b = 0; b < nsplit; b++) {
             const int32_t* cb = c + (size_t)b * cstride;
             s += (uint32_t)cb[kk] + ((uint32_t)cb[(n + 1) + kk] << 8) +
                  ((uint32_t)cb[2 * (n + 1) + kk] << 16) + ((uint32_t)cb[3 * (n + 1) + kk] << 24);
         }
-        out[(size_t)gate * (n + 1) + kk] = v - s;
     }
+    out[(size_t)gate * (n + 1) + kk] = v - s;
 }
 
 }  // namespace vsp

@@ -894,13 +894,46 @@ void iks_gemm_run(vsp_ctx* c, const int8_t* S, int Mpad, int32_t* C, cudaStream_
             lt_check(cublasLtMatmulPreferenceCreate(&pref), "preference");
             lt_check(cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES,
                                                           &ws_bytes, sizeof ws_bytes), "workspace");
-            cublasLtMatmulHeuristicResult_t h{};
+            // the heuristic's first choice is tuned for large M; time its top candidates
+            // once per shape (a narrow level's M ~ 150 is one row of 256-wide tiles)
+            cublasLtMatmulHeuristicResult_t hs[8];
             int found = 0;
-            lt_check(cublasLtMatmulAlgoGetHeuristic(c->lt, desc, la, lb, lc, lc, pref, 1, &h, &found),
+            lt_check(cublasLtMatmulAlgoGetHeuristic(c->lt, desc, la, lb, lc, lc, pref, 8, hs, &found),
                      "heuristic");
             if (found < 1)
                 throw std::runtime_error("cuBLASLt: no int8 GEMM algorithm for the key switch");
-            it = c->lt_algo.emplace(Mpad * 64 + nsplit, h.algo).first;
+            int best = 0;
+            if (found > 1) {
+                cudaEvent_t e0, e1;
+                VSP_CUDA_CHECK(cudaEventCreate(&e0));
+                VSP_CUDA_CHECK(cudaEventCreate(&e1));
+                float best_ms = 1e30f;
+                const int32_t one = 1, zero = 0;
+                for (int k = 0; k < found; k++) {
+                    if (hs[k].state != CUBLAS_STATUS_SUCCESS || hs[k].workspaceSize > ws_bytes)
+                        continue;
+                    auto run = [&] {
+                        return cublasLtMatmul(c->lt, desc, &one, c->d_k4t, la, S, lb, &zero, C, lc, C,
+                                              lc, &hs[k].algo, ws, ws_bytes, st);
+                    };
+                    if (run() != CUBLAS_STATUS_SUCCESS)
+                        continue;
+                    VSP_CUDA_CHECK(cudaEventRecord(e0, st));
+                    for (int r = 0; r < 3; r++)
+                        run();
+                    VSP_CUDA_CHECK(cudaEventRecord(e1, st));
+                    VSP_CUDA_CHECK(cudaEventSynchronize(e1));
+                    float ms = 0.f;
+                    VSP_CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+                    if (ms < best_ms) {
+                        best_ms = ms;
+                        best = k;
+                    }
+                }
+                cudaEventDestroy(e0);
+                cudaEventDestroy(e1);
+            }
+            it = c->lt_algo.emplace(Mpad * 64 + nsplit, hs[best].algo).first;
         }
         const int32_t one = 1, zero = 0;
         lt_check(cublasLtMatmul(c->lt, desc, &one, c->d_k4t, la, S, lb, &zero, C, lc, C, lc,
@@ -932,7 +965,8 @@ void launch_iks(vsp_ctx* c, const uint32_t* d_trlwe, const int2* d_gtask, const 
                                                           (int)p.N1);
             VSP_CUDA_CHECK(cudaGetLastError());
             iks_gemm_run(c, S, Mpad, C, st, nsplit);
-            iks_gemm_epilogue_kernel<<<Gl, 128, 0, st>>>(C, c->k4_npad, nsplit, (size_t)Mpad * c->k4_npad,
+            iks_gemm_epilogue_kernel<<<dim3(Gl, (unsigned)((p.n + 1 + 127) / 128)), 128, 0, st>>>(
+                                                         C, c->k4_npad, nsplit, (size_t)Mpad * c->k4_npad,
                                                          d_trlwe, d_gtask, d_glist, d_seidx, d_out,
                                                          (int)p.n, (int)p.N1);
             VSP_CUDA_CHECK(cudaGetLastError());
