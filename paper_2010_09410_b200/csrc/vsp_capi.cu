@@ -570,9 +570,9 @@ void launch_br2(vsp_ctx* c, const uint32_t* d_lwe, int ninputs, const uint64_t* 
 // the inputs of wave k + 1 while wave k runs.
 // Launch plan of a level-1 blind rotation of T tasks (FFT path), from a cost model of
 // measured wave times at n = 630 (ms per wave; scripts/br_occupancy.py, scripts/br_ab.py):
-//   br1024, W tasks per SM (one warp per task):  5.7 5.7 5.9 6.5 8.3 8.7 8.8 8.7
-//   br1024p, W <= 4 tasks per SM (two warps per task): 4.3 4.3 4.32 4.59
-//   br_lat, one task per SM (four warps):       1.96
+//   br1024, W tasks per SM (one warp per task):  5.87 5.71 5.84 6.02 7.70 7.72 7.88 7.97
+//   br1024p, W <= 4 tasks per SM (two warps per task): 4.3 4.3 4.31 4.62
+//   br_lat, one task per SM (four warps):       1.63 (br_lat2, two per SM: 3.21)
 // Every task costs the same and one CTA runs per SM, so a partial wave costs a whole one.
 // Candidates: one launch of W tasks per SM (ceil(T / (SMs W)) waves), or k whole W = 8
 // waves + the remainder at its own best (latency kernel when it fits two of its waves);
@@ -587,12 +587,13 @@ struct BrPlan {
 
 double br_wave_ms(int W, bool pair)
 {
-    static const double t[9] = {0, 5.7, 5.7, 5.9, 6.5, 8.3, 8.7, 8.8, 8.7};
-    static const double tp[5] = {0, 4.3, 4.3, 4.32, 4.59};
+    // session-3 calibration (scripts/calib_waves.py, profiles/r02_calib_waves.json)
+    static const double t[9] = {0, 5.87, 5.71, 5.84, 6.02, 7.70, 7.72, 7.88, 7.97};
+    static const double tp[5] = {0, 4.3, 4.3, 4.31, 4.62};
     return (pair && W <= 4) ? tp[W] : t[W];
 }
 
-constexpr double kLatWaveMs = 1.96;
+constexpr double kLatWaveMs = 1.63;  // a 148-task level (149 tasks: two waves, 3.23 ms)
 
 // best single launch for T tasks: (cost, W)
 std::pair<double, int> br_best_single(long T, int sms, bool pair)
