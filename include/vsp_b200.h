@@ -184,6 +184,12 @@ vsp_netlist* vsp_netlist_create(vsp_ctx* ctx, int32_t net_count, int32_t cells,
 void vsp_netlist_destroy(vsp_netlist* nl);
 /* out6: dag nodes, dffs, gMax, depth, rom cell, ram cell; levels[dag node] optional. */
 int vsp_netlist_info(vsp_netlist* nl, int32_t* out6, int32_t* levels);
+/* The level each DAG node is EVALUATED in (same order as vsp_netlist_info's levels): the
+ * ASAP level, except gates with slack moved one level later out of a level that holds
+ * more blind-rotation tasks than the device has SMs (a 149-task level would cost two
+ * latency waves).  Results are unchanged: every gate still runs after all its producers
+ * and before all its consumers.  No reference counterpart (scheduling only). */
+int vsp_netlist_launch_levels(vsp_netlist* nl, int32_t* levels);
 /* Evaluator::setInput (engine.hpp:160-163) by index into input_nets. */
 int vsp_netlist_set_input(vsp_netlist* nl, int32_t input_index, const uint32_t* tlwe);
 /* Evaluator::output (engine.hpp:165-176) for any net. */

@@ -58,6 +58,7 @@ struct vsp_netlist {
     std::vector<int> kind, id, in_off, in_nets, out_off, out_nets;
     // DAG (buildDag, netlist.cpp:348-432)
     std::vector<int> dag_cells, level, height, dff_cells;
+    std::vector<int> launch_level;  // per DAG node: the level it is evaluated in (build_dag)
     std::vector<int> node_of_cell;
     int rom_cell = -1, ram_cell = -1, gmax = 0, depth = 0;
     // per level: gate cells (kinds 0..9) and memory ports
@@ -234,13 +235,72 @@ void build_dag(vsp_netlist* nl)
     for (int w : width)
         nl->gmax = std::max(nl->gmax, w);
     nl->depth = maxLevel + 1;
+    // Launch schedule: the ASAP levels (nl->level, the reference's buildDag) with gates that
+    // have slack moved one level later when their level holds more blind-rotation tasks
+    // than one wave of the latency kernel (one task per SM): a 149-task level costs two
+    // 630-step waves, 148 tasks one.  A gate moves from L to L + 1 only if every consumer
+    // sits at L + 2 or later (DFF inputs and module outputs are read after the cycle), so
+    // each gate still sees the same input ciphertexts and computes the same output words.
+    std::vector<int> slev(nl->level);
+    {
+        auto tasks_of = [&](int node) {
+            const int k = nl->kind[nl->dag_cells[node]];
+            return k == cMux ? 2 : (k == cNot || k > cXor) ? 0 : 1;
+        };
+        std::vector<std::vector<int>> at(std::max(nl->depth, 0));
+        for (int node = 0; node < n; node++)
+            if (nl->kind[nl->dag_cells[node]] <= cXor)
+                at[slev[node]].push_back(node);
+        // Only when the level can get down to one wave, and without pushing the next level
+        // out of the latency kernel's two-wave range; the next level then sheds its own
+        // excess the same way (the last level keeps what it receives).
+        const int cap = nl->ctx->sms;
+        auto level_tasks = [&](int L) {
+            int T = 0;
+            for (int node : at[L])
+                T += tasks_of(node);
+            return T;
+        };
+        for (int L = 0; L + 1 < nl->depth; L++) {
+            int T = level_tasks(L);
+            if (T <= cap || T > 2 * cap)
+                continue;
+            auto movable = [&](int node) {
+                if (tasks_of(node) == 0)
+                    return false;
+                for (int cns : consumers[node])
+                    if (slev[cns] < L + 2)
+                        return false;
+                return true;
+            };
+            int M = 0;
+            for (int node : at[L])
+                M += movable(node) ? tasks_of(node) : 0;
+            int Tn = level_tasks(L + 1);
+            if (T - M > cap || Tn + (T - cap) > 2 * cap)
+                continue;
+            std::vector<int> keep;
+            for (int node : at[L]) {
+                if (T > cap && movable(node)) {
+                    slev[node] = L + 1;
+                    at[L + 1].push_back(node);
+                    T -= tasks_of(node);
+                }
+                else {
+                    keep.push_back(node);
+                }
+            }
+            at[L].swap(keep);
+        }
+    }
+    nl->launch_level = slev;
     nl->level_gates.assign(std::max(nl->depth, 0), {});
     nl->level_mem.assign(std::max(nl->depth, 0), {});
     for (int node = 0; node < n; node++) {
         const int c = nl->dag_cells[node];
         const int k = nl->kind[c];
         if (k <= cXor)
-            nl->level_gates[nl->level[node]].push_back(c);
+            nl->level_gates[slev[node]].push_back(c);
         else if (k == cRom || k == cRam)
             nl->level_mem[nl->level[node]].push_back(c);
         else

@@ -2581,6 +2581,14 @@ int vsp_netlist_info(vsp_netlist* nl, int32_t* out6, int32_t* levels)
     });
 }
 
+int vsp_netlist_launch_levels(vsp_netlist* nl, int32_t* levels)
+{
+    return guard([&] {
+        for (size_t i = 0; i < nl->launch_level.size(); i++)
+            levels[i] = nl->launch_level[i];
+    });
+}
+
 int vsp_netlist_set_input(vsp_netlist* nl, int32_t input_index, const uint32_t* tlwe)
 {
     return guard([&] {

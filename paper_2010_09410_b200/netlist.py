@@ -277,6 +277,7 @@ def _bind():
     L.vsp_netlist_create.argtypes = [vp, i32, i32, vp, vp, vp, vp, vp, vp, vp, i32]
     L.vsp_netlist_destroy.argtypes = [vp]
     L.vsp_netlist_info.argtypes = [vp, vp, vp]
+    L.vsp_netlist_launch_levels.argtypes = [vp, vp]
     L.vsp_netlist_set_input.argtypes = [vp, i32, vp]
     L.vsp_netlist_get_net.argtypes = [vp, i32, vp]
     L.vsp_netlist_dff.argtypes = [vp, vp, vp]
@@ -351,6 +352,13 @@ class Evaluator:
         lv = np.zeros(max(self.dag_nodes, 1), np.int32)
         info = np.zeros(6, np.int32)
         _check(lib().vsp_netlist_info(self.h, _ptr(info), _ptr(lv)))
+        return lv[:self.dag_nodes]
+
+    def launch_levels(self) -> np.ndarray:
+        """The level each DAG node is evaluated in (vsp_netlist_launch_levels): ASAP, with
+        slack gates moved out of levels wider than one latency wave."""
+        lv = np.zeros(max(self.dag_nodes, 1), np.int32)
+        _check(lib().vsp_netlist_launch_levels(self.h, _ptr(lv)))
         return lv[:self.dag_nodes]
 
     @staticmethod

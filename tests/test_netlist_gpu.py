@@ -113,6 +113,86 @@ def test_runner_matches_reference_evaluator_testdet():
     assert ev.cycle == 2
 
 
+def _launch_schedule_ok(nl, ev, sms):
+    """Launch levels vs the ASAP levels: never earlier, every gate before all of its
+    consumers (gates and memory ports), memory ports unmoved.  Returns the latency-kernel
+    waves (ceil(tasks / SMs) per level) of the ASAP and of the launch schedule."""
+    nodes = [c for c in nl.cells if c.kind != "DFF"]
+    asap, launch = ev.levels(), ev.launch_levels()
+    assert np.all(launch >= asap) and launch.max() == asap.max()
+    producer = {b: i for i, c in enumerate(nodes) for b in c.outputs}
+    for i, c in enumerate(nodes):
+        for b in c.inputs:
+            if b in producer:
+                assert launch[producer[b]] < launch[i], (producer[b], i)
+        if c.kind in ("ROM", "RAM", "CONST0", "CONST1"):
+            assert launch[i] == asap[i]
+
+    def waves(lv):
+        t = {}
+        for i, c in enumerate(nodes):
+            cost = 2 if c.kind == "MUX" else 0 if c.kind in ("NOT", "ROM", "RAM", "CONST0", "CONST1") else 1
+            t[lv[i]] = t.get(lv[i], 0) + cost
+        return sum(-(-x // sms) for x in t.values())
+    return waves(asap), waves(launch)
+
+
+def test_level_balancing_schedule_matches_reference_evaluator_testdet():
+    """Levels wider than one latency wave (more blind-rotation tasks than SMs) hand their
+    gates with slack to the next level (vsp_netlist_launch_levels); the runner's DFF state,
+    outputs and RAM stay word-for-word equal to the reference Evaluator<TfheBackend>,
+    which evaluates the ASAP levels."""
+    if not pyoracle.available("ref"):
+        pytest.skip("reference not built")
+    seed = 515253
+    r = CpuTfhe("ref", "test-det", seed=seed)
+    r.keygen(True)
+    e = vsp.Engine("test-det")
+    e.upload_keys(oracle_keys("test-det", seed, True))
+    nl = N.synthetic_netlist(seed=3, scale=0.134, levels=4, dffs=48, ram=(3, 4))
+    ev = N.Evaluator(nl, e)
+    w_asap, w_launch = _launch_schedule_ok(nl, ev, e.sms)
+    assert w_launch <= w_asap
+    if e.sms == 148:
+        assert w_launch < w_asap, (w_asap, w_launch)
+    rev = RefEval(r, N.netlist_to_json(nl))
+    rng = np.random.default_rng(4)
+    v, w = 3, 4
+    ram = r.encrypt_ram(words_to_image([int(x) for x in rng.integers(0, 16, 8)], v, w), v, w)
+    ev.set_ram(ram, v, w)
+    rev.set_ram(ram, v, w)
+    luts = r.encrypt_rom(rng.integers(0, 256, 512).astype(np.uint8))
+    ev.set_rom(luts, 512)
+    rev.set_rom(luts, 512)
+    for i in range(len(nl.inputs[0].bits)):
+        ct = r.encrypt(int(rng.integers(0, 2)))
+        ev.set_input("in", i, ct)
+        rev.set_input("in", i, ct)
+    init = np.stack([r.encrypt(int(b)) for b in rng.integers(0, 2, ev.n_dffs)])
+    ev.set_dff_state_raw(init)
+    rev.set_dff(init)
+    for cyc in range(2):
+        ev.run(1)
+        rev.run(1)
+        assert np.array_equal(ev.dff_state(), rev.dff()), f"DFF state differs at cycle {cyc}"
+        for k in range(16):
+            assert np.array_equal(ev.output("out", k), rev.output("out", k))
+    assert np.array_equal(ev.ram(), rev.get_ram(ram.shape))
+
+
+def test_level_balancing_on_the_bench_netlist():
+    """The bench's cycle netlist (one ASAP level of 149 tasks) launches every level in a
+    single latency wave on a 148-SM B200."""
+    e = vsp.Engine("test-det")
+    e.upload_keys(oracle_keys("test-det", 515253, True))
+    nl = N.synthetic_netlist(seed=1, levels=32)
+    ev = N.Evaluator(nl, e)
+    w_asap, w_launch = _launch_schedule_ok(nl, ev, e.sms)
+    assert w_launch <= w_asap
+    if e.sms == 148:
+        assert (w_asap, w_launch) == (ev.depth + 1, ev.depth), (w_asap, w_launch)
+
+
 def test_runner_backend_equivalence_tfhe80():
     """Decrypted TFHE outputs == PlainBackend outputs every cycle (no memory ports)."""
     p = vsp.ParameterSet("tfhe-80")
