@@ -59,6 +59,7 @@ struct vsp_netlist {
     // DAG (buildDag, netlist.cpp:348-432)
     std::vector<int> dag_cells, level, height, dff_cells;
     std::vector<int> launch_level;  // per DAG node: the level it is evaluated in (build_dag)
+    std::vector<int> level_tasks;   // blind-rotation tasks of each launch level's gates
     std::vector<int> node_of_cell;
     int rom_cell = -1, ram_cell = -1, gmax = 0, depth = 0;
     // per level: gate cells (kinds 0..9) and memory ports
@@ -308,10 +309,12 @@ void build_dag(vsp_netlist* nl)
     }
     const int sms = nl->ctx->sms;
     nl->max_level_ctas = 0;
+    nl->level_tasks.clear();
     for (const auto& lg : nl->level_gates) {
         int tasks = 0;
         for (int cell : lg)
             tasks += nl->kind[cell] == cMux ? 2 : nl->kind[cell] == cNot ? 0 : 1;
+        nl->level_tasks.push_back(tasks);
         const int ctas = tasks <= 2 * sms ? (tasks > 64 ? (tasks + 1) / 2 : tasks) : sms;
         nl->max_level_ctas = std::max(nl->max_level_ctas, ctas);
     }
@@ -428,6 +431,25 @@ void run_cycle_body(vsp_netlist* nl, cudaStream_t st)
         c->launches++;
     }
     VSP_CUDA_CHECK(cudaGetLastError());
+    // write-bar backfill: idle latency-wave slots of the levels after L (one GPU, FFT path,
+    // write unit inline); levels without blind rotations launch nothing and take none
+    c->bar_total = c->bar_done = 0;
+    struct BarReset {  // no deferred write bar outlives the cycle (also on an exception)
+        vsp_ctx* c;
+        ~BarReset() { c->bar_total = c->bar_done = c->bar_cap = 0; }
+    } bar_reset{c};
+    const bool backfill = c->p.fft && !sharded(c) && !c->defer_write_now;
+    auto spare_after = [&](int L) {
+        int cap = 0;
+        for (int l = L + 1; l < nl->depth; l++)
+            if (nl->level_tasks[l] >= 1 && nl->level_tasks[l] < c->sms)
+                cap += c->sms - nl->level_tasks[l];
+        return cap;
+    };
+    struct BarCap {  // bar_cap is open only while a RAM port of this cycle runs
+        vsp_ctx* c;
+        ~BarCap() { c->bar_cap = 0; }
+    };
     for (int L = 0; L < nl->depth; L++) {
         const auto& gates = nl->level_gates[L];
         if (!gates.empty()) {
@@ -453,6 +475,9 @@ void run_cycle_body(vsp_netlist* nl, cudaStream_t st)
             c->launches++;
             VSP_CUDA_CHECK(cudaGetLastError());
         }
+        BarCap bar_guard{c};
+        if (backfill && !nl->level_mem[L].empty())
+            c->bar_cap = spare_after(L);
         if (nl->level_mem[L].size() == 2 && nl->has_rom && nl->has_ram) {
             run_mem_pair(nl, nl->level_mem[L], vals, st);
             continue;
@@ -492,6 +517,7 @@ void run_cycle_body(vsp_netlist* nl, cudaStream_t st)
             VSP_CUDA_CHECK(cudaGetLastError());
         }
     }
+    bar_flush(c, st);  // deferred write bars no later level took
     nl->table_valid = true;
     // synchronous DFF latch (engine.hpp:341-345): sample every D, then update all Qs
     if (!nl->dff_d.empty()) {

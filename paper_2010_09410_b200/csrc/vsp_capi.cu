@@ -287,6 +287,14 @@ struct vsp_ctx {
     // run two tasks per SM); joined before the next access to the RAM image.
     bool ram_overlap = false;
     bool defer_write_now = false;  // set by the runner around a cycle
+    // Write-bar backfill (runner, one GPU): the RAM write unit leaves up to bar_cap of its
+    // blind rotations (the last cells) to the later narrow levels of the cycle, whose
+    // latency launches have idle SMs; bar_lwe holds their key-switched inputs, bar_dst the
+    // first deferred RAM cell.  bar_cap > 0 only while the runner evaluates a RAM port.
+    int bar_cap = 0;
+    int bar_total = 0, bar_done = 0;
+    uint32_t* bar_dst = nullptr;
+    DevBuf bar_lwe;
     int w_ctas = 0;
     cudaStream_t wstream = nullptr;
     cudaEvent_t ev_wfork = nullptr, ev_wdone = nullptr;
@@ -1151,6 +1159,8 @@ struct HostIO {
     uint32_t* out;
 };
 
+int bar_take(vsp_ctx* c, int T);
+
 void hom_gate_dev(vsp_ctx* c, const int32_t* kinds, const uint32_t* d_in, uint32_t* d_out,
                   size_t G, cudaStream_t st, const HostIO* io = nullptr)
 {
@@ -1168,9 +1178,16 @@ void hom_gate_dev(vsp_ctx* c, const int32_t* kinds, const uint32_t* d_in, uint32
     if (!pl.glist.empty())
         VSP_CUDA_CHECK(cudaMemcpyAsync(d_glist, pl.glist.data(), pl.glist.size() * sizeof(int),
                                        cudaMemcpyHostToDevice, st));
-    uint32_t* d_tasks = c->tasks.as<uint32_t>((size_t)std::max(pl.T, 1) * (p.n + 1));
-    uint32_t* d_trlwe = c->trlwe.as<uint32_t>((size_t)std::max(pl.T, 1) * 2 * p.N1);
+    // write-bar backfill (runner only: no host I/O): deferred RAM-cell blind rotations in
+    // this level's idle SMs
+    const int kbar = io ? 0 : bar_take(c, pl.T);
+    uint32_t* d_tasks = c->tasks.as<uint32_t>((size_t)std::max(pl.T + kbar, 1) * (p.n + 1));
+    uint32_t* d_trlwe = c->trlwe.as<uint32_t>((size_t)std::max(pl.T + kbar, 1) * 2 * p.N1);
     const size_t w = p.n + 1;
+    if (kbar)
+        VSP_CUDA_CHECK(cudaMemcpyAsync(d_tasks + (size_t)pl.T * w,
+                                       c->bar_lwe.as<uint32_t>(0) + (size_t)c->bar_done * w,
+                                       (size_t)kbar * w * 4, cudaMemcpyDeviceToDevice, st));
     // gates [g0, g1): upload (host pipeline) and linear combinations
     auto prep = [&](size_t g0, size_t g1) {
         if (g1 <= g0)
@@ -1258,8 +1275,14 @@ void hom_gate_dev(vsp_ctx* c, const int32_t* kinds, const uint32_t* d_in, uint32
     // the INT8-GEMM key switch of the whole batch after the last wave is cheaper than the
     // tensor-free one forked under the remainder wave (which then has the SMs to itself)
     const bool fork = !iks_gemm_on(c, Gl);
-    launch_br(c, d_tasks, d_trlwe, pl.T, st, fork ? std::function<void(int)>(fork_iks)
-                                                  : std::function<void(int)>(), before_part);
+    launch_br(c, d_tasks, d_trlwe, pl.T + kbar, st, fork ? std::function<void(int)>(fork_iks)
+                                                         : std::function<void(int)>(), before_part);
+    if (kbar) {
+        VSP_CUDA_CHECK(cudaMemcpyAsync(c->bar_dst + (size_t)c->bar_done * 2 * p.N1,
+                                       d_trlwe + (size_t)pl.T * 2 * p.N1,
+                                       (size_t)kbar * 2 * p.N1 * 4, cudaMemcpyDeviceToDevice, st));
+        c->bar_done += kbar;
+    }
     launch_iks(c, d_trlwe, d_gtask, d_glist + k1, Gl - k1, d_out, st);
     if (forked)
         VSP_CUDA_CHECK(cudaStreamWaitEvent(st, c->ev_join, 0));
@@ -1594,7 +1617,46 @@ void ram_write_unit_dev(vsp_ctx* c, uint32_t* d_ram, int v, int w, const uint32_
         return;
     }
     iks_of_trlwes(c, chain_out, (int)cells, nullptr, lw, st);
-    launch_br(c, lw, d_ram, (int)cells, st);
+    int now = (int)cells;
+    if (c->bar_cap > 0 && p.fft && c->bar_total == 0) {
+        // the remainder after the whole waves goes (up to bar_cap tasks) to the idle SMs of
+        // the cycle's later narrow levels; what is left runs here, one latency wave
+        const int full = br_plan(c, T).full;
+        const int K = std::min(T - full, c->bar_cap);
+        if (full > 0 && K > 0) {
+            now = T - K;
+            uint32_t* bl = c->bar_lwe.as<uint32_t>((size_t)K * n1);
+            VSP_CUDA_CHECK(cudaMemcpyAsync(bl, lw + (size_t)now * n1, (size_t)K * n1 * 4,
+                                           cudaMemcpyDeviceToDevice, st));
+            c->bar_total = K;
+            c->bar_done = 0;
+            c->bar_dst = d_ram + (size_t)now * cw;
+        }
+    }
+    launch_br(c, lw, d_ram, now, st);
+}
+
+// Backfill: the next k deferred write-bar inputs into task slots [T, T + k) of a level's
+// launch (d_tasks), then (after the launch) their outputs into the RAM cells.
+int bar_take(vsp_ctx* c, int T)
+{
+    const int left = c->bar_total - c->bar_done;
+    if (left <= 0 || T < 1 || T >= c->sms)
+        return 0;
+    return std::min(left, c->sms - T);
+}
+
+// Flush: blind rotations of the deferred cells no level took (end of the cycle).
+void bar_flush(vsp_ctx* c, cudaStream_t st)
+{
+    const int left = c->bar_total - c->bar_done;
+    if (left > 0) {
+        const size_t n1 = c->p.n + 1, cw = 2 * (size_t)c->p.N1;
+        launch_br(c, c->bar_lwe.as<uint32_t>(0) + (size_t)c->bar_done * n1,
+                  c->bar_dst + (size_t)c->bar_done * cw, left, st);
+    }
+    c->bar_total = c->bar_done = 0;
+    c->bar_dst = nullptr;
 }
 
 void check_ram_geometry(int v, int w)
