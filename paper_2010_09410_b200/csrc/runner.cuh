@@ -431,7 +431,7 @@ void run_cycle_body(vsp_netlist* nl, cudaStream_t st)
         c->launches++;
     }
     VSP_CUDA_CHECK(cudaGetLastError());
-    // write-bar backfill: idle latency-wave slots of the levels after L (one GPU, FFT path,
+    // write-bar backfill: idle latency-wave slots of levels L.. (one GPU, FFT path,
     // write unit inline); levels without blind rotations launch nothing and take none
     c->bar_total = c->bar_done = 0;
     struct BarReset {  // no deferred write bar outlives the cycle (also on an exception)
@@ -439,9 +439,9 @@ void run_cycle_body(vsp_netlist* nl, cudaStream_t st)
         ~BarReset() { c->bar_total = c->bar_done = c->bar_cap = 0; }
     } bar_reset{c};
     const bool backfill = c->p.fft && !sharded(c) && !c->defer_write_now;
-    auto spare_after = [&](int L) {
+    auto spare_from = [&](int L) {
         int cap = 0;
-        for (int l = L + 1; l < nl->depth; l++)
+        for (int l = L; l < nl->depth; l++)
             if (nl->level_tasks[l] >= 1 && nl->level_tasks[l] < c->sms)
                 cap += c->sms - nl->level_tasks[l];
         return cap;
@@ -450,37 +450,16 @@ void run_cycle_body(vsp_netlist* nl, cudaStream_t st)
         vsp_ctx* c;
         ~BarCap() { c->bar_cap = 0; }
     };
-    for (int L = 0; L < nl->depth; L++) {
-        const auto& gates = nl->level_gates[L];
-        if (!gates.empty()) {
-            const int G = (int)gates.size();
-            std::vector<int> gnets((size_t)G * 3, -1), onets(G);
-            std::vector<int32_t> kinds(G);
-            for (int g = 0; g < G; g++) {
-                const int cell = gates[g];
-                kinds[g] = nl->kind[cell];  // CellKind 0..9 == GateKind 0..9
-                for (int k = nl->in_off[cell], s = 0; k < nl->in_off[cell + 1]; k++, s++)
-                    gnets[(size_t)g * 3 + s] = nl->in_nets[k];
-                onets[g] = nl->out_nets[nl->out_off[cell]];
-            }
-            upload_ints(c, nl->nets_buf, gnets, st);
-            uint32_t* gin = nl->gin.as<uint32_t>((size_t)G * 3 * n1);
-            uint32_t* gout = nl->gout.as<uint32_t>((size_t)G * n1);
-            gather_tlwe_kernel<<<G * 3, 128, 0, st>>>(nl->nets_buf.as<int>(0), G * 3, vals, gin,
-                                                      (int)n);
-            c->launches++;
-            hom_gate_level_dev(c, kinds.data(), gin, gout, (size_t)G, st);  // sharded when world > 1
-            upload_ints(c, nl->nets_buf, onets, st);
-            scatter_tlwe_kernel<<<G, 128, 0, st>>>(nl->nets_buf.as<int>(0), G, gout, vals, (int)n);
-            c->launches++;
-            VSP_CUDA_CHECK(cudaGetLastError());
-        }
+    // Each level: its memory ports first, then its gates (same ASAP level, so neither
+    // reads the other's outputs): the level's gate launch can then take deferred write
+    // bars of its own RAM port.
+    auto run_mem = [&](int L) {
         BarCap bar_guard{c};
         if (backfill && !nl->level_mem[L].empty())
-            c->bar_cap = spare_after(L);
+            c->bar_cap = spare_from(L);
         if (nl->level_mem[L].size() == 2 && nl->has_rom && nl->has_ram) {
             run_mem_pair(nl, nl->level_mem[L], vals, st);
-            continue;
+            return;
         }
         for (int cell : nl->level_mem[L]) {
             std::vector<int> ins(nl->in_nets.begin() + nl->in_off[cell],
@@ -516,6 +495,36 @@ void run_cycle_body(vsp_netlist* nl, cudaStream_t st)
             c->launches++;
             VSP_CUDA_CHECK(cudaGetLastError());
         }
+    };
+    auto run_gates = [&](int L) {
+        const auto& gates = nl->level_gates[L];
+        if (!gates.empty()) {
+            const int G = (int)gates.size();
+            std::vector<int> gnets((size_t)G * 3, -1), onets(G);
+            std::vector<int32_t> kinds(G);
+            for (int g = 0; g < G; g++) {
+                const int cell = gates[g];
+                kinds[g] = nl->kind[cell];  // CellKind 0..9 == GateKind 0..9
+                for (int k = nl->in_off[cell], s = 0; k < nl->in_off[cell + 1]; k++, s++)
+                    gnets[(size_t)g * 3 + s] = nl->in_nets[k];
+                onets[g] = nl->out_nets[nl->out_off[cell]];
+            }
+            upload_ints(c, nl->nets_buf, gnets, st);
+            uint32_t* gin = nl->gin.as<uint32_t>((size_t)G * 3 * n1);
+            uint32_t* gout = nl->gout.as<uint32_t>((size_t)G * n1);
+            gather_tlwe_kernel<<<G * 3, 128, 0, st>>>(nl->nets_buf.as<int>(0), G * 3, vals, gin,
+                                                      (int)n);
+            c->launches++;
+            hom_gate_level_dev(c, kinds.data(), gin, gout, (size_t)G, st);  // sharded when world > 1
+            upload_ints(c, nl->nets_buf, onets, st);
+            scatter_tlwe_kernel<<<G, 128, 0, st>>>(nl->nets_buf.as<int>(0), G, gout, vals, (int)n);
+            c->launches++;
+            VSP_CUDA_CHECK(cudaGetLastError());
+        }
+    };
+    for (int L = 0; L < nl->depth; L++) {
+        run_mem(L);
+        run_gates(L);
     }
     bar_flush(c, st);  // deferred write bars no later level took
     nl->table_valid = true;
