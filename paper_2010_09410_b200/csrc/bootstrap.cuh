@@ -980,6 +980,52 @@ __global__ void gate_prep_kernel(const int* __restrict__ kinds, const uint32_t* 
     }
 }
 
+// The same, reading the gate inputs straight from the netlist runner's value table
+// (innet[3 g + s]: net of input s, -1 for none) and writing NOT outputs to their net.
+__global__ void gate_prep_idx_kernel(const int* __restrict__ kinds, const uint32_t* __restrict__ vals,
+                                     const int* __restrict__ innet, const int* __restrict__ onet,
+                                     const int2* __restrict__ gtask, uint32_t* __restrict__ tasks,
+                                     uint32_t* __restrict__ outvals, int G, int n)
+{
+    const int g = blockIdx.x;
+    if (g >= G)
+        return;
+    const int kind = kinds[g];
+    const int2 tt = gtask[g];
+    const size_t w = n + 1;
+    const int i0 = innet[3 * g], i1 = innet[3 * g + 1], i2 = innet[3 * g + 2];
+    const uint32_t* x = vals + (size_t)i0 * w;
+    const uint32_t* y = vals + (size_t)(i1 >= 0 ? i1 : i0) * w;
+    const uint32_t* z = vals + (size_t)(i2 >= 0 ? i2 : i0) * w;
+    const uint32_t mu = kMu32, nmu = 0u - kMu32;
+    int c0 = 1, c1 = 1;
+    uint32_t bias = nmu;
+    switch (kind) {
+    case kAnd: c0 = 1; c1 = 1; bias = nmu; break;
+    case kNand: c0 = -1; c1 = -1; bias = mu; break;
+    case kOr: c0 = 1; c1 = 1; bias = mu; break;
+    case kNor: c0 = -1; c1 = -1; bias = nmu; break;
+    case kXor: c0 = 2; c1 = 2; bias = 2 * mu; break;
+    case kXnor: c0 = -2; c1 = -2; bias = 2 * nmu; break;
+    case kAndNot: c0 = 1; c1 = -1; bias = nmu; break;
+    case kOrNot: c0 = 1; c1 = -1; bias = mu; break;
+    default: break;
+    }
+    for (int k = threadIdx.x; k <= n; k += blockDim.x) {
+        const uint32_t bk = (k == n) ? 1u : 0u;
+        if (kind == kNot) {
+            outvals[(size_t)onet[g] * w + k] = 0u - x[k];
+        }
+        else if (kind == kMux) {  // in = {sel, a, b}
+            tasks[(size_t)tt.x * w + k] = x[k] + y[k] + bk * nmu;
+            tasks[(size_t)tt.y * w + k] = z[k] - x[k] + bk * nmu;
+        }
+        else {
+            tasks[(size_t)tt.x * w + k] = (uint32_t)c0 * x[k] + (uint32_t)c1 * y[k] + bk * bias;
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Batched identity key switch (ops.cpp:651-679) fused with sampleExtract(.,0)
 // (ops.cpp:628-643) and the MUX level-1 sum (ops.cpp:886-892).
@@ -1007,9 +1053,12 @@ __device__ __forceinline__ void iks_level1_coef(const uint32_t* __restrict__ trl
         a += se_coef(trlwe + (size_t)tt.y * 2 * N, N, k, i);
 }
 
+// oidx (optional, every key-switch kernel): output row of gate g is oidx[g] instead of g
+// (the netlist runner writes straight into its value table, row = output net).
 __global__ void iks_init_kernel(const uint32_t* __restrict__ trlwe, const int2* __restrict__ gtask,
                                 const int* __restrict__ glist, const int* __restrict__ seidx,
-                                int Gl, uint32_t* __restrict__ out, int n, int N)
+                                int Gl, uint32_t* __restrict__ out, int n, int N,
+                                const int* __restrict__ oidx = nullptr)
 {
     const int gi = blockIdx.x;
     if (gi >= Gl)
@@ -1024,7 +1073,7 @@ __global__ void iks_init_kernel(const uint32_t* __restrict__ trlwe, const int2* 
             if (tt.y >= 0)
                 v += trlwe[(size_t)tt.y * 2 * N + N + se] + kMu32;
         }
-        out[(size_t)gate * (n + 1) + k] = v;
+        out[(size_t)(oidx ? oidx[gate] : gate) * (n + 1) + k] = v;
     }
 }
 
@@ -1032,7 +1081,8 @@ template <int BASEBITS, int GT, int KPT>
 __global__ void __launch_bounds__(256) iks_kernel(
     const uint32_t* __restrict__ trlwe, const int2* __restrict__ gtask,
     const int* __restrict__ glist, const int* __restrict__ seidx, int Gl,
-    const uint32_t* __restrict__ ksk, uint32_t* __restrict__ out, int n, int N, int t)
+    const uint32_t* __restrict__ ksk, uint32_t* __restrict__ out, int n, int N, int t,
+    const int* __restrict__ oidx = nullptr)
 {
     static_assert(GT * BASEBITS <= 64, "digit packing");
     constexpr uint32_t kMask = (1u << BASEBITS) - 1;
@@ -1115,7 +1165,7 @@ __global__ void __launch_bounds__(256) iks_kernel(
         for (int kk = 0; kk < KPT; kk++) {
             const int k = threadIdx.x + kk * 256;
             if (k <= n && acc[g][kk] != 0u)
-                atomicAdd(out + (size_t)gate * (n + 1) + k, 0u - acc[g][kk]);
+                atomicAdd(out + (size_t)(oidx ? oidx[gate] : gate) * (n + 1) + k, 0u - acc[g][kk]);
         }
     }
 }
@@ -1135,7 +1185,8 @@ template <int KPT, int GT>
 __global__ void __launch_bounds__(128) iks_b2_kernel(
     const uint32_t* __restrict__ trlwe, const int2* __restrict__ gtask,
     const int* __restrict__ glist, const int* __restrict__ seidx, int Gl,
-    const uint32_t* __restrict__ ksk, uint32_t* __restrict__ out, int n, int N)
+    const uint32_t* __restrict__ ksk, uint32_t* __restrict__ out, int n, int N,
+    const int* __restrict__ oidx = nullptr)
 {
     constexpr int T = 8;  // ksLen
     extern __shared__ __align__(16) uint16_t dig16[];  // [islice][GT]
@@ -1248,7 +1299,7 @@ __global__ void __launch_bounds__(128) iks_b2_kernel(
         for (int kk = 0; kk < KPT; kk++) {
             const int k = kbase + 32 * kk;
             if (k <= n && acc[g][kk] != 0u)
-                atomicAdd(out + (size_t)gate * rs + k, 0u - acc[g][kk]);  // RED.ADD
+                atomicAdd(out + (size_t)(oidx ? oidx[gate] : gate) * rs + k, 0u - acc[g][kk]);  // RED.ADD
         }
     }
 }

@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(128) iks_gemm_epilogue_kernel(
     const int32_t* __restrict__ C, int npad, int nsplit, size_t cstride,
     const uint32_t* __restrict__ trlwe, const int2* __restrict__ gtask,
     const int* __restrict__ glist, const int* __restrict__ seidx, uint32_t* __restrict__ out,
-    int n, int N)
+    int n, int N, const int* __restrict__ oidx = nullptr)
 {
     const int gi = blockIdx.x;
     const int kk = blockIdx.y * 128 + threadIdx.x;
@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(128) iks_gemm_epilogue_kernel(
                  ((uint32_t)cb[2 * (n + 1) + kk] << 16) + ((uint32_t)cb[3 * (n + 1) + kk] << 24);
         }
     }
-    out[(size_t)gate * (n + 1) + kk] = v - s;
+    out[(size_t)(oidx ? oidx[gate] : gate) * (n + 1) + kk] = v - s;
 }
 
 }  // namespace vsp

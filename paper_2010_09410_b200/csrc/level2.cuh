@@ -733,6 +733,116 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(256, 1)
 // table 0 (pksNegS) into row rowA[g] and table 1 (pksId) into row rowB[g] of the
 // destination (each row 2*N1 u32, pre-zeroed).
 // Grid: (islices, N1*2 / 512, 2 tables); CTA: 256 threads x 2 coordinates x GT tasks.
+// Streaming private key switch (same result as pks_kernel, all tasks of the batch in one
+// CTA): for every (i, j) the CTA reads the 2^b - 1 candidate rows of the table once,
+// coalesced, at its 512 coordinates (two per thread), and each task adds the row its digit
+// selects -- the digit is the same for every thread of the CTA, so the selection is an
+// indexed read of the thread's own shared-memory column (row 0 = zeros: digit 0 adds
+// nothing).  The tables (2 x 1.175 GB) stream from HBM once instead of being gathered as
+// 8-byte rows per task (pks_kernel, latency-bound at ~63% of the copy bandwidth).  Each
+// thread stages its own candidates with cp.async kPksRing steps ahead (no barrier: a thread
+// reads only what it copied); a task's digits of one i sit in a register for its t steps.
+// Grid (islices, 2 N1 / 512, 2 tables); TM >= T2 tasks (the others read digit 0).
+constexpr int kPksRing = 4;
+template <int TM>
+__global__ void __launch_bounds__(256) pks_stream_kernel(
+    const uint64_t* __restrict__ acc2, const uint64_t* __restrict__ hv, int T2,
+    const uint32_t* __restrict__ pks_negs, const uint32_t* __restrict__ pks_id,
+    uint32_t* __restrict__ dst, const int* __restrict__ rowA, const int* __restrict__ rowB,
+    int N2, int N1, int basebits, int t, int islice)
+{
+    constexpr int kMaxBase = 7;  // 2^b - 1 for b <= 3 (tfhe-80: b = 3)
+    extern __shared__ uint32_t pks_sm[];
+    uint32_t* pk = pks_sm;                                             // [islice][TM]
+    uint2* ring = reinterpret_cast<uint2*>(pks_sm + (size_t)islice * TM);  // [R][8][256]
+    const int i0 = blockIdx.x * islice;
+    const int i1 = min(N2 + 1, i0 + islice);
+    const int table = blockIdx.z;
+    const uint32_t* tab = table == 0 ? pks_negs : pks_id;
+    const int nb = basebits * t;
+    const uint64_t offset = nb >= 64 ? 0ull : 1ull << (64 - (1 + nb));
+    const int perBase = (1 << basebits) - 1;
+    const uint32_t dmask = (1u << basebits) - 1;
+    const int tid = threadIdx.x;
+    const int k = (blockIdx.y * 256 + tid) * 2;
+    const bool kvalid = k < 2 * N1;
+    const int kk = kvalid ? k : 0;
+    for (int x = tid; x < (i1 - i0) * TM; x += blockDim.x) {
+        const int ii = x / TM, g = x % TM;
+        uint32_t w = 0;
+        if (g < T2) {
+            const int i = i0 + ii;
+            const uint64_t* A = acc2 + (size_t)g * 2 * N2;
+            uint64_t val;
+            if (i < N2)
+                val = (i == 0) ? A[0] : 0ull - A[N2 - i];
+            else
+                val = A[N2] + hv[g] / 2;
+            w = (uint32_t)((val + offset) >> (64 - nb));
+        }
+        pk[x] = w;
+    }
+    for (int q = 0; q < kPksRing; q++)
+        ring[(q * (kMaxBase + 1)) * 256 + tid] = make_uint2(0, 0);  // digit 0 of every slot
+    __syncthreads();
+    uint32_t acc[TM][2];
+#pragma unroll
+    for (int g = 0; g < TM; g++)
+        acc[g][0] = acc[g][1] = 0;
+    const int steps = (i1 - i0) * t;
+    // candidate row d of step s = (i, j): tab[((i t + j) perBase + d - 1) 2 N1 + k]
+    auto issue = [&](int s) {
+        if (s < steps) {
+            const uint32_t* r = tab + ((size_t)(i0 * t + s) * perBase) * 2 * N1 + kk;
+            uint2* slot = ring + (size_t)((s % kPksRing) * (kMaxBase + 1) + 1) * 256 + tid;
+#pragma unroll
+            for (int d = 0; d < kMaxBase; d++)
+                if (d < perBase)
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(slot + d * 256)),
+                                 "l"(r + (size_t)d * 2 * N1)
+                                 : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    for (int s = 0; s < kPksRing - 1; s++)
+        issue(s);
+    int s = 0;
+#pragma unroll 1
+    for (int ii = 0; ii < i1 - i0; ii++) {
+        uint32_t pkr[TM];
+#pragma unroll
+        for (int g = 0; g < TM; g++)
+            pkr[g] = pk[ii * TM + g];
+#pragma unroll 1
+        for (int j = 0; j < t; j++, s++) {
+            issue(s + kPksRing - 1);
+            asm volatile("cp.async.wait_group %0;" ::"n"(kPksRing - 1) : "memory");
+            const int sh = nb - (j + 1) * basebits;
+            const uint2* slot = ring + (size_t)((s % kPksRing) * (kMaxBase + 1)) * 256 + tid;
+#pragma unroll
+            for (int g = 0; g < TM; g++) {
+                const uint32_t d = (pkr[g] >> sh) & dmask;  // same for every thread
+                const uint2 v = slot[d * 256];
+                acc[g][0] += v.x;
+                acc[g][1] += v.y;
+            }
+        }
+    }
+    if (!kvalid)
+        return;
+#pragma unroll
+    for (int g = 0; g < TM; g++) {
+        if (g >= T2)
+            break;
+        const int r = table == 0 ? rowA[g] : rowB[g];
+        uint32_t* o = dst + (size_t)r * 2 * N1 + k;
+        if (acc[g][0])
+            atomicAdd(o, 0u - acc[g][0]);
+        if (acc[g][1])
+            atomicAdd(o + 1, 0u - acc[g][1]);
+    }
+}
+
 template <int GT>
 __global__ void __launch_bounds__(256) pks_kernel(const uint64_t* __restrict__ acc2,
                                                   const uint64_t* __restrict__ hv, int T2,

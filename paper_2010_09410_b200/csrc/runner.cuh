@@ -60,6 +60,11 @@ struct vsp_netlist {
     std::vector<int> dag_cells, level, height, dff_cells;
     std::vector<int> launch_level;  // per DAG node: the level it is evaluated in (build_dag)
     std::vector<int> level_tasks;   // blind-rotation tasks of each launch level's gates
+    // per launch level: the gates' input nets [G][3] then output nets [G], device resident
+    // (uploaded once), so a level reads and writes the value table in place
+    DevBuf lvl_nets;
+    std::vector<size_t> lvl_off;
+    std::vector<std::vector<int32_t>> lvl_kinds;
     std::vector<int> node_of_cell;
     int rom_cell = -1, ram_cell = -1, gmax = 0, depth = 0;
     // per level: gate cells (kinds 0..9) and memory ports
@@ -496,9 +501,41 @@ void run_cycle_body(vsp_netlist* nl, cudaStream_t st)
             VSP_CUDA_CHECK(cudaGetLastError());
         }
     };
+    if (nl->lvl_off.empty()) {
+        // static per netlist: every level's input / output nets and kinds
+        std::vector<int> all;
+        nl->lvl_kinds.assign(nl->depth, {});
+        for (int L = 0; L < nl->depth; L++) {
+            const auto& gates = nl->level_gates[L];
+            nl->lvl_off.push_back(all.size());
+            const size_t base = all.size();
+            all.resize(base + gates.size() * 4, -1);
+            for (size_t g = 0; g < gates.size(); g++) {
+                const int cell = gates[g];
+                nl->lvl_kinds[L].push_back(nl->kind[cell]);
+                for (int k = nl->in_off[cell], q = 0; k < nl->in_off[cell + 1]; k++, q++)
+                    all[base + g * 3 + q] = nl->in_nets[k];
+                all[base + gates.size() * 3 + g] = nl->out_nets[nl->out_off[cell]];
+            }
+        }
+        int* d = nl->lvl_nets.as<int>(std::max<size_t>(all.size(), 1));
+        if (!all.empty())
+            VSP_CUDA_CHECK(cudaMemcpyAsync(d, all.data(), all.size() * sizeof(int),
+                                           cudaMemcpyHostToDevice, st));
+        VSP_CUDA_CHECK(cudaStreamSynchronize(st));  // `all` is pageable and goes out of scope
+    }
     auto run_gates = [&](int L) {
         const auto& gates = nl->level_gates[L];
-        if (!gates.empty()) {
+        if (!gates.empty() && !sharded(c)) {
+            // one GPU: the level reads its inputs from and writes its outputs into the value
+            // table by net index (no gather / scatter kernels)
+            const size_t G = gates.size();
+            const int* d = nl->lvl_nets.as<int>(0) + nl->lvl_off[L];
+            const LevelIdx lx{vals, d, d + 3 * G};
+            hom_gate_dev(c, nl->lvl_kinds[L].data(), nullptr, nullptr, G, st, nullptr, &lx);
+            VSP_CUDA_CHECK(cudaGetLastError());
+        }
+        else if (!gates.empty()) {
             const int G = (int)gates.size();
             std::vector<int> gnets((size_t)G * 3, -1), onets(G);
             std::vector<int32_t> kinds(G);

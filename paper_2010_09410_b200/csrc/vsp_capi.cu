@@ -959,7 +959,7 @@ void iks_gemm_run(vsp_ctx* c, const int8_t* S, int Mpad, int32_t* C, cudaStream_
 // blind-rotation wave; the key is streamed twice as often).
 void launch_iks(vsp_ctx* c, const uint32_t* d_trlwe, const int2* d_gtask, const int* d_glist,
                 int Gl, uint32_t* d_out, cudaStream_t st, const int* d_seidx = nullptr,
-                bool gt8 = false)
+                bool gt8 = false, const int* d_oidx = nullptr)
 {
     if (Gl == 0)
         return;
@@ -977,7 +977,7 @@ void launch_iks(vsp_ctx* c, const uint32_t* d_trlwe, const int2* d_gtask, const 
             iks_gemm_epilogue_kernel<<<dim3(Gl, (unsigned)((p.n + 1 + 127) / 128)), 128, 0, st>>>(
                                                          C, c->k4_npad, nsplit, (size_t)Mpad * c->k4_npad,
                                                          d_trlwe, d_gtask, d_glist, d_seidx, d_out,
-                                                         (int)p.n, (int)p.N1);
+                                                         (int)p.n, (int)p.N1, d_oidx);
             VSP_CUDA_CHECK(cudaGetLastError());
         });
         c->launches += 3;
@@ -987,7 +987,7 @@ void launch_iks(vsp_ctx* c, const uint32_t* d_trlwe, const int2* d_gtask, const 
     const int kpt = (int)((p.n + 1 + 255) / 256);
     timed(c, "iks", st, [&] {
         iks_init_kernel<<<Gl, 128, 0, st>>>(d_trlwe, d_gtask, d_glist, d_seidx, Gl, d_out, p.n,
-                                            p.N1);
+                                            p.N1, d_oidx);
         const int kpt4 = (int)((p.n + 1 + 127) / 128);
         if (p.ksBaseBits == 2 && p.ksLen == 8 && kpt4 >= 1 && kpt4 <= 5) {
             auto run = [&](auto gtc) {
@@ -1000,7 +1000,7 @@ void launch_iks(vsp_ctx* c, const uint32_t* d_trlwe, const int2* d_gtask, const 
                 const size_t smem = (size_t)(p.N1 / split) * GT * sizeof(uint16_t);
 #define VSP_IKS_B2(K)                                                                       \
     iks_b2_kernel<K, GT><<<grid, 128, smem, st>>>(d_trlwe, d_gtask, d_glist, d_seidx, Gl, \
-                                                  c->d_ksk, d_out, p.n, p.N1)
+                                                  c->d_ksk, d_out, p.n, p.N1, d_oidx)
                 switch (kpt4) {
                 case 1: VSP_IKS_B2(1); break;
                 case 2: VSP_IKS_B2(2); break;
@@ -1023,13 +1023,13 @@ void launch_iks(vsp_ctx* c, const uint32_t* d_trlwe, const int2* d_gtask, const 
             const size_t smem = (size_t)(p.N1 / split) * p.ksLen * sizeof(uint64_t);
             if (kpt == 1)
                 iks_kernel<2, GT, 1><<<grid, 256, smem, st>>>(d_trlwe, d_gtask, d_glist, d_seidx, Gl,
-                                                              c->d_ksk, d_out, p.n, p.N1, p.ksLen);
+                                                              c->d_ksk, d_out, p.n, p.N1, p.ksLen, d_oidx);
             else if (kpt == 2)
                 iks_kernel<2, GT, 2><<<grid, 256, smem, st>>>(d_trlwe, d_gtask, d_glist, d_seidx, Gl,
-                                                              c->d_ksk, d_out, p.n, p.N1, p.ksLen);
+                                                              c->d_ksk, d_out, p.n, p.N1, p.ksLen, d_oidx);
             else if (kpt == 3)
                 iks_kernel<2, GT, 3><<<grid, 256, smem, st>>>(d_trlwe, d_gtask, d_glist, d_seidx, Gl,
-                                                              c->d_ksk, d_out, p.n, p.N1, p.ksLen);
+                                                              c->d_ksk, d_out, p.n, p.N1, p.ksLen, d_oidx);
             else
                 throw std::invalid_argument("identity key switch: n too large");
         }
@@ -1039,7 +1039,7 @@ void launch_iks(vsp_ctx* c, const uint32_t* d_trlwe, const int2* d_gtask, const 
             const int split = iks_split(tiles, (int)p.N1, c->sms);
             const size_t smem = (size_t)(p.N1 / split) * p.ksLen * sizeof(uint64_t);
             iks_kernel<4, GT, 1><<<dim3(tiles, split), 256, smem, st>>>(
-                d_trlwe, d_gtask, d_glist, d_seidx, Gl, c->d_ksk, d_out, p.n, p.N1, p.ksLen);
+                d_trlwe, d_gtask, d_glist, d_seidx, Gl, c->d_ksk, d_out, p.n, p.N1, p.ksLen, d_oidx);
         }
         else {
             throw std::invalid_argument("identity key switch: unsupported base");
@@ -1088,6 +1088,8 @@ void configure_kernels()
                                         (int)sizeof(Br2Smem)));
     VSP_CUDA_CHECK(cudaFuncSetAttribute(br2c_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)sizeof(Br2cSmem)));
+    VSP_CUDA_CHECK(cudaFuncSetAttribute(pks_stream_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        128 * 1024));
     VSP_CUDA_CHECK(cudaFuncSetAttribute(br2q_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)sizeof(Br2qSmem)));
     VSP_CUDA_CHECK(cudaFuncSetAttribute(br2q_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1161,8 +1163,17 @@ struct HostIO {
 
 int bar_take(vsp_ctx* c, int T);
 
+// Netlist-runner mode of hom_gate_dev: inputs read from and outputs written to the value
+// table by net index (no gather / scatter of the level's ciphertexts).
+struct LevelIdx {
+    uint32_t* vals;     // value table [nets][n + 1]
+    const int* innet;   // [G][3] input nets (-1: none)
+    const int* onet;    // [G] output nets
+};
+
 void hom_gate_dev(vsp_ctx* c, const int32_t* kinds, const uint32_t* d_in, uint32_t* d_out,
-                  size_t G, cudaStream_t st, const HostIO* io = nullptr)
+                  size_t G, cudaStream_t st, const HostIO* io = nullptr,
+                  const LevelIdx* lx = nullptr)
 {
     require_keys(c);
     if (G == 0)
@@ -1200,9 +1211,14 @@ void hom_gate_dev(vsp_ctx* c, const int32_t* kinds, const uint32_t* d_in, uint32
             VSP_CUDA_CHECK(cudaStreamWaitEvent(st, c->ev_in[0], 0));
         }
         timed(c, "gate_prep", st, [&] {
-            gate_prep_kernel<<<(unsigned)(g1 - g0), 128, 0, st>>>(
-                d_kinds + g0, d_in + g0 * 3 * w, d_gtask + g0, d_tasks, d_out + g0 * w,
-                (int)(g1 - g0), (int)p.n);
+            if (lx)
+                gate_prep_idx_kernel<<<(unsigned)(g1 - g0), 128, 0, st>>>(
+                    d_kinds + g0, lx->vals, lx->innet + 3 * g0, lx->onet + g0, d_gtask + g0,
+                    d_tasks, lx->vals, (int)(g1 - g0), (int)p.n);
+            else
+                gate_prep_kernel<<<(unsigned)(g1 - g0), 128, 0, st>>>(
+                    d_kinds + g0, d_in + g0 * 3 * w, d_gtask + g0, d_tasks, d_out + g0 * w,
+                    (int)(g1 - g0), (int)p.n);
         });
         VSP_CUDA_CHECK(cudaGetLastError());
         c->launches++;
@@ -1266,7 +1282,8 @@ void hom_gate_dev(vsp_ctx* c, const int32_t* kinds, const uint32_t* d_in, uint32
         VSP_CUDA_CHECK(cudaEventRecord(c->ev_fork, st));
         VSP_CUDA_CHECK(cudaStreamWaitEvent(c->astream, c->ev_fork, 0));
         static const bool gt8 = !getenv("VSP_IKS_FORK_GT") || atoi(getenv("VSP_IKS_FORK_GT")) == 8;
-        launch_iks(c, d_trlwe, d_gtask, d_glist, k1, d_out, c->astream, nullptr, gt8);
+        launch_iks(c, d_trlwe, d_gtask, d_glist, k1, lx ? lx->vals : d_out, c->astream, nullptr,
+                   gt8, lx ? lx->onet : nullptr);
         VSP_CUDA_CHECK(cudaEventRecord(c->ev_join, c->astream));
         forked = true;
         if (io)  // gates below the first remainder task are final once this key switch is
@@ -1283,7 +1300,8 @@ void hom_gate_dev(vsp_ctx* c, const int32_t* kinds, const uint32_t* d_in, uint32
                                        (size_t)kbar * 2 * p.N1 * 4, cudaMemcpyDeviceToDevice, st));
         c->bar_done += kbar;
     }
-    launch_iks(c, d_trlwe, d_gtask, d_glist + k1, Gl - k1, d_out, st);
+    launch_iks(c, d_trlwe, d_gtask, d_glist + k1, Gl - k1, lx ? lx->vals : d_out, st, nullptr,
+               false, lx ? lx->onet : nullptr);
     if (forked)
         VSP_CUDA_CHECK(cudaStreamWaitEvent(st, c->ev_join, 0));
     if (io) {
@@ -1362,12 +1380,27 @@ void cb_batch(vsp_ctx* c, const uint32_t* d_lwe, int C, uint32_t* d_out, cudaStr
     VSP_CUDA_CHECK(cudaMemsetAsync(d_out, 0, (size_t)C * 2 * l * 2 * N1 * 4, st));
     const int islices = std::min<int>(64, (int)N2 + 1);
     const dim3 grid(islices, (unsigned)((2 * N1 + 511) / 512), 2);
+    constexpr int kPksStreamTM = 32;  // tasks per CTA of the streaming kernel (ROM + RAM: 30;
+                                      // configure_kernels sets its shared-memory limit)
     constexpr int kPksGT = 8;  // gates per tile: fewer registers, more CTAs and gathers in flight (16: 2.07 ms, 8: 1.54, 4: 1.85 per access)
     const size_t smem = (size_t)((N2 + 1 + islices - 1) / islices) * kPksGT * 4;
+    static const bool gather = getenv("VSP_PKS_GATHER") && atoi(getenv("VSP_PKS_GATHER")) == 1;
     timed(c, "pks", st, [&] {
-        pks_kernel<kPksGT><<<grid, 256, smem, st>>>(d_acc2, d_hv, T2, c->d_pks[0], c->d_pks[1], d_out,
-                                                d_rows, d_rows + T2, (int)N2, (int)N1,
-                                                (int)p.pksBaseBits, (int)p.pksLen);
+        if (T2 <= kPksStreamTM && p.pksBaseBits <= 3 && !gather) {
+            // streaming tables, all tasks per CTA (pks_stream_kernel)
+            // 37 i-slices x 4 coordinate chunks x 2 tables = 296 CTAs: one wave at 2 per SM
+            const int slices = std::min<int>(37, (int)N2 + 1);
+            const int islice = ((int)N2 + 1 + slices - 1) / slices;
+            const size_t sm2 = (size_t)islice * kPksStreamTM * 4 + (size_t)kPksRing * 8 * 256 * 8;
+            const dim3 g2((unsigned)((N2 + 1 + islice - 1) / islice), (unsigned)((2 * N1 + 511) / 512), 2);
+            pks_stream_kernel<kPksStreamTM><<<g2, 256, sm2, st>>>(
+                d_acc2, d_hv, T2, c->d_pks[0], c->d_pks[1], d_out, d_rows, d_rows + T2, (int)N2,
+                (int)N1, (int)p.pksBaseBits, (int)p.pksLen, islice);
+        }
+        else
+            pks_kernel<kPksGT><<<grid, 256, smem, st>>>(d_acc2, d_hv, T2, c->d_pks[0], c->d_pks[1], d_out,
+                                                    d_rows, d_rows + T2, (int)N2, (int)N1,
+                                                    (int)p.pksBaseBits, (int)p.pksLen);
     });
     VSP_CUDA_CHECK(cudaGetLastError());
     c->launches++;

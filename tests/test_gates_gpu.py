@@ -232,7 +232,8 @@ def test_mux_straddling_wave_boundaries_host_pipeline(prod):
     G = 1601
     kid = np.array([GATE_KINDS.index("AND")] + [GATE_KINDS.index("MUX")] * 1600, np.int32)
     if e.sms == 148:
-        assert e.br_plan(3201) == {"lat": False, "full": 2368, "w_rem": 3, "rem_kernel": "br1024p"}
+        # the 833-task remainder: one W=6 wave (7.72 ms) beats two W=3 two-warp waves (8.62)
+        assert e.br_plan(3201) == {"lat": False, "full": 2368, "w_rem": 6, "rem_kernel": "br1024"}
     rng = np.random.default_rng(1601)
     k = oracle_keys("tfhe-80", 20200729, False)
     p = vsp.ParameterSet("tfhe-80")
