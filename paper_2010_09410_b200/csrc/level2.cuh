@@ -492,7 +492,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(256, 1)
                 uint64_t* __restrict__ out, int n, int bgbits,
                 unsigned long long* __restrict__ probe = nullptr)
 {
-    unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long ph[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     long long tprev = 0;
     auto mark = [&](int k) {
         if constexpr (PROBE) {
@@ -588,6 +588,7 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(256, 1)
                     z[t] = split_fwd(u, v, br);
                 }
             }
+            mark(8);  // digits + split (probe slot 8); the forward transform is slot 0
             double2* rg = sm.reg[L];
             if (br == 0)
                 fft512_fwd_pair<1>(z, rg, sm.tw2, lane, h, 1 + L);
@@ -716,8 +717,8 @@ __global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(256, 1)
     }
     if constexpr (PROBE) {
         if (lane == 0 && task == 0)
-            for (int k = 0; k < 8; k++)
-                probe[((size_t)cr * 8 + warp) * 8 + k] = ph[k];
+            for (int k = 0; k < 10; k++)
+                probe[((size_t)cr * 8 + warp) * 10 + k] = ph[k];
     }
     if (br == 0) {
         uint64_t* dst = out + (size_t)task * 4096 + (size_t)P * 2048;

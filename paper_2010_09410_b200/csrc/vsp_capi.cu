@@ -543,19 +543,19 @@ void launch_br2(vsp_ctx* c, const uint32_t* d_lwe, int ninputs, const uint64_t* 
                                                             (int)c->p.Bg2Bits);
     else if (getenv("VSP_BR2_PROBE")) {  // tuning only: per-phase clock64 of task 0
         unsigned long long* d_pr = nullptr;
-        VSP_CUDA_CHECK(cudaMalloc(&d_pr, 4 * 8 * 8 * 8));
+        VSP_CUDA_CHECK(cudaMalloc(&d_pr, 4 * 8 * 10 * 8));
         br2q_kernel<true><<<4 * T, 256, sizeof(Br2qSmem), st>>>(d_lwe, ninputs, d_hv, c->d_bk2fd,
                                                                 c->d_tw2, d_acc, (int)c->p.n,
                                                                 (int)c->p.Bg2Bits, d_pr);
-        std::vector<unsigned long long> h(256);
-        VSP_CUDA_CHECK(cudaMemcpyAsync(h.data(), d_pr, 256 * 8, cudaMemcpyDeviceToHost, st));
+        std::vector<unsigned long long> h(320);
+        VSP_CUDA_CHECK(cudaMemcpyAsync(h.data(), d_pr, 320 * 8, cudaMemcpyDeviceToHost, st));
         VSP_CUDA_CHECK(cudaStreamSynchronize(st));
         cudaFree(d_pr);
         for (int r = 0; r < 4; r += 3)
             for (int w = 0; w < 8; w += 2) {
                 fprintf(stderr, "br2q probe cta %d warp %d cycles/step:", r, w);
-                for (int k = 0; k < 8; k++)
-                    fprintf(stderr, " %.0f", (double)h[(r * 8 + w) * 8 + k] / c->p.n);
+                for (int k = 0; k < 10; k++)
+                    fprintf(stderr, " %.0f", (double)h[(r * 8 + w) * 10 + k] / c->p.n);
                 fprintf(stderr, "\n");
             }
     }
