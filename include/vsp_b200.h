@@ -160,6 +160,16 @@ int vsp_mem_ports_dev(vsp_ctx* ctx, uint32_t depth_bytes, const uint32_t* d_luts
                       const uint32_t* d_wflag, const uint32_t* d_wdata, uint32_t* d_readout,
                       void* stream);
 
+/* The same access with HOST buffers (the drop-in form of one memory stage: romRead +
+ * ramCycle, mem.cpp:122-177, engine.cpp:133-148): luts (nluts x 2 N1) and both ports'
+ * ciphertexts in, rom_out (32 x (n+1)) and readout (w x (n+1)) out, and the RAM image
+ * (w 2^v x 2 N1) in AND out, updated in place like the reference's EncryptedRam&.  Pinned
+ * host buffers (cudaHostAlloc / cudaHostRegister) make the copies run at link speed. */
+int vsp_mem_ports(vsp_ctx* ctx, uint32_t depth_bytes, const uint32_t* luts, uint32_t nluts,
+                  const uint32_t* rom_addr, uint32_t vrom, uint32_t* rom_out, uint32_t v,
+                  uint32_t w, uint32_t* ram, const uint32_t* ram_addr, const uint32_t* wflag,
+                  const uint32_t* wdata, uint32_t* readout);
+
 /* blindRotate<uint64_t> (ops.cpp:713-742) with test vector (0, h[t]/2 ...): T level-0
  * TLWEs -> T level-2 TRLWE accumulators (2 x N2 u64).  Exposed for parity tests of the
  * circuit-bootstrapping inner loop. */

@@ -55,6 +55,7 @@ def lib() -> ctypes.CDLL:
         L.vsp_hom_gate_batch_dev.argtypes = [vp, vp, vp, vp, sz, vp]
         L.vsp_ram_cycle_dev.argtypes = [vp, u32, u32, vp, vp, vp, vp, vp, vp]
         L.vsp_rom_read_dev.argtypes = [vp, u32, vp, u32, vp, u32, vp, vp]
+        L.vsp_mem_ports.argtypes = [vp, u32, vp, u32, vp, u32, vp, u32, u32, vp, vp, vp, vp, vp]
         L.vsp_mem_ports_dev.argtypes = [vp, u32, vp, u32, vp, u32, vp, u32, u32, vp, vp, vp, vp,
                                         vp, vp]
         L.vsp_bootstrap_to_trlwe_batch.argtypes = [vp, vp, vp, sz]
@@ -544,6 +545,34 @@ class Engine:
         _check(lib().vsp_rom_read_dev(self.h, depth_bytes, ctypes.c_void_p(d_luts), nluts,
                                       ctypes.c_void_p(d_addr), vrom, ctypes.c_void_p(d_out),
                                       ctypes.c_void_p(stream)))
+
+    def mem_ports(self, luts: np.ndarray, depth_bytes: int, rom_addr, ram: np.ndarray, v: int,
+                  w: int, addr, wflag, wdata):
+        """One memory stage with host buffers (vsp_mem_ports): romRead + ramCycle with the
+        two ports' address bootstraps batched.  Returns (rom_out (32, n+1), readOut (w, n+1),
+        ram).  A C-contiguous uint32 `ram` of shape (w << v, 2 N1) is updated IN PLACE (the
+        reference's EncryptedRam&; pass a pinned array for link-speed copies), any other is
+        copied first and the new image returned."""
+        p = self.params
+        luts = np.ascontiguousarray(luts, np.uint32)
+        ra = np.ascontiguousarray(np.atleast_2d(rom_addr), np.uint32)
+        if ra.shape[1] != p.n + 1 or luts.ndim != 2 or luts.shape[1] != 2 * p.N1:
+            raise ValueError("romRead: address / LUT shape mismatch")
+        shape = ((w << v), 2 * p.N1)
+        if not (isinstance(ram, np.ndarray) and ram.dtype == np.uint32 and ram.shape == shape
+                and ram.flags.c_contiguous and ram.flags.writeable):
+            ram = np.ascontiguousarray(np.array(ram, np.uint32).reshape(shape))
+        a = np.ascontiguousarray(addr, np.uint32)
+        f = np.ascontiguousarray(wflag, np.uint32)
+        d = np.ascontiguousarray(wdata, np.uint32)
+        if len(a) != v or a.shape != (v, p.n + 1) or f.size != p.n + 1 or d.shape != (w, p.n + 1):
+            raise ValueError("ramCycle: address width mismatch")
+        rom_out = np.zeros((32, p.n + 1), np.uint32)
+        ro = np.zeros((w, p.n + 1), np.uint32)
+        _check(lib().vsp_mem_ports(self.h, depth_bytes, _ptr(luts), luts.shape[0], _ptr(ra),
+                                   ra.shape[0], _ptr(rom_out), v, w, _ptr(ram), _ptr(a), _ptr(f),
+                                   _ptr(d), _ptr(ro)))
+        return rom_out, ro, ram
 
     def mem_ports_dev(self, d_luts: int, nluts: int, depth_bytes: int, d_rom_addr: int,
                       vrom: int, d_rom_out: int, d_ram: int, v: int, w: int, d_ram_addr: int,

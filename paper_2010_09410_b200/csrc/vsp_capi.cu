@@ -2420,6 +2420,45 @@ int vsp_mem_ports_dev(vsp_ctx* c, uint32_t depth_bytes, const uint32_t* d_luts, 
     });
 }
 
+int vsp_mem_ports(vsp_ctx* c, uint32_t depth_bytes, const uint32_t* luts, uint32_t nluts,
+                  const uint32_t* rom_addr, uint32_t vrom, uint32_t* rom_out, uint32_t v,
+                  uint32_t w, uint32_t* ram, const uint32_t* ram_addr, const uint32_t* wflag,
+                  const uint32_t* wdata, uint32_t* readout)
+{
+    return guard([&] {
+        CallScope cs(c, c->stream);
+        const Params& p = c->p;
+        if (v == 0 || w == 0)
+            throw std::invalid_argument("ramCycle: address width mismatch");
+        if (vrom == 0 || nluts == 0)
+            throw std::invalid_argument("romRead: empty address or LUT table");
+        const size_t n1 = p.n + 1, cw = 2 * (size_t)p.N1, cells = (size_t)w << v;
+        cudaStream_t st = c->stream;
+        uint32_t* d_ram = c->ramio.as<uint32_t>(cells * cw);
+        uint32_t* d_luts = c->romio.as<uint32_t>((size_t)nluts * cw);
+        uint32_t* d_io = c->in.as<uint32_t>((vrom + 32 + v + 1 + 2 * (size_t)w) * n1);
+        uint32_t* d_raddr = d_io;
+        uint32_t* d_rout = d_raddr + vrom * n1;
+        uint32_t* d_addr = d_rout + 32 * n1;
+        uint32_t* d_wflag = d_addr + v * n1;
+        uint32_t* d_wdata = d_wflag + n1;
+        uint32_t* d_ro = d_wdata + w * n1;
+        VSP_CUDA_CHECK(cudaMemcpyAsync(d_ram, ram, cells * cw * 4, cudaMemcpyHostToDevice, st));
+        VSP_CUDA_CHECK(cudaMemcpyAsync(d_luts, luts, (size_t)nluts * cw * 4, cudaMemcpyHostToDevice, st));
+        VSP_CUDA_CHECK(cudaMemcpyAsync(d_raddr, rom_addr, vrom * n1 * 4, cudaMemcpyHostToDevice, st));
+        VSP_CUDA_CHECK(cudaMemcpyAsync(d_addr, ram_addr, v * n1 * 4, cudaMemcpyHostToDevice, st));
+        VSP_CUDA_CHECK(cudaMemcpyAsync(d_wflag, wflag, n1 * 4, cudaMemcpyHostToDevice, st));
+        VSP_CUDA_CHECK(cudaMemcpyAsync(d_wdata, wdata, w * n1 * 4, cudaMemcpyHostToDevice, st));
+        mem_pair_dev(c, d_luts, (int)nluts, depth_bytes, d_raddr, (int)vrom, d_rout, d_ram, (int)v,
+                     (int)w, d_addr, d_wflag, d_wdata, d_ro, st);
+        ram_gather_dev(c, d_ram, (int)v, (int)w, st);  // sharded RAM: whole image back
+        VSP_CUDA_CHECK(cudaMemcpyAsync(rom_out, d_rout, 32 * n1 * 4, cudaMemcpyDeviceToHost, st));
+        VSP_CUDA_CHECK(cudaMemcpyAsync(readout, d_ro, w * n1 * 4, cudaMemcpyDeviceToHost, st));
+        VSP_CUDA_CHECK(cudaMemcpyAsync(ram, d_ram, cells * cw * 4, cudaMemcpyDeviceToHost, st));
+        VSP_CUDA_CHECK(cudaStreamSynchronize(st));
+    });
+}
+
 int vsp_rom_read_dev(vsp_ctx* c, uint32_t depth_bytes, const uint32_t* d_luts, uint32_t nluts,
                      const uint32_t* d_addr, uint32_t vrom, uint32_t* d_out, void* stream)
 {

@@ -236,6 +236,34 @@ def test_mem_ports_dev_equals_separate_calls_and_oracle(det):
             words[A] = X
 
 
+def test_mem_ports_host_call_equals_oracle_and_updates_ram_in_place(det):
+    """vsp_mem_ports (host buffers: the drop-in form of one memory stage) == the oracle's
+    romRead and ramCycle bit for bit over consecutive accesses; a C-contiguous uint32 RAM
+    image is updated in place (EncryptedRam&), any other input is copied and returned."""
+    e, o = det
+    rng = np.random.default_rng(18)
+    v, w = 3, 4
+    words = [int(x) for x in rng.integers(0, 1 << w, 1 << v)]
+    ram = np.ascontiguousarray(o.encrypt_ram(words_to_image(words, v, w), v, w), np.uint32)
+    luts = o.encrypt_rom(rng.integers(0, 256, 512).astype(np.uint8))
+    ram_o = ram.copy()
+    for A, wf, X, blk in [(6, 1, 5, 33), (6, 0, 2, 100), (1, 1, 15, 127)]:
+        addr, f, d, raddr = enc_word(o, A, v), o.encrypt(wf), enc_word(o, X, w), enc_word(o, blk, 7)
+        rom, ro, out = e.mem_ports(luts, 512, raddr, ram, v, w, addr, f, d)
+        assert out is ram  # in place
+        rom_o = o.rom_read(luts, 512, raddr)
+        ro_o, ram_o = o.ram_cycle(ram_o, v, w, addr, f, d)
+        assert np.array_equal(rom, rom_o) and np.array_equal(ro, ro_o)
+        assert np.array_equal(ram, ram_o)
+        assert dec_word(o, ro_o) == words[A]
+        if wf:
+            words[A] = X
+    as_list = ram.astype(np.int64)  # not uint32: copied, the caller's array untouched
+    _, _, out = e.mem_ports(luts, 512, enc_word(o, 0, 7), as_list, v, w, enc_word(o, 0, v),
+                            o.encrypt(1), enc_word(o, 0, w))
+    assert out is not as_list and np.array_equal(as_list, ram.astype(np.int64))
+
+
 def test_tfhe80_full_size_ram_cycles(prod_cb):
     """BASELINE configs[1] geometry (v=8, w=16: 4,096 cells) on the FFT path, where the
     write unit key-switches the whole-wave cells under the remainder blind-rotation wave:
