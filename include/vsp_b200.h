@@ -200,6 +200,14 @@ int vsp_netlist_info(vsp_netlist* nl, int32_t* out6, int32_t* levels);
  * latency waves).  Results are unchanged: every gate still runs after all its producers
  * and before all its consumers.  No reference counterpart (scheduling only). */
 int vsp_netlist_launch_levels(vsp_netlist* nl, int32_t* levels);
+/* The same schedule without a device (host only): validates the flat netlist like
+ * vsp_netlist_create and returns, per DAG node, the ASAP level (buildDag, netlist.cpp:348-432)
+ * and the launch level for a device with `sms` SMs, plus the depth. */
+int vsp_netlist_schedule(int32_t net_count, int32_t cells, const int32_t* kinds, const int32_t* ids,
+                         const int32_t* in_off, const int32_t* in_nets, const int32_t* out_off,
+                         const int32_t* out_nets, const int32_t* input_nets, int32_t n_inputs,
+                         int32_t sms, int32_t* asap_levels, int32_t* launch_levels,
+                         int32_t* depth);
 /* Evaluator::setInput (engine.hpp:160-163) by index into input_nets. */
 int vsp_netlist_set_input(vsp_netlist* nl, int32_t input_index, const uint32_t* tlwe);
 /* Evaluator::output (engine.hpp:165-176) for any net. */

@@ -171,7 +171,8 @@ void validate_netlist(const vsp_netlist* nl)
         nl_fail("at most one ROM port and one RAM port are supported");
 }
 
-void build_dag(vsp_netlist* nl)
+// sms: SMs of the device the levels launch on (one latency wave = sms tasks).
+void build_dag(vsp_netlist* nl, int sms)
 {
     const int C = (int)nl->kind.size();
     nl->node_of_cell.assign(C, -1);
@@ -260,7 +261,7 @@ void build_dag(vsp_netlist* nl)
         // Only when the level can get down to one wave, and without pushing the next level
         // out of the latency kernel's two-wave range; the next level then sheds its own
         // excess the same way (the last level keeps what it receives).
-        const int cap = nl->ctx->sms;
+        const int cap = sms;
         auto level_tasks = [&](int L) {
             int T = 0;
             for (int node : at[L])
@@ -312,7 +313,6 @@ void build_dag(vsp_netlist* nl)
         else
             nl->const_cells.push_back(c);
     }
-    const int sms = nl->ctx->sms;
     nl->max_level_ctas = 0;
     nl->level_tasks.clear();
     for (const auto& lg : nl->level_gates) {

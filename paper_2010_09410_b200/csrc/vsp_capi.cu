@@ -2650,7 +2650,7 @@ vsp_netlist* vsp_netlist_create(vsp_ctx* c, int32_t net_count, int32_t cells, co
         nl->out_nets.assign(out_nets, out_nets + nl->out_off[cells]);
         nl->input_nets.assign(input_nets, input_nets + n_inputs);
         validate_netlist(nl.get());
-        build_dag(nl.get());
+        build_dag(nl.get(), c->sms);
         for (int ci : nl->dff_cells) {
             nl->dff_q.push_back(nl->out_nets[nl->out_off[ci]]);
             nl->dff_d.push_back(nl->in_nets[nl->in_off[ci]]);
@@ -2684,6 +2684,44 @@ vsp_netlist* vsp_netlist_create(vsp_ctx* c, int32_t net_count, int32_t cells, co
         out = nl.release();
     });
     return out;
+}
+
+int vsp_netlist_schedule(int32_t net_count, int32_t cells, const int32_t* kinds, const int32_t* ids,
+                         const int32_t* in_off, const int32_t* in_nets, const int32_t* out_off,
+                         const int32_t* out_nets, const int32_t* input_nets, int32_t n_inputs,
+                         int32_t sms, int32_t* asap_levels, int32_t* launch_levels,
+                         int32_t* depth)
+{
+    return guard([&] {
+        if (net_count < 0 || cells < 0 || n_inputs < 0 || sms < 1)
+            throw std::invalid_argument("netlist: negative size");
+        if (cells > 0 && (!kinds || !ids || !in_off || !out_off))
+            throw std::invalid_argument("netlist: missing cell arrays");
+        vsp_netlist nl;
+        nl.nets = net_count;
+        nl.kind.assign(kinds, kinds + cells);
+        nl.id.assign(ids, ids + cells);
+        nl.in_off.assign(in_off, in_off + cells + 1);
+        nl.out_off.assign(out_off, out_off + cells + 1);
+        for (int i = 0; i < cells; i++)
+            if (nl.in_off[i + 1] < nl.in_off[i] || nl.out_off[i + 1] < nl.out_off[i])
+                throw std::invalid_argument("netlist: pin offsets must be non-decreasing");
+        if (nl.in_off[0] != 0 || nl.out_off[0] != 0)
+            throw std::invalid_argument("netlist: pin offsets must start at 0");
+        nl.in_nets.assign(in_nets, in_nets + nl.in_off[cells]);
+        nl.out_nets.assign(out_nets, out_nets + nl.out_off[cells]);
+        nl.input_nets.assign(input_nets, input_nets + n_inputs);
+        validate_netlist(&nl);
+        build_dag(&nl, sms);
+        for (size_t i = 0; i < nl.level.size(); i++) {
+            if (asap_levels)
+                asap_levels[i] = nl.level[i];
+            if (launch_levels)
+                launch_levels[i] = nl.launch_level[i];
+        }
+        if (depth)
+            *depth = nl.depth;
+    });
 }
 
 void vsp_netlist_destroy(vsp_netlist* nl)

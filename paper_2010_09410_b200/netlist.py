@@ -278,6 +278,7 @@ def _bind():
     L.vsp_netlist_destroy.argtypes = [vp]
     L.vsp_netlist_info.argtypes = [vp, vp, vp]
     L.vsp_netlist_launch_levels.argtypes = [vp, vp]
+    L.vsp_netlist_schedule.argtypes = [i32, i32, vp, vp, vp, vp, vp, vp, vp, i32, i32, vp, vp, vp]
     L.vsp_netlist_set_input.argtypes = [vp, i32, vp]
     L.vsp_netlist_get_net.argtypes = [vp, i32, vp]
     L.vsp_netlist_dff.argtypes = [vp, vp, vp]
@@ -297,6 +298,39 @@ def _bind():
     return L
 
 
+def _flat(nl: Netlist):
+    """The flat C-ABI arrays of a netlist (vsp_netlist_create / vsp_netlist_schedule)."""
+    kinds = np.array([KIND_ID[c.kind] for c in nl.cells], np.int32)
+    ids = np.array([c.id for c in nl.cells], np.int32)
+    in_off = np.zeros(len(nl.cells) + 1, np.int32)
+    out_off = np.zeros(len(nl.cells) + 1, np.int32)
+    for i, c in enumerate(nl.cells):
+        in_off[i + 1] = in_off[i] + len(c.inputs)
+        out_off[i + 1] = out_off[i] + len(c.outputs)
+    in_nets = np.array([x for c in nl.cells for x in c.inputs] or [0], np.int32)
+    out_nets = np.array([x for c in nl.cells for x in c.outputs] or [0], np.int32)
+    inp = [b for p in nl.inputs for b in p.bits]
+    return kinds, ids, in_off, in_nets, out_off, out_nets, inp
+
+
+def schedule(nl: Netlist, sms: int = 148):
+    """The engine's launch schedule without a device (vsp_netlist_schedule): per DAG node
+    (non-DFF cells, in cell order) the ASAP level and the launch level on an `sms`-SM GPU,
+    and the depth."""
+    L = _bind()
+    kinds, ids, in_off, in_nets, out_off, out_nets, inp = _flat(nl)
+    nodes = sum(1 for c in nl.cells if c.kind != "DFF")
+    asap = np.zeros(max(nodes, 1), np.int32)
+    launch = np.zeros(max(nodes, 1), np.int32)
+    depth = np.zeros(1, np.int32)
+    inp_arr = np.array(inp or [0], np.int32)
+    _check(L.vsp_netlist_schedule(nl.net_count, len(nl.cells), _ptr(kinds), _ptr(ids),
+                                  _ptr(in_off), _ptr(in_nets), _ptr(out_off), _ptr(out_nets),
+                                  _ptr(inp_arr), len(inp), sms, _ptr(asap), _ptr(launch),
+                                  _ptr(depth)))
+    return asap[:nodes], launch[:nodes], int(depth[0])
+
+
 class Evaluator:
     """hvp::netlist::Evaluator<TfheBackend> on the GPU engine."""
 
@@ -305,21 +339,8 @@ class Evaluator:
         self.engine = engine
         self.n = engine.params.n
         L = _bind()
-        kinds = np.array([KIND_ID[c.kind] for c in nl.cells], np.int32)
-        ids = np.array([c.id for c in nl.cells], np.int32)
-        in_off = np.zeros(len(nl.cells) + 1, np.int32)
-        out_off = np.zeros(len(nl.cells) + 1, np.int32)
-        for i, c in enumerate(nl.cells):
-            in_off[i + 1] = in_off[i] + len(c.inputs)
-            out_off[i + 1] = out_off[i] + len(c.outputs)
-        in_nets = np.array([x for c in nl.cells for x in c.inputs] or [0], np.int32)
-        out_nets = np.array([x for c in nl.cells for x in c.outputs] or [0], np.int32)
-        self._input_index = {}
-        inp = []
-        for p in nl.inputs:
-            for b in p.bits:
-                self._input_index[b] = len(inp)
-                inp.append(b)
+        kinds, ids, in_off, in_nets, out_off, out_nets, inp = _flat(nl)
+        self._input_index = {b: i for i, b in enumerate(inp)}
         inp_arr = np.array(inp or [0], np.int32)
         h = L.vsp_netlist_create(engine.h, nl.net_count, len(nl.cells), _ptr(kinds), _ptr(ids),
                                  _ptr(in_off), _ptr(in_nets), _ptr(out_off), _ptr(out_nets),

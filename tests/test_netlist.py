@@ -97,3 +97,60 @@ def test_synthetic_ruby_shape():
     # JSON round trip (netlistToJson / parseNetlist)
     again = N.parse_netlist(N.netlist_to_json(nl))
     assert N.netlist_to_json(again) == N.netlist_to_json(nl)
+
+
+# ---- the engine's launch schedule (vsp_netlist_schedule: host-only C ABI, no device) ----
+
+def _tasks(kind):
+    return 2 if kind == "MUX" else 0 if kind in ("NOT", "ROM", "RAM", "CONST0", "CONST1") else 1
+
+
+def _waves(nodes, lv, sms):
+    t = {}
+    for i, c in enumerate(nodes):
+        t[lv[i]] = t.get(lv[i], 0) + _tasks(c.kind)
+    return sum(-(-x // sms) for x in t.values())
+
+
+def _check_schedule(nl, sms):
+    nodes = [c for c in nl.cells if c.kind != "DFF"]
+    asap, launch, depth = N.schedule(nl, sms)
+    assert len(asap) == len(nodes)
+    assert np.array_equal(asap, np.asarray(N.build_dag(nl)["level"]))  # buildDag semantics
+    assert np.all(launch >= asap) and depth == int(asap.max()) + 1 and launch.max() < depth
+    producer = {b: i for i, c in enumerate(nodes) for b in c.outputs}
+    for i, c in enumerate(nodes):
+        for b in c.inputs:
+            if b in producer:
+                assert launch[producer[b]] < launch[i]
+        if c.kind in ("ROM", "RAM", "CONST0", "CONST1"):
+            assert launch[i] == asap[i]
+    return _waves(nodes, asap, sms), _waves(nodes, launch, sms)
+
+
+@pytest.mark.parametrize("sms", [148, 132, 64])
+@pytest.mark.parametrize("seed", range(1, 9))
+def test_launch_schedule_properties(seed, sms):
+    """Level balancing never evaluates a gate before a producer or after a consumer, never
+    moves memory ports or constants, never deepens the cycle and never adds a latency
+    wave; on netlists with levels just over one wave it removes waves."""
+    rng = np.random.default_rng(seed)
+    nl = N.synthetic_netlist(seed=seed, scale=float(rng.uniform(0.05, 0.3)),
+                             levels=int(rng.integers(3, 8)), dffs=48, ram=(3, 4))
+    w_asap, w_launch = _check_schedule(nl, sms)
+    assert w_launch <= w_asap
+
+
+def test_launch_schedule_removes_waves():
+    """Netlists whose ASAP levels sit just above one wave of 148 SMs: the bench's cycle
+    netlist (one 149-task level: 34 -> 33 waves) and a small one (7 -> 5)."""
+    assert _check_schedule(N.synthetic_netlist(seed=1, levels=32), 148) == (34, 33)
+    small = N.synthetic_netlist(seed=3, scale=0.134, levels=4, dffs=48, ram=(3, 4))
+    assert _check_schedule(small, 148) == (7, 5)
+
+
+def test_launch_schedule_rejects_invalid_netlists():
+    nl = N.synthetic_netlist(seed=2, scale=0.02, levels=3, dffs=8, rom=False, ram=None)
+    nl.cells[-1].inputs = [nl.net_count + 5]  # dangling input
+    with pytest.raises(RuntimeError, match="dangling input net"):
+        N.schedule(nl, 148)
