@@ -303,8 +303,12 @@ int vsp_sm_count(vsp_ctx* ctx);
  *   "iks_gemm" 0|1: identity key switching as an INT8 tensor-core GEMM (default 1);
  *   "br_pair" 0|1: partial blind-rotation waves with two warps per task (default 1);
  *   "iks_split" k: split-K factor of the key-switch GEMM, k divides 24,576 into multiples
- *      of 16 (0 = automatic: 4 up to 512 key switches, else 2). */
+ *      of 16 (0 = automatic: 4 up to 512 key switches, else 2);
+ *   "backfill" 0|1: the netlist runner's write-bar backfill (default 1). */
 int vsp_set_option(vsp_ctx* ctx, const char* name, int64_t value);
+/* Reads an option back, or the statistic "bars_backfilled" (write-bar blind rotations the
+ * runner has run inside narrow levels since the context was created). */
+int vsp_get_option(vsp_ctx* ctx, const char* name, int64_t* value);
 
 /* Measured dense FP64 FMA throughput of `device` in TFLOP/s (the denominator of the
  * blind-rotation roofline; MEASURED_PEAKS.json carries no FP64 figure). */

@@ -83,6 +83,7 @@ def lib() -> ctypes.CDLL:
         L.vsp_br_plan.argtypes = [vp, sz, vp]
         L.vsp_sm_count.argtypes = [vp]
         L.vsp_set_option.argtypes = [vp, ctypes.c_char_p, ctypes.c_int64]
+        L.vsp_get_option.argtypes = [vp, ctypes.c_char_p, ctypes.POINTER(ctypes.c_int64)]
         L.vsp_fp64_peak_probe.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
         L.vsp_client_keygen.argtypes = [ctypes.POINTER(VspParams), u64, ctypes.c_int] + [vp] * 8
         L.vsp_client_keygen_dev.argtypes = [ctypes.POINTER(VspParams), u64, ctypes.c_int,
@@ -603,8 +604,14 @@ class Engine:
 
     def set_option(self, name: str, value: int):
         """Engine tuning option (vsp_set_option): "lat_tasks" (1|2), "ram_overlap",
-        "iks_gemm", "br_pair" (0|1), "iks_split" (split-K factor, 0 = automatic)."""
+        "iks_gemm", "br_pair", "backfill" (0|1), "iks_split" (split-K factor, 0 = automatic)."""
         _check(lib().vsp_set_option(self.h, name.encode(), int(value)))
+
+    def get_option(self, name: str) -> int:
+        """An option's value, or the statistic "bars_backfilled" (vsp_get_option)."""
+        v = ctypes.c_int64()
+        _check(lib().vsp_get_option(self.h, name.encode(), ctypes.byref(v)))
+        return int(v.value)
 
     def counters(self) -> dict:
         """OpCounters (counters.hpp:11-28)."""

@@ -443,7 +443,7 @@ void run_cycle_body(vsp_netlist* nl, cudaStream_t st)
         vsp_ctx* c;
         ~BarReset() { c->bar_total = c->bar_done = c->bar_cap = 0; }
     } bar_reset{c};
-    const bool backfill = c->p.fft && !sharded(c) && !c->defer_write_now;
+    const bool backfill = c->backfill && c->p.fft && !sharded(c) && !c->defer_write_now;
     auto spare_from = [&](int L) {
         int cap = 0;
         for (int l = L; l < nl->depth; l++)

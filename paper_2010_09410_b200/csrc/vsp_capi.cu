@@ -273,6 +273,8 @@ struct vsp_ctx {
     // planes, cuBLASLt handle, selector / product scratch; option "iks_gemm"
     bool iks_gemm = true;
     int iks_split = 0;  // option "iks_split": split-K factor of the key-switch GEMM (0: auto)
+    bool backfill = true;  // option "backfill": the runner's write-bar backfill
+    uint64_t bars_backfilled = 0;  // write-bar blind rotations run inside narrow levels (stat)
     // partial blind-rotation waves on br1024p_kernel (two warps per task); option "br_pair"
     bool br_pair = true;
     int8_t* d_k4t = nullptr;
@@ -1299,6 +1301,7 @@ void hom_gate_dev(vsp_ctx* c, const int32_t* kinds, const uint32_t* d_in, uint32
                                        d_trlwe + (size_t)pl.T * 2 * p.N1,
                                        (size_t)kbar * 2 * p.N1 * 4, cudaMemcpyDeviceToDevice, st));
         c->bar_done += kbar;
+        c->bars_backfilled += (uint64_t)kbar;
     }
     launch_iks(c, d_trlwe, d_gtask, d_glist + k1, Gl - k1, lx ? lx->vals : d_out, st, nullptr,
                false, lx ? lx->onet : nullptr);
@@ -3179,6 +3182,9 @@ int vsp_set_option(vsp_ctx* c, const char* name, int64_t value)
         else if (k == "br_pair") {
             c->br_pair = value != 0;
         }
+        else if (k == "backfill") {
+            c->backfill = value != 0;
+        }
         else if (k == "iks_split") {
             if (value != 0 && !iks_split_valid((int)value))
                 throw std::invalid_argument("iks_split must divide 24576 into multiples of 16");
@@ -3187,6 +3193,30 @@ int vsp_set_option(vsp_ctx* c, const char* name, int64_t value)
         else {
             throw std::invalid_argument("unknown option: " + k);
         }
+    });
+}
+
+int vsp_get_option(vsp_ctx* c, const char* name, int64_t* value)
+{
+    return guard([&] {
+        std::lock_guard<std::mutex> lk(c->mu);
+        const std::string k = name ? name : "";
+        if (k == "lat_tasks")
+            *value = c->lat_tasks;
+        else if (k == "ram_overlap")
+            *value = c->ram_overlap;
+        else if (k == "iks_gemm")
+            *value = c->iks_gemm;
+        else if (k == "br_pair")
+            *value = c->br_pair;
+        else if (k == "iks_split")
+            *value = c->iks_split;
+        else if (k == "backfill")
+            *value = c->backfill;
+        else if (k == "bars_backfilled")
+            *value = (int64_t)c->bars_backfilled;
+        else
+            throw std::invalid_argument("unknown option: " + k);
     });
 }
 

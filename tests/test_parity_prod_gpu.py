@@ -307,3 +307,45 @@ def test_runner_with_memory_ports_matches_reference_evaluator_n630(prod630):
                               dec(np.stack([rev.output("out", j) for j in range(16)])))
         assert np.array_equal(vsp.decrypt_ram(k, ev.ram(), v, w),
                               vsp.decrypt_ram(k, rev.get_ram(ram.shape), v, w))
+
+
+def test_write_bar_backfill_equals_inline_write_unit_n630(prod630):
+    """The runner's write-bar backfill (the RAM write unit's remainder blind rotations run in
+    the idle SMs of later narrow levels) at the bench's RAM geometry (v=8, w=16: 4,096
+    cells, three whole waves + a 544-cell remainder) gives the same DFF state, outputs and
+    RAM image, word for word, as the write unit run inline (backfill off) -- which the other
+    runner tests pin to the reference Evaluator."""
+    from paper_2010_09410_b200 import netlist as N
+    e, ref, k, p = prod630
+    nl = N.synthetic_netlist(seed=12, scale=0.1, levels=6, dffs=48, ram=(8, 16))
+    rng = np.random.default_rng(120)
+    v, w = 8, 16
+    words = [int(x) for x in rng.integers(0, 1 << w, 1 << v)]
+    ram = vsp.encrypt_ram(p, k, words_to_image(words, v, w), v, w, 121)
+    luts = vsp.encrypt_rom(p, k, rng.integers(0, 256, 512).astype(np.uint8), 122)
+    init = enc_bits(p, k, rng.integers(0, 2, 48), 123)
+    ins = [enc_bits(p, k, rng.integers(0, 2, len(nl.inputs[0].bits)), 124 + c) for c in range(2)]
+
+    def run(backfill):
+        e.set_option("backfill", backfill)
+        try:
+            ev = N.Evaluator(nl, e)
+            ev.set_ram(ram, v, w)
+            ev.set_rom(luts, 512)
+            ev.set_dff_state_raw(init)
+            before = e.get_option("bars_backfilled")
+            outs = []
+            for cts in ins:
+                for i, ct in enumerate(cts):
+                    ev.set_input("in", i, ct)
+                ev.run(1)
+                outs.append(np.stack([ev.output("out", j) for j in range(16)]))
+            return ev.dff_state(), np.stack(outs), ev.ram(), e.get_option("bars_backfilled") - before
+        finally:
+            e.set_option("backfill", 1)
+
+    dff_a, out_a, ram_a, bars_a = run(1)
+    dff_b, out_b, ram_b, bars_b = run(0)
+    assert bars_b == 0 and bars_a > 0, (bars_a, bars_b)
+    assert np.array_equal(dff_a, dff_b) and np.array_equal(out_a, out_b)
+    assert np.array_equal(ram_a, ram_b)
