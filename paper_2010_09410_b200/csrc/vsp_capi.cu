@@ -1994,7 +1994,7 @@ void vsp_destroy(vsp_ctx* c)
     for (DevBuf* b : {&c->tasks, &c->trlwe, &c->in, &c->out, &c->kinds, &c->gtask, &c->glist,
                       &c->acc2, &c->hv, &c->rows, &c->cbraw, &c->selraw, &c->selfd, &c->chains,
                       &c->layerA, &c->layerB, &c->ram, &c->aux, &c->aux2, &c->seidx, &c->pairs,
-                      &c->ramio, &c->romio, &c->cbraw2, &c->cbaddr})
+                      &c->ramio, &c->romio, &c->cbraw2, &c->cbaddr, &c->bar_lwe})
         b->release();
     for (void* q : {(void*)c->d_bk2fd, (void*)c->d_tv2[0], (void*)c->d_tv2[1]})
         if (q)
@@ -2734,7 +2734,7 @@ void vsp_netlist_destroy(vsp_netlist* nl)
     cudaSetDevice(nl->ctx->device);
     cudaStreamSynchronize(nl->ctx->stream);
     for (DevBuf* b : {&nl->values, &nl->dff, &nl->gin, &nl->gout, &nl->nets_buf, &nl->inputs_store,
-                      &nl->ram, &nl->rom})
+                      &nl->ram, &nl->rom, &nl->lvl_nets})
         b->release();
     delete nl;
 }
