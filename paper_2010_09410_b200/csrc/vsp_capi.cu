@@ -2633,7 +2633,7 @@ vsp_netlist* vsp_netlist_create(vsp_ctx* c, int32_t net_count, int32_t cells, co
         CallScope cs(c, c->stream);
         if (net_count < 0 || cells < 0 || n_inputs < 0)
             throw std::invalid_argument("netlist: negative size");
-        if (cells > 0 && (!kinds || !ids || !in_off || !out_off))
+        if (!in_off || !out_off || (cells > 0 && (!kinds || !ids)))
             throw std::invalid_argument("netlist: missing cell arrays");
         if (n_inputs > 0 && !input_nets)
             throw std::invalid_argument("netlist: missing input nets");
@@ -2698,7 +2698,7 @@ int vsp_netlist_schedule(int32_t net_count, int32_t cells, const int32_t* kinds,
     return guard([&] {
         if (net_count < 0 || cells < 0 || n_inputs < 0 || sms < 1)
             throw std::invalid_argument("netlist: negative size");
-        if (cells > 0 && (!kinds || !ids || !in_off || !out_off))
+        if (!in_off || !out_off || (cells > 0 && (!kinds || !ids)))
             throw std::invalid_argument("netlist: missing cell arrays");
         vsp_netlist nl;
         nl.nets = net_count;
