@@ -2649,6 +2649,8 @@ vsp_netlist* vsp_netlist_create(vsp_ctx* c, int32_t net_count, int32_t cells, co
                 throw std::invalid_argument("netlist: pin offsets must be non-decreasing");
         if (nl->in_off[0] != 0 || nl->out_off[0] != 0)
             throw std::invalid_argument("netlist: pin offsets must start at 0");
+        if ((nl->in_off[cells] > 0 && !in_nets) || (nl->out_off[cells] > 0 && !out_nets))
+            throw std::invalid_argument("netlist: missing pin arrays");
         nl->in_nets.assign(in_nets, in_nets + nl->in_off[cells]);
         nl->out_nets.assign(out_nets, out_nets + nl->out_off[cells]);
         nl->input_nets.assign(input_nets, input_nets + n_inputs);
@@ -2711,6 +2713,9 @@ int vsp_netlist_schedule(int32_t net_count, int32_t cells, const int32_t* kinds,
                 throw std::invalid_argument("netlist: pin offsets must be non-decreasing");
         if (nl.in_off[0] != 0 || nl.out_off[0] != 0)
             throw std::invalid_argument("netlist: pin offsets must start at 0");
+        if ((nl.in_off[cells] > 0 && !in_nets) || (nl.out_off[cells] > 0 && !out_nets) ||
+            (n_inputs > 0 && !input_nets))
+            throw std::invalid_argument("netlist: missing pin arrays");
         nl.in_nets.assign(in_nets, in_nets + nl.in_off[cells]);
         nl.out_nets.assign(out_nets, out_nets + nl.out_off[cells]);
         nl.input_nets.assign(input_nets, input_nets + n_inputs);
