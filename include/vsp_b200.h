@@ -304,7 +304,10 @@ int vsp_sm_count(vsp_ctx* ctx);
  *   "br_pair" 0|1: partial blind-rotation waves with two warps per task (default 1);
  *   "iks_split" k: split-K factor of the key-switch GEMM, k divides 24,576 into multiples
  *      of 16 (0 = automatic: 4 up to 512 key switches, else 2);
- *   "backfill" 0|1: the netlist runner's write-bar backfill (default 1). */
+ *   "backfill" 0|1: the netlist runner's write-bar backfill (default 1);
+ *   "graph" 0|1: the runner replays each clock cycle as a CUDA graph (one GPU, captured
+ *      after one eager cycle, recaptured when buffers, options, keys or the ROM / RAM
+ *      geometry change; default 1). */
 int vsp_set_option(vsp_ctx* ctx, const char* name, int64_t value);
 /* Reads an option back, or the statistic "bars_backfilled" (write-bar blind rotations the
  * runner has run inside narrow levels since the context was created). */

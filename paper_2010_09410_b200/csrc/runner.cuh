@@ -65,6 +65,12 @@ struct vsp_netlist {
     DevBuf lvl_nets;
     std::vector<size_t> lvl_off;
     std::vector<std::vector<int32_t>> lvl_kinds;
+    // the cycle as a CUDA graph (one GPU): captured after an eager warm-up cycle at the
+    // same buffer / option generations, replayed while they hold
+    cudaGraphExec_t gexec = nullptr;
+    uint64_t g_buf = ~0ull, g_opt = ~0ull, ready_buf = ~0ull, ready_opt = ~0ull;
+    uint64_t g_launches = 0, g_counters[5] = {0, 0, 0, 0, 0};
+    PinnedArena arena;
     std::vector<int> node_of_cell;
     int rom_cell = -1, ram_cell = -1, gmax = 0, depth = 0;
     // per level: gate cells (kinds 0..9) and memory ports
@@ -336,9 +342,7 @@ std::vector<uint32_t> trivial_tlwe(uint32_t n, bool m)
 void upload_ints(vsp_ctx* c, DevBuf& buf, const std::vector<int>& v, cudaStream_t st)
 {
     int* d = buf.as<int>(std::max<size_t>(v.size(), 1));
-    if (!v.empty())
-        VSP_CUDA_CHECK(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-    (void)c;
+    h2d(c, d, v.data(), v.size() * sizeof(int), st);
 }
 
 // A ROM port and a RAM port in the same level: their address circuit bootstraps (v_rom + v

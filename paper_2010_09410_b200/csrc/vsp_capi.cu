@@ -7,6 +7,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -59,6 +60,10 @@ int guard(F&& f)
     }
 }
 
+// Bumped whenever any device scratch buffer is (re)allocated or freed: a captured CUDA graph
+// (the netlist runner's cycle) is valid only while the buffers it names stay put.
+std::atomic<uint64_t> g_buf_gen{0};
+
 struct DevBuf {
     void* p = nullptr;
     size_t cap = 0;
@@ -71,6 +76,7 @@ struct DevBuf {
             cap = 0;
             VSP_CUDA_CHECK(cudaMalloc(&p, std::max<size_t>(bytes, 256)));
             cap = std::max<size_t>(bytes, 256);
+            g_buf_gen++;
         }
         return p;
     }
@@ -81,10 +87,43 @@ struct DevBuf {
     }
     void release()
     {
-        if (p)
+        if (p) {
             cudaFree(p);
+            g_buf_gen++;
+        }
         p = nullptr;
         cap = 0;
+    }
+};
+
+// Pinned host arena for the small host->device uploads of a CUDA-graph capture: a captured
+// memcpy node reads its host source at every replay, so the bytes are copied here (pinned,
+// alive as long as the graph) instead of coming from a transient pageable vector.
+struct PinnedArena {
+    std::vector<std::pair<void*, size_t>> blocks;  // (pointer, capacity)
+    size_t block = 0, used = 0;
+    void* put(const void* src, size_t bytes)
+    {
+        const size_t need = (bytes + 255) / 256 * 256;
+        if (blocks.empty() || used + need > blocks[block].second) {
+            const size_t cap = std::max<size_t>(need, 1u << 20);
+            void* p = nullptr;
+            VSP_CUDA_CHECK(cudaHostAlloc(&p, cap, cudaHostAllocDefault));
+            blocks.emplace_back(p, cap);
+            block = blocks.size() - 1;
+            used = 0;
+        }
+        void* dst = static_cast<uint8_t*>(blocks[block].first) + used;
+        memcpy(dst, src, bytes);
+        used += need;
+        return dst;
+    }
+    void release()
+    {
+        for (auto& b : blocks)
+            cudaFreeHost(b.first);
+        blocks.clear();
+        block = used = 0;
     }
 };
 
@@ -216,6 +255,11 @@ struct vsp_ctx {
         pairs, ramio, romio, cbraw2, cbaddr;
     uint64_t counters[5] = {0, 0, 0, 0, 0};
     uint64_t launches = 0;
+    // CUDA-graph capture of a runner cycle: h2d() stages uploads in this arena while set;
+    // opt_gen changes with every option / key upload (a captured graph bakes them in)
+    PinnedArena* cap_arena = nullptr;
+    uint64_t opt_gen = 0;
+    bool graph = true;  // option "graph": replay each netlist's cycle as a CUDA graph
     // multi-GPU (multi.cuh): NCCL communicator over the ranks, level slices staged here
     void* comm = nullptr;  // ncclComm_t
     int rank = 0, world = 1;
@@ -375,6 +419,16 @@ struct CallScope {
         }
     }
 };
+
+// Host -> device upload on `st`; while a runner cycle is being captured into a CUDA graph
+// the bytes are staged in the capture's pinned arena first (see PinnedArena).
+void h2d(vsp_ctx* c, void* dst, const void* src, size_t bytes, cudaStream_t st)
+{
+    if (!bytes)
+        return;
+    const void* s = c->cap_arena ? c->cap_arena->put(src, bytes) : src;
+    VSP_CUDA_CHECK(cudaMemcpyAsync(dst, s, bytes, cudaMemcpyHostToDevice, st));
+}
 
 int lat_tasks(const vsp_ctx* c)
 {
@@ -1185,12 +1239,10 @@ void hom_gate_dev(vsp_ctx* c, const int32_t* kinds, const uint32_t* d_in, uint32
     int* d_kinds = c->kinds.as<int>(G);
     int2* d_gtask = c->gtask.as<int2>(G);
     int* d_glist = c->glist.as<int>(std::max<size_t>(pl.glist.size(), 1));
-    VSP_CUDA_CHECK(cudaMemcpyAsync(d_kinds, kinds, G * sizeof(int), cudaMemcpyHostToDevice, st));
-    VSP_CUDA_CHECK(cudaMemcpyAsync(d_gtask, pl.gtask.data(), G * sizeof(int2),
-                                   cudaMemcpyHostToDevice, st));
+    h2d(c, d_kinds, kinds, G * sizeof(int), st);
+    h2d(c, d_gtask, pl.gtask.data(), G * sizeof(int2), st);
     if (!pl.glist.empty())
-        VSP_CUDA_CHECK(cudaMemcpyAsync(d_glist, pl.glist.data(), pl.glist.size() * sizeof(int),
-                                       cudaMemcpyHostToDevice, st));
+        h2d(c, d_glist, pl.glist.data(), pl.glist.size() * sizeof(int), st);
     // write-bar backfill (runner only: no host I/O): deferred RAM-cell blind rotations in
     // this level's idle SMs
     const int kbar = io ? 0 : bar_take(c, pl.T);
@@ -1360,9 +1412,9 @@ void cb_batch(vsp_ctx* c, const uint32_t* d_lwe, int C, uint32_t* d_out, cudaStr
         }
     uint64_t* d_hv = c->hv.as<uint64_t>(T2);
     int* d_rows = c->rows.as<int>(2 * (size_t)T2);
-    VSP_CUDA_CHECK(cudaMemcpyAsync(d_hv, hv.data(), T2 * 8, cudaMemcpyHostToDevice, st));
-    VSP_CUDA_CHECK(cudaMemcpyAsync(d_rows, rowA.data(), T2 * 4, cudaMemcpyHostToDevice, st));
-    VSP_CUDA_CHECK(cudaMemcpyAsync(d_rows + T2, rowB.data(), T2 * 4, cudaMemcpyHostToDevice, st));
+    h2d(c, d_hv, hv.data(), T2 * 8, st);
+    h2d(c, d_rows, rowA.data(), T2 * 4, st);
+    h2d(c, d_rows + T2, rowB.data(), T2 * 4, st);
     if (p.fft) {
         timed(c, "br2", st, [&] {
             launch_br2(c, d_lwe, C, d_hv, T2, d_acc2, st);
@@ -1441,8 +1493,7 @@ void run_chains(vsp_ctx* c, const std::vector<ChainTask>& tasks, cudaStream_t st
         return;
     const Params& p = c->p;
     ChainTask* d = c->chains.as<ChainTask>(tasks.size());
-    VSP_CUDA_CHECK(cudaMemcpyAsync(d, tasks.data(), tasks.size() * sizeof(ChainTask),
-                                   cudaMemcpyHostToDevice, st));
+    h2d(c, d, tasks.data(), tasks.size() * sizeof(ChainTask), st);
     const int T = (int)tasks.size();
     if (p.fft) {
         for (const auto& t : tasks)
@@ -1494,12 +1545,12 @@ void iks_of_trlwes(vsp_ctx* c, const uint32_t* d_trlwe, int count, const int* se
     }
     int2* d_gt = c->gtask.as<int2>(count);
     int* d_gl = c->glist.as<int>(count);
-    VSP_CUDA_CHECK(cudaMemcpyAsync(d_gt, gt.data(), count * sizeof(int2), cudaMemcpyHostToDevice, st));
-    VSP_CUDA_CHECK(cudaMemcpyAsync(d_gl, gl.data(), count * sizeof(int), cudaMemcpyHostToDevice, st));
+    h2d(c, d_gt, gt.data(), count * sizeof(int2), st);
+    h2d(c, d_gl, gl.data(), count * sizeof(int), st);
     int* d_se = nullptr;
     if (se) {
         d_se = c->seidx.as<int>(count);
-        VSP_CUDA_CHECK(cudaMemcpyAsync(d_se, se, count * sizeof(int), cudaMemcpyHostToDevice, st));
+        h2d(c, d_se, se, count * sizeof(int), st);
     }
     launch_iks(c, d_trlwe, d_gt, d_gl, count, d_out, st, d_se);
 }
@@ -1553,7 +1604,7 @@ void ram_control_unit_dev(vsp_ctx* c, const uint32_t* read, int w, const uint32_
     for (int j = 0; j < w; j++)
         pr[j] = make_int2(2 * j, 2 * j + 1);
     int2* d_pr = c->pairs.as<int2>(w);
-    VSP_CUDA_CHECK(cudaMemcpyAsync(d_pr, pr.data(), w * sizeof(int2), cudaMemcpyHostToDevice, st));
+    h2d(c, d_pr, pr.data(), w * sizeof(int2), st);
     trlwe_sum_mu_kernel<<<w, 256, 0, st>>>(mux_tr, d_pr, controlled, w, (int)p.N1);
     VSP_CUDA_CHECK(cudaGetLastError());
     c->launches++;
@@ -1598,8 +1649,8 @@ void ram_write_unit_dev(vsp_ctx* c, uint32_t* d_ram, int v, int w, const uint32_
         }
         int2* d_gt = c->wgt.as<int2>(T);
         int* d_gl = c->wgl.as<int>(T);
-        VSP_CUDA_CHECK(cudaMemcpyAsync(d_gt, gt.data(), T * sizeof(int2), cudaMemcpyHostToDevice, ws));
-        VSP_CUDA_CHECK(cudaMemcpyAsync(d_gl, gl.data(), T * sizeof(int), cudaMemcpyHostToDevice, ws));
+        h2d(c, d_gt, gt.data(), T * sizeof(int2), ws);
+        h2d(c, d_gl, gl.data(), T * sizeof(int), ws);
         launch_iks(c, chain_out, d_gt, d_gl, T, wl, ws);
         const int per_launch = 8 * c->w_ctas;
         const int launches = (T + per_launch - 1) / per_launch;
@@ -1635,8 +1686,8 @@ void ram_write_unit_dev(vsp_ctx* c, uint32_t* d_ram, int v, int w, const uint32_
         }
         int2* d_gt = c->gtask.as<int2>(full);
         int* d_gl = c->glist.as<int>(full);
-        VSP_CUDA_CHECK(cudaMemcpyAsync(d_gt, gt.data(), full * sizeof(int2), cudaMemcpyHostToDevice, st));
-        VSP_CUDA_CHECK(cudaMemcpyAsync(d_gl, gl.data(), full * sizeof(int), cudaMemcpyHostToDevice, st));
+        h2d(c, d_gt, gt.data(), full * sizeof(int2), st);
+        h2d(c, d_gl, gl.data(), full * sizeof(int), st);
         // identity maps relative to each part's base pointers
         launch_iks(c, chain_out + (size_t)full * cw, d_gt, d_gl, rem, lw + (size_t)full * n1, st);
         c->ensure_aux_stream();
@@ -1815,9 +1866,9 @@ void rom_read_dev(vsp_ctx* c, const uint32_t* d_luts, int nluts, uint32_t depth_
     int2* d_gt = c->gtask.as<int2>(32);
     int* d_gl = c->glist.as<int>(32);
     int* d_se = c->seidx.as<int>(32);
-    VSP_CUDA_CHECK(cudaMemcpyAsync(d_gt, gt.data(), 32 * sizeof(int2), cudaMemcpyHostToDevice, st));
-    VSP_CUDA_CHECK(cudaMemcpyAsync(d_gl, gl.data(), 32 * sizeof(int), cudaMemcpyHostToDevice, st));
-    VSP_CUDA_CHECK(cudaMemcpyAsync(d_se, se, 32 * sizeof(int), cudaMemcpyHostToDevice, st));
+    h2d(c, d_gt, gt.data(), 32 * sizeof(int2), st);
+    h2d(c, d_gl, gl.data(), 32 * sizeof(int), st);
+    h2d(c, d_se, se, 32 * sizeof(int), st);
     launch_iks(c, acc, d_gt, d_gl, 32, d_out, st, d_se);
 }
 
@@ -2045,6 +2096,7 @@ int vsp_upload_keys(vsp_ctx* c, const uint32_t* bk1, const uint32_t* ksk, const 
     return guard([&] {
         CallScope cs(c, c->stream);
         VSP_CUDA_CHECK(cudaStreamSynchronize(c->stream));  // keys may be in use
+        c->opt_gen++;  // key buffers move: captured cycle graphs are stale
         const Params& p = c->p;
         if (!bk1 || !ksk)
             throw std::invalid_argument("bk1 and ksk are required");
@@ -2738,6 +2790,9 @@ void vsp_netlist_destroy(vsp_netlist* nl)
         return;
     cudaSetDevice(nl->ctx->device);
     cudaStreamSynchronize(nl->ctx->stream);
+    if (nl->gexec)
+        cudaGraphExecDestroy(nl->gexec);
+    nl->arena.release();
     for (DevBuf* b : {&nl->values, &nl->dff, &nl->gin, &nl->gout, &nl->nets_buf, &nl->inputs_store,
                       &nl->ram, &nl->rom, &nl->lvl_nets})
         b->release();
@@ -2841,6 +2896,7 @@ int vsp_netlist_set_rom(vsp_netlist* nl, uint32_t depth_bytes, const uint32_t* l
         nl->rom_depth = depth_bytes;
         nl->rom_nluts = nluts;
         nl->has_rom = true;
+        nl->g_buf = nl->ready_buf = ~0ull;  // the ROM geometry is baked into a captured cycle
     });
 }
 
@@ -2860,6 +2916,7 @@ int vsp_netlist_ram(vsp_netlist* nl, uint32_t v, uint32_t w, uint32_t* get, cons
             nl->ram_v = v;
             nl->ram_w = w;
             nl->has_ram = true;
+            nl->g_buf = nl->ready_buf = ~0ull;  // RAM geometry baked into a captured cycle
         }
         if (get) {
             if (!nl->has_ram || v != nl->ram_v || w != nl->ram_w)
@@ -2873,6 +2930,99 @@ int vsp_netlist_ram(vsp_netlist* nl, uint32_t v, uint32_t w, uint32_t* get, cons
 
 // Evaluator::run (engine.hpp:238-247).  stats (optional, 4 per cycle): evaluated cells,
 // gMax, depth, seconds (device time of the cycle).
+namespace {
+
+// One cycle through its CUDA graph (runner.cuh vsp_netlist::gexec): replay when the graph
+// was captured at the current buffer and option generations; otherwise run eagerly once
+// (buffers sized, GEMM algorithms chosen), and capture + replay on the next cycle.
+bool graph_ok(const vsp_netlist* nl)
+{
+    const vsp_ctx* c = nl->ctx;
+    static const bool off = getenv("VSP_GRAPH") && atoi(getenv("VSP_GRAPH")) == 0;
+    return !off && c->graph && c->p.fft && !sharded(c) && !c->ram_overlap && !c->profiling;
+}
+
+void graph_drop(vsp_netlist* nl)
+{
+    if (nl->gexec) {
+        VSP_CUDA_CHECK(cudaStreamSynchronize(nl->ctx->stream));  // a replay may still read the arena
+        cudaGraphExecDestroy(nl->gexec);
+        nl->gexec = nullptr;
+    }
+    nl->arena.release();
+}
+
+void run_cycle_graph(vsp_netlist* nl)
+{
+    vsp_ctx* c = nl->ctx;
+    cudaStream_t st = c->stream;
+    const uint64_t gb = g_buf_gen.load(), go = c->opt_gen;
+    auto replay = [&] {
+        VSP_CUDA_CHECK(cudaGraphLaunch(nl->gexec, st));
+        c->launches += nl->g_launches;
+        for (int k = 0; k < 5; k++)
+            c->counters[k] += nl->g_counters[k];
+    };
+    if (nl->gexec && nl->g_buf == gb && nl->g_opt == go) {
+        replay();
+        return;
+    }
+    if (nl->ready_buf != gb || nl->ready_opt != go) {
+        run_cycle(nl, st);
+        nl->ready_buf = g_buf_gen.load();
+        nl->ready_opt = c->opt_gen;
+        return;
+    }
+    graph_drop(nl);
+    const uint64_t l0 = c->launches;
+    uint64_t k0[5];
+    for (int k = 0; k < 5; k++)
+        k0[k] = c->counters[k];
+    cudaGraph_t g = nullptr;
+    c->cap_arena = &nl->arena;
+    VSP_CUDA_CHECK(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+    try {
+        run_cycle_body(nl, st);
+    }
+    catch (...) {
+        cudaStreamEndCapture(st, &g);
+        if (g)
+            cudaGraphDestroy(g);
+        c->cap_arena = nullptr;
+        c->launches = l0;
+        for (int k = 0; k < 5; k++)
+            c->counters[k] = k0[k];
+        throw;
+    }
+    c->cap_arena = nullptr;
+    VSP_CUDA_CHECK(cudaStreamEndCapture(st, &g));
+    // the capture ran no kernel: its host-side counts become the per-replay counts
+    nl->g_launches = c->launches - l0;
+    c->launches = l0;
+    for (int k = 0; k < 5; k++) {
+        nl->g_counters[k] = c->counters[k] - k0[k];
+        c->counters[k] = k0[k];
+    }
+    if (g_buf_gen.load() != gb) {  // a buffer moved while capturing: run this cycle eagerly
+        cudaGraphDestroy(g);
+        nl->arena.release();
+        run_cycle(nl, st);
+        nl->ready_buf = g_buf_gen.load();
+        return;
+    }
+    const cudaError_t e = cudaGraphInstantiate(&nl->gexec, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) {
+        nl->gexec = nullptr;
+        throw std::runtime_error(std::string("CUDA graph instantiation: ") + cudaGetErrorString(e));
+    }
+    nl->g_buf = gb;
+    nl->g_opt = go;
+    replay();
+}
+
+}  // namespace
+
 int vsp_netlist_run(vsp_netlist* nl, uint64_t cycles, double* stats)
 {
     return guard([&] {
@@ -2883,7 +3033,10 @@ int vsp_netlist_run(vsp_netlist* nl, uint64_t cycles, double* stats)
         VSP_CUDA_CHECK(cudaEventCreate(&b));
         for (uint64_t i = 0; i < cycles; i++) {
             VSP_CUDA_CHECK(cudaEventRecord(a, c->stream));
-            run_cycle(nl, c->stream);
+            if (graph_ok(nl))
+                run_cycle_graph(nl);
+            else
+                run_cycle(nl, c->stream);
             if (i + 1 == cycles)  // a deferred write unit finishes inside the last cycle
                 c->ram_join(c->stream);
             VSP_CUDA_CHECK(cudaEventRecord(b, c->stream));
@@ -2977,6 +3130,7 @@ int vsp_netlist_snapshot_load(vsp_netlist* nl, const char* param_name, const uin
         CallScope cs(c, c->stream);
         c->ram_join(c->stream);
         VSP_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+        nl->g_buf = nl->ready_buf = ~0ull;
         snapshot_load(nl, param_name ? param_name : "", in, len);
     });
 }
@@ -3173,6 +3327,7 @@ int vsp_set_option(vsp_ctx* c, const char* name, int64_t value)
     return guard([&] {
         CallScope cs(c, c->stream);
         const std::string k = name ? name : "";
+        c->opt_gen++;  // a captured cycle graph bakes the options in
         if (k == "lat_tasks") {
             if (value != 1 && value != 2)
                 throw std::invalid_argument("lat_tasks must be 1 or 2");
@@ -3189,6 +3344,9 @@ int vsp_set_option(vsp_ctx* c, const char* name, int64_t value)
         }
         else if (k == "backfill") {
             c->backfill = value != 0;
+        }
+        else if (k == "graph") {
+            c->graph = value != 0;
         }
         else if (k == "iks_split") {
             if (value != 0 && !iks_split_valid((int)value))
@@ -3218,6 +3376,8 @@ int vsp_get_option(vsp_ctx* c, const char* name, int64_t* value)
             *value = c->iks_split;
         else if (k == "backfill")
             *value = c->backfill;
+        else if (k == "graph")
+            *value = c->graph;
         else if (k == "bars_backfilled")
             *value = (int64_t)c->bars_backfilled;
         else

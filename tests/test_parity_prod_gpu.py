@@ -349,3 +349,50 @@ def test_write_bar_backfill_equals_inline_write_unit_n630(prod630):
     assert bars_b == 0 and bars_a > 0, (bars_a, bars_b)
     assert np.array_equal(dff_a, dff_b) and np.array_equal(out_a, out_b)
     assert np.array_equal(ram_a, ram_b)
+
+
+def test_cycle_graph_replay_equals_eager_n630(prod630):
+    """The runner's cycle as a CUDA graph (captured after one eager cycle, then replayed)
+    gives the same DFF state, outputs and RAM image, word for word, every cycle, as eager
+    cycles; the op counters and kernel-launch counts per cycle agree too, and a rebound ROM
+    forces a new capture."""
+    from paper_2010_09410_b200 import netlist as N
+    e, ref, k, p = prod630
+    nl = N.synthetic_netlist(seed=14, scale=0.06, levels=5, dffs=40, ram=(4, 8))
+    rng = np.random.default_rng(140)
+    v, w = 4, 8
+    ram = vsp.encrypt_ram(p, k, words_to_image([int(x) for x in rng.integers(0, 256, 16)], v, w),
+                          v, w, 141)
+    luts = vsp.encrypt_rom(p, k, rng.integers(0, 256, 512).astype(np.uint8), 142)
+    luts2 = vsp.encrypt_rom(p, k, rng.integers(0, 256, 512).astype(np.uint8), 143)
+    init = enc_bits(p, k, rng.integers(0, 2, 40), 144)
+    ins = [enc_bits(p, k, rng.integers(0, 2, len(nl.inputs[0].bits)), 145 + c) for c in range(5)]
+
+    def run(graph):
+        e.set_option("graph", graph)
+        try:
+            ev = N.Evaluator(nl, e)
+            ev.set_ram(ram, v, w)
+            ev.set_rom(luts, 512)
+            ev.set_dff_state_raw(init)
+            res = []
+            for cyc, cts in enumerate(ins):
+                if cyc == 3:
+                    ev.set_rom(luts2, 512)
+                for i, ct in enumerate(cts):
+                    ev.set_input("in", i, ct)
+                e.counters_reset()
+                l0 = e.kernel_launches()
+                ev.run(1)
+                res.append((ev.dff_state(), np.stack([ev.output("out", j) for j in range(16)]),
+                            ev.ram(), e.counters(), e.kernel_launches() - l0))
+            ev.close()
+            return res
+        finally:
+            e.set_option("graph", 1)
+
+    eager, graph = run(0), run(1)
+    for cyc, (a, b) in enumerate(zip(eager, graph)):
+        for x, y in zip(a[:3], b[:3]):
+            assert np.array_equal(x, y), f"cycle {cyc}"
+        assert a[3] == b[3] and a[4] == b[4], (cyc, a[3:], b[3:])
