@@ -2939,7 +2939,9 @@ bool graph_ok(const vsp_netlist* nl)
 {
     const vsp_ctx* c = nl->ctx;
     static const bool off = getenv("VSP_GRAPH") && atoi(getenv("VSP_GRAPH")) == 0;
-    return !off && c->graph && c->p.fft && !sharded(c) && !c->ram_overlap && !c->profiling;
+    // (the tensor-free key-switch schedules fork work onto side streams: kept eager)
+    return !off && c->graph && c->p.fft && c->iks_gemm && !sharded(c) && !c->ram_overlap &&
+           !c->profiling;
 }
 
 void graph_drop(vsp_netlist* nl)
