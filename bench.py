@@ -441,8 +441,10 @@ def measure_gates(cx: Ctx) -> dict | None:
                    "gates_per_gpu": G, "n": p.n, "N": p.N1, "l": p.l1, "Bg_bits": p.Bg1Bits,
                    "ks": f"2^{p.ksBaseBits} x {p.ksLen}", "l2": "flushed (512 MiB write) "
                    "between timed steps",
-                   "parallelism": f"level sharded over {world} GPU(s), outputs all-gathered "
-                                  "over NCCL" if world > 1 else "1 GPU"},
+                   "parallelism": (f"level sharded over {world} GPU(s), outputs all-gathered "
+                                   + ("through the engine's host-callback exchange over gloo "
+                                      "(flow check; ranks may share a GPU)" if cx.gloo else
+                                      "over NCCL")) if world > 1 else "1 GPU"},
         "outputs_decrypt_correct": correct,
         "gpu_launches": int(launches),
         "e2e": e2e,
